@@ -1,0 +1,244 @@
+// extern "C" boundary of libedak.so (declared in include/edak.h).
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace edak {
+
+static thread_local char g_err[512] = "";
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const char* msg) {
+  std::strncpy(g_err, msg, sizeof(g_err) - 1);
+  g_err[sizeof(g_err) - 1] = 0;
+}
+void count_launch(int k) { g_launches += k; }
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    std::snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+    return EDAK_ECUDA;
+  }
+  return EDAK_OK;
+}
+
+// launchers (l96.cu, circ.cu, blas.cu, small.cu, pcg.cu)
+int launch_tl(const edak_problem*, const double*, double*, int, const int32_t*, cudaStream_t);
+int launch_ad(const edak_problem*, const double*, double*, int, const int32_t*, cudaStream_t);
+int launch_integrate(int, int, double, double, const double*, int, double*, int64_t, double*, int64_t,
+                     cudaStream_t);
+int launch_observe(const double*, int64_t, int, const int32_t*, int, const int32_t*, int, int, double*,
+                   cudaStream_t);
+int launch_circ(const edak_problem*, const double*, double*, int, double, const double*, cudaStream_t);
+int64_t gemm_tn_partials(int, int, int64_t);
+int launch_gemm_tn(const double*, int64_t, const double*, int64_t, double*, int, int, int, int64_t, double*,
+                   cudaStream_t);
+int launch_gemm_nn(const double*, int64_t, const double*, int, const double*, const double*, int64_t, double,
+                   double*, int64_t, int64_t, int, int, cudaStream_t);
+int launch_col_dots(int, int, const double*, const double*, double*, cudaStream_t);
+int launch_potrf_shifted(const double*, int, double*, int, double, double*, int32_t*, cudaStream_t);
+int launch_trinv_upper(const double*, int, double*, cudaStream_t);
+int64_t svd_work_doubles(int, int);
+int launch_svd_jacobi(const double*, int, int, double*, double*, double*, double*, cudaStream_t);
+int launch_pcg_init(int, int, const double*, const double*, double*, double*, double*, double*, double*, int,
+                    int32_t*, int32_t*, cudaStream_t);
+int launch_pcg_alpha(int, int, const double*, const double*, double*, double*, const double*, int32_t*, int32_t*,
+                     int, int, const double*, double*, const double*, double, double*, int, cudaStream_t);
+int launch_pcg_beta(int, int, const double*, const double*, double*, double*, double, double*, int, int32_t*,
+                    int32_t*, int, cudaStream_t);
+int launch_pcg_cost0(int, int, const double*, double*, double, double*, int, cudaStream_t);
+int launch_cost(int, int, int, const double*, const double*, const double*, double, double*, cudaStream_t);
+
+static bool bad_problem(const edak_problem* P) {
+  if (!P || P->n < 8 || P->n_steps < 1 || !P->gpos || !P->tpos || !P->taps || P->ntaps < 1 || P->G < 0 ||
+      P->T < 0) {
+    set_error("invalid edak_problem");
+    return true;
+  }
+  if ((P->stage_mode == 0 && !P->states) || (P->stage_mode == 1 && !P->stages)) {
+    set_error("edak_problem: trajectory buffer missing for stage_mode");
+    return true;
+  }
+  return false;
+}
+
+}  // namespace edak
+
+using namespace edak;
+
+extern "C" {
+
+const char* edak_version(void) { return "edak 0.1 (sm_100a)"; }
+const char* edak_last_error(void) { return g_err; }
+int64_t edak_launch_count(void) { return g_launches.load(); }
+
+int edak_integrate(int n, int n_steps, double dt, double forcing, const double* x0, int ncols, double* states_out,
+                   int64_t out_stride, double* stages_out, int64_t stg_stride, void* stream) {
+  if (n < 8 || n_steps < 0 || ncols < 0 || !x0 || !states_out || out_stride < (int64_t)(n_steps + 1) * n) {
+    set_error("edak_integrate: bad arguments");
+    return EDAK_EINVAL;
+  }
+  if (ncols == 0) return EDAK_OK;
+  return launch_integrate(n, n_steps, dt, forcing, x0, ncols, states_out, out_stride, stages_out, stg_stride,
+                          as_stream(stream));
+}
+
+int edak_observe(const double* states, int64_t traj_stride, int n, const int32_t* grid, int G, const int32_t* times,
+                 int T, int ncols, double* y, void* stream) {
+  if (!states || !grid || !times || !y || n < 1) return EDAK_EINVAL;
+  if (ncols == 0 || G * T == 0) return EDAK_OK;
+  return launch_observe(states, traj_stride, n, grid, G, times, T, ncols, y, as_stream(stream));
+}
+
+int edak_circ_apply(const edak_problem* P, const double* in, double* out, int ncols, void* stream) {
+  if (!P || !P->taps || !in || !out) return EDAK_EINVAL;
+  if (ncols == 0) return EDAK_OK;
+  return launch_circ(P, in, out, ncols, 0.0, nullptr, as_stream(stream));
+}
+
+int edak_tl_sweep(const edak_problem* P, const double* v0, double* obs, int ncols, const int32_t* col_traj,
+                  void* stream) {
+  if (bad_problem(P) || !v0 || !obs) return EDAK_EINVAL;
+  if (ncols == 0) return EDAK_OK;
+  return launch_tl(P, v0, obs, ncols, col_traj, as_stream(stream));
+}
+
+int edak_ad_sweep(const edak_problem* P, const double* forcing, double* g, int ncols, const int32_t* col_traj,
+                  void* stream) {
+  if (bad_problem(P) || !forcing || !g) return EDAK_EINVAL;
+  if (ncols == 0) return EDAK_OK;
+  return launch_ad(P, forcing, g, ncols, col_traj, as_stream(stream));
+}
+
+int64_t edak_work_doubles(const edak_problem* P, int ncols) {
+  if (!P) return -1;
+  return (int64_t)ncols * (2 * (int64_t)P->n + (int64_t)P->G * P->T);
+}
+
+int edak_hessian_block(const edak_problem* P, const double* z, double* az, int ncols, const int32_t* col_traj,
+                       double ident, double* work, double* obs_out, void* stream) {
+  if (bad_problem(P) || !z || !az || !work) return EDAK_EINVAL;
+  if (ncols == 0) return EDAK_OK;
+  cudaStream_t st = as_stream(stream);
+  const int64_t n = P->n, p = (int64_t)P->G * P->T;
+  double* v0 = work;
+  double* obs = obs_out ? obs_out : work + ncols * n;
+  double* g = work + ncols * (n + p);
+  int rc;
+  // A z = U_B^T G^T R^-1 G U_B z (assim.py:66-68); I + A (assim.py:70-72)
+  if ((rc = launch_circ(P, z, v0, ncols, 0.0, nullptr, st))) return rc;
+  if ((rc = launch_tl(P, v0, obs, ncols, col_traj, st))) return rc;
+  if ((rc = launch_ad(P, obs, g, ncols, col_traj, st))) return rc;
+  return launch_circ(P, g, az, ncols, ident, ident != 0.0 ? z : nullptr, st);
+}
+
+int edak_rhs(const edak_problem* P, const double* innov, double* b, int ncols, const int32_t* col_traj, double* work,
+             void* stream) {
+  if (bad_problem(P) || !innov || !b || !work) return EDAK_EINVAL;
+  if (ncols == 0) return EDAK_OK;
+  cudaStream_t st = as_stream(stream);
+  int rc;
+  if ((rc = launch_ad(P, innov, work, ncols, col_traj, st))) return rc;
+  return launch_circ(P, work, b, ncols, 0.0, nullptr, st);
+}
+
+int edak_cost(const edak_problem* P, const double* z, const double* innov, double* J, int ncols,
+              const int32_t* col_traj, double* work, void* stream) {
+  if (bad_problem(P) || !z || !innov || !J || !work) return EDAK_EINVAL;
+  if (ncols == 0) return EDAK_OK;
+  cudaStream_t st = as_stream(stream);
+  const int64_t n = P->n;
+  const int p = P->G * P->T;
+  double* v0 = work;
+  double* obs = work + ncols * n;
+  int rc;
+  if ((rc = launch_circ(P, z, v0, ncols, 0.0, nullptr, st))) return rc;
+  if ((rc = launch_tl(P, v0, obs, ncols, col_traj, st))) return rc;
+  return launch_cost(P->n, p, ncols, z, obs, innov, P->sigma2, J, st);
+}
+
+int64_t edak_gemm_tn_partials(int m, int nb, int64_t K) { return gemm_tn_partials(m, nb, K); }
+
+int edak_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int ldc, int m, int nb,
+                 int64_t K, double* partial, void* stream) {
+  if (!A || !B || !C || !partial || m < 1 || nb < 1 || K < 1) return EDAK_EINVAL;
+  return launch_gemm_tn(A, lda, B, ldb, C, ldc, m, nb, K, partial, as_stream(stream));
+}
+
+int edak_gemm_nn(const double* A, int64_t lda, const double* B, int ldb, const double* bscale, const double* Cin,
+                 int64_t ldc, double beta, double* D, int64_t ldd, int64_t M, int N, int kk, void* stream) {
+  if (!A || !B || !D || M < 1 || N < 1 || kk < 1) return EDAK_EINVAL;
+  return launch_gemm_nn(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M, N, kk, as_stream(stream));
+}
+
+int edak_potrf_shifted(const double* W, int l, double* C, int mode, double scale, double* nu_out, int32_t* info,
+                       void* stream) {
+  if (!W || !C || !nu_out || !info || l < 1) return EDAK_EINVAL;
+  return launch_potrf_shifted(W, l, C, mode, scale, nu_out, info, as_stream(stream));
+}
+
+int edak_trinv_upper(const double* R, int l, double* Rinv, void* stream) {
+  if (!R || !Rinv || l < 1) return EDAK_EINVAL;
+  return launch_trinv_upper(R, l, Rinv, as_stream(stream));
+}
+
+int64_t edak_svd_work_doubles(int rows, int cols) { return svd_work_doubles(rows, cols); }
+
+int edak_svd_jacobi(const double* M, int rows, int cols, double* U, double* sig, double* V, double* work,
+                    void* stream) {
+  if (!M || !U || !sig || !work || cols < 1 || rows < cols) return EDAK_EINVAL;
+  return launch_svd_jacobi(M, rows, cols, U, sig, V, work, as_stream(stream));
+}
+
+int edak_pcg_init(int n, int ncols, const double* b, const double* z, double* x, double* r, double* p, double* rz,
+                  double* hist_rz, int hist_ld, int32_t* status, int32_t* iters, void* stream) {
+  if (ncols == 0) return EDAK_OK;
+  return launch_pcg_init(n, ncols, b, z, x, r, p, rz, hist_rz, hist_ld, status, iters, as_stream(stream));
+}
+
+int edak_pcg_cost0(int p_obs, int ncols, const double* d, double* m, double sigma2, double* hist_J, int hist_ld,
+                   void* stream) {
+  if (ncols == 0) return EDAK_OK;
+  return launch_pcg_cost0(p_obs, ncols, d, m, sigma2, hist_J, hist_ld, as_stream(stream));
+}
+
+int edak_pcg_alpha(int n, int ncols, const double* p, const double* hp, double* x, double* r, const double* rz,
+                   int32_t* status, int32_t* iters, int it, int p_obs, const double* gp, double* m, const double* d,
+                   double sigma2, double* hist_J, int hist_ld, void* stream) {
+  if (ncols == 0) return EDAK_OK;
+  return launch_pcg_alpha(n, ncols, p, hp, x, r, rz, status, iters, it, p_obs, gp, m, d, sigma2, hist_J, hist_ld,
+                          as_stream(stream));
+}
+
+int edak_pcg_beta(int n, int ncols, const double* z, const double* r, double* p, double* rz, double rtol,
+                  double* hist_rz, int hist_ld, int32_t* status, int32_t* iters, int it, void* stream) {
+  if (ncols == 0) return EDAK_OK;
+  return launch_pcg_beta(n, ncols, z, r, p, rz, rtol, hist_rz, hist_ld, status, iters, it, as_stream(stream));
+}
+
+int64_t edak_lmp_work_doubles(int n, int k, int ncols) {
+  return (int64_t)k * ncols + gemm_tn_partials(k, ncols, n);
+}
+
+int edak_lmp_apply(int n, int k, int ncols, const double* S, const double* coef, const double* r, double* z,
+                   double* work, void* stream) {
+  if (!S || !coef || !r || !z || !work || n < 1 || k < 1) return EDAK_EINVAL;
+  if (ncols == 0) return EDAK_OK;
+  cudaStream_t st = as_stream(stream);
+  double* W = work;
+  double* part = work + (int64_t)k * ncols;
+  int rc;
+  // W = S^T r (lmp.py:63);  z = r + S (coef o W) (lmp.py:64-65)
+  if ((rc = launch_gemm_tn(S, n, r, n, W, k, k, ncols, n, part, st))) return rc;
+  return launch_gemm_nn(S, n, W, k, coef, r, n, 1.0, z, n, n, ncols, k, st);
+}
+
+int edak_col_dots(int n, int ncols, const double* a, const double* b, double* out, void* stream) {
+  if (!a || !b || !out) return EDAK_EINVAL;
+  if (ncols == 0) return EDAK_OK;
+  return launch_col_dots(n, ncols, a, b, out, as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// Circulant background-covariance factor U_B applied column-wise
+// (GridCovFactor.apply / apply_t, covariance.py:41-47).
+//
+// U_B is circulant with generator u = irfft(symbol); the host truncates u to
+// the taps whose magnitude exceeds 2^-60 of the peak (the Gaussian factor
+// decays like exp(-d^2/L^2), so 2w+1 ~ 12.5 L taps) or keeps all n taps.
+//   out_i = sum_k taps[k] * in[(i + tap_w - k) mod n],  k < ntaps
+// One CTA = one column x a tile of NT*R outputs.  The input segment (tile +
+// halo) is staged in shared memory with one pad double per R (bank-conflict
+// free strided reads); each thread keeps R consecutive outputs in registers
+// and slides an R-wide window over the segment, so per tap it issues one
+// shared load of the segment, one broadcast load of the tap and R DFMAs.
+#include "common.cuh"
+
+namespace edak {
+
+constexpr int CIRC_R = 8;
+constexpr int CIRC_NT = 128;
+constexpr int CIRC_MAXTAPS = 4096;
+
+__device__ __forceinline__ int padi(int q) { return q + q / CIRC_R; }
+
+template <int R, int NT>
+__global__ void __launch_bounds__(NT) k_circ(int n, const double* __restrict__ taps, int K, int Kp, int w,
+                                             const double* __restrict__ in, double* __restrict__ out,
+                                             double ident, const double* __restrict__ zadd) {
+  extern __shared__ double sm[];
+  double* st = sm;                      // reversed taps, Kp (zero padded)
+  double* sg = sm + Kp;                 // segment, padded
+  const int col = blockIdx.y;
+  const int i0 = blockIdx.x * NT * R;
+  const int t = threadIdx.x;
+  const double* src = in + (size_t)col * n;
+  // correlation form: out[i0+o] = sum_m T[m] * seg[o + m], T[m] = taps[K-1-m],
+  // seg[q] = in[(i0 + w - K + 1 + q) mod n]
+  for (int m = t; m < Kp; m += NT) st[m] = m < K ? taps[K - 1 - m] : 0.0;
+  const int seglen = NT * R + Kp + R;
+  int g0 = wrap(i0 + w - K + 1, n);
+  for (int q = t; q < seglen; q += NT) {
+    int g = g0 + q % n;
+    if (g >= n) g -= n;
+    sg[padi(q)] = src[g];
+  }
+  __syncthreads();
+
+  double acc[R], cur[R], nxt[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    acc[r] = 0.0;
+    cur[r] = sg[padi(t * R + r)];
+  }
+  for (int m0 = 0; m0 < Kp; m0 += R) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) nxt[r] = sg[padi(t * R + m0 + R + r)];
+#pragma unroll
+    for (int mm = 0; mm < R; ++mm) {
+      const double tm = st[m0 + mm];
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = fma(tm, (r + mm < R) ? cur[r + mm] : nxt[r + mm - R], acc[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) cur[r] = nxt[r];
+  }
+  double* dst = out + (size_t)col * n;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = i0 + t * R + r;
+    if (i < n) dst[i] = zadd ? acc[r] + ident * zadd[(size_t)col * n + i] : acc[r];
+  }
+}
+
+// out = U_B in (+ ident * zadd when zadd != NULL: the I + A of assim.py:70-72)
+int launch_circ(const edak_problem* P, const double* in, double* out, int ncols, double ident,
+                const double* zadd, cudaStream_t st) {
+  const int n = P->n, K = P->ntaps;
+  if (K < 1 || K > CIRC_MAXTAPS) {
+    set_error("circulant factor: tap count outside [1, 4096]");
+    return EDAK_EUNSUPPORTED;
+  }
+  const int Kp = (K + CIRC_R - 1) / CIRC_R * CIRC_R;
+  const int tile = CIRC_NT * CIRC_R;
+  dim3 grid((n + tile - 1) / tile, ncols);
+  const int seglen = tile + Kp + CIRC_R;
+  const size_t smem = (size_t)(Kp + seglen + seglen / CIRC_R + 1) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_circ<CIRC_R, CIRC_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_circ<CIRC_R, CIRC_NT><<<grid, CIRC_NT, smem, st>>>(n, P->taps, K, Kp, P->tap_w, in, out, ident, zadd);
+  count_launch();
+  return check_launch("k_circ");
+}
+
+}  // namespace edak

@@ -1,0 +1,70 @@
+// Shared helpers for the edak sm_100a kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/edak.h"
+
+namespace edak {
+
+// error/launch bookkeeping (capi.cu)
+void set_error(const char* msg);
+int check_launch(const char* what);
+void count_launch(int k = 1);
+
+__host__ __device__ __forceinline__ int wrap(int i, int n) {
+  i %= n;
+  return i < 0 ? i + n : i;
+}
+
+// ---- bit-exact nonlinear Lorenz-96 pieces (no FMA contraction) ----------
+// tendency (model.py:20-22): ((x[i+1] - x[i-2]) * x[i-1] - x[i]) + F
+__device__ __forceinline__ double l96_f(double xp1, double xm2, double xm1,
+                                        double x0, double F) {
+  return __dadd_rn(__dsub_rn(__dmul_rn(__dsub_rn(xp1, xm2), xm1), x0), F);
+}
+// stage update x + c*k (model.py:41,43,45): rounded product then sum
+__device__ __forceinline__ double axpy_rn(double x, double c, double k) {
+  return __dadd_rn(x, __dmul_rn(c, k));
+}
+
+// ---- tangent-linear / adjoint tendencies (FMA allowed; rel ~1e-16) ----
+// tendency_tlm (model.py:25-28)
+__device__ __forceinline__ double l96_tl(double vp1, double vm2, double vm1,
+                                         double v0, double xp1, double xm2,
+                                         double xm1) {
+  return (vp1 - vm2) * xm1 + (xp1 - xm2) * vm1 - v0;
+}
+// tendency_adj (model.py:31-35):
+//   x[i-2] w[i-1] + (x[i+2] - x[i-1]) w[i+1] - x[i+1] w[i+2] - w[i]
+__device__ __forceinline__ double l96_ad(double xm2, double xm1, double xp1,
+                                         double xp2, double wm1, double w0,
+                                         double wp1, double wp2) {
+  return xm2 * wm1 + (xp2 - xm1) * wp1 - xp1 * wp2 - w0;
+}
+
+// warp / block reductions in a fixed order (deterministic)
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (w == 0) {
+    s = lane < NT / 32 ? sh[lane] : 0.0;
+    s = warp_sum(s);
+  }
+  return s;  // valid in warp 0 (all lanes)
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace edak

@@ -1,0 +1,464 @@
+// Lorenz-96 window sweeps on sm_100a:
+//   k_integrate : nonlinear RK4 producer, bit-exact with model.integrate
+//                 (model.py:38-48,118-131)
+//   k_tl        : tangent-linear sweep + time-major observation capture
+//                 (model.tlm + ObsNetwork.observe_tlm, model.py:56-63,134-144,
+//                 obs.py:47-50)
+//   k_ad        : adjoint sweep with observation forcing
+//                 (model.adjoint + ObsNetwork.observe_adj, model.py:66-84,
+//                 147-157, obs.py:52-57)
+// Stages are recomputed from the stored states (16 B/elem-step of HBM instead
+// of 64) with IEEE-rounded ops in the reference's order, so they are the
+// reference's stages bit for bit; STREAM=true reads stored stages instead.
+#include "sweep.cuh"
+
+namespace edak {
+
+struct SweepGeom {
+  int W;         // output window per tile (ring elements)
+  int HL;        // left halo
+  int periodic;  // 1: one tile covers the ring, nact = n / C
+  int nact;
+};
+
+// ------------------------------------------------------------------ RK4 --
+
+// One RK4 stage chain on own elements.  x (with halo) -> (k, x + c*k)
+template <int C>
+__device__ __forceinline__ void l96_stage(const double (&x)[C + 4], const double (&X)[C + 4], double c,
+                                          double F, double (&kk)[C], double (&xn)[C + 4]) {
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    kk[j] = l96_f(x[j + 3], x[j], x[j + 1], x[j + 2], F);
+    xn[j + 2] = axpy_rn(X[j + 2], c, kk[j]);
+  }
+}
+
+template <int C, int NT>
+__global__ void __launch_bounds__(NT) k_integrate(int n, int K, int s0, double dt, double F,
+                                                  const double* __restrict__ xin, int64_t in_stride,
+                                                  double* __restrict__ states, int64_t st_stride,
+                                                  double* __restrict__ stages, int64_t sg_stride,
+                                                  SweepGeom geo) {
+  extern __shared__ __align__(16) double dsm_[];
+  XBuf<NT>& xb = *reinterpret_cast<XBuf<NT>*>(dsm_);
+  Ring<C, NT> R;
+  const int i0 = blockIdx.x * geo.W;
+  R.init(n, geo.periodic ? 0 : i0 - geo.HL, geo.nact, geo.periodic);
+  const int col = blockIdx.y;
+  const int wlo = geo.periodic ? 0 : geo.HL;
+  const int whi = geo.periodic ? n : geo.HL + min(geo.W, n - i0);
+  const double h = 0.5 * dt, c6 = dt / 6.0;
+  double* st = states + (size_t)col * st_stride;
+  double* sg = stages ? stages + (size_t)col * sg_stride : nullptr;
+  int buf = 0;
+
+  double x[C + 4];
+  R.load_halo(xin + (size_t)col * in_stride, x);
+  for (int s = 0; s < K; ++s) {
+    double k1[C], k2[C], k3[C], k4[C], x2[C + 4], x3[C + 4], x4[C + 4];
+    l96_stage<C>(x, x, h, F, k1, x2);
+    xchg1(R, xb, buf, x2);
+    l96_stage<C>(x2, x, h, F, k2, x3);
+    xchg1(R, xb, buf, x3);
+    l96_stage<C>(x3, x, dt, F, k3, x4);
+    xchg1(R, xb, buf, x4);
+    double xn[C + 4];
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      k4[j] = l96_f(x4[j + 3], x4[j], x4[j + 1], x4[j + 2], F);
+      // x + (dt/6) * (((k1 + 2 k2) + 2 k3) + k4)   (model.py:47)
+      double sum = __dadd_rn(__dadd_rn(__dadd_rn(k1[j], 2.0 * k2[j]), 2.0 * k3[j]), k4[j]);
+      xn[j + 2] = __dadd_rn(x[j + 2], __dmul_rn(c6, sum));
+    }
+    // store own elements inside the output window
+    if (R.t < R.nact) {
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        const int e = R.t * C + j;
+        if (e >= wlo && e < whi) {
+          const int g = R.gidx(j);
+          st[(size_t)(s0 + s + 1) * n + g] = xn[j + 2];
+          if (sg) {
+            double* o = sg + (size_t)(s0 + s) * 4 * n + g;
+            o[0] = x[j + 2];
+            o[n] = x2[j + 2];
+            o[2 * n] = x3[j + 2];
+            o[3 * n] = x4[j + 2];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < C; ++j) x[j + 2] = xn[j + 2];
+    if (s + 1 < K) xchg1(R, xb, buf, x);
+  }
+}
+
+// ------------------------------------------------------------------- TL --
+
+template <int C>
+__device__ __forceinline__ void tl_sub(const double (&u)[C + 4], const double (&x)[C + 4], double (&a)[C]) {
+#pragma unroll
+  for (int j = 0; j < C; ++j)
+    a[j] = l96_tl(u[j + 3], u[j], u[j + 1], u[j + 2], x[j + 3], x[j], x[j + 1]);
+}
+
+template <int C, int NT, bool STREAM>
+__global__ void __launch_bounds__(NT) k_tl(edak_problem P, const double* __restrict__ v0,
+                                           double* __restrict__ obs, const int32_t* __restrict__ col_traj,
+                                           SweepGeom geo) {
+  extern __shared__ __align__(16) double dsm_[];
+  XBuf<NT>& xb = *reinterpret_cast<XBuf<NT>*>(dsm_);
+  Ring<C, NT> R;
+  const int n = P.n, N = P.n_steps;
+  const int i0 = blockIdx.x * geo.W;
+  R.init(n, geo.periodic ? 0 : i0 - geo.HL, geo.nact, geo.periodic);
+  const int col = blockIdx.y;
+  const int wlo = geo.periodic ? 0 : geo.HL;
+  const int whi = geo.periodic ? n : geo.HL + min(geo.W, n - i0);
+  const int traj = col_traj ? col_traj[col] : 0;
+  const double* tr = (STREAM ? P.stages : P.states) + (size_t)traj * P.traj_stride;
+  const int G = P.G;
+  double* ob = obs + (size_t)col * G * P.T;
+  const double dt = P.dt, h = 0.5 * dt, c6 = dt / 6.0, F = P.forcing;
+  int buf = 0;
+
+  double v[C + 4];
+  R.load_own(v0 + (size_t)col * n, v);
+
+  auto capture = [&](int level) {
+    const int tp = __ldg(P.tpos + level);
+    if (tp < 0 || R.t >= R.nact) return;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int e = R.t * C + j;
+      if (e >= wlo && e < whi) {
+        const int gp = __ldg(P.gpos + R.gidx(j));
+        if (gp >= 0) ob[(size_t)tp * G + gp] = v[j + 2];
+      }
+    }
+  };
+  capture(0);
+
+  for (int s = 0; s < N; ++s) {
+    const double* Xs = STREAM ? tr + (size_t)s * 4 * n : tr + (size_t)s * n;
+    double X[C + 4];
+    R.load_halo(Xs, X);
+    xchg1(R, xb, buf, v);
+    double acc[C], a[C], kk[C];
+    double x2[C + 4], u2[C + 4];
+    tl_sub<C>(v, X, a);
+    if (STREAM) {
+      R.load_halo(Xs + n, x2);
+    } else {
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        kk[j] = l96_f(X[j + 3], X[j], X[j + 1], X[j + 2], F);
+        x2[j + 2] = axpy_rn(X[j + 2], h, kk[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      acc[j] = a[j];
+      u2[j + 2] = v[j + 2] + h * a[j];
+    }
+    if (STREAM) xchg1(R, xb, buf, u2); else xchg2(R, xb, buf, x2, u2);
+
+    double x3[C + 4], u3[C + 4];
+    tl_sub<C>(u2, x2, a);
+    if (STREAM) {
+      R.load_halo(Xs + 2 * n, x3);
+    } else {
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        kk[j] = l96_f(x2[j + 3], x2[j], x2[j + 1], x2[j + 2], F);
+        x3[j + 2] = axpy_rn(X[j + 2], h, kk[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      acc[j] = acc[j] + 2.0 * a[j];
+      u3[j + 2] = v[j + 2] + h * a[j];
+    }
+    if (STREAM) xchg1(R, xb, buf, u3); else xchg2(R, xb, buf, x3, u3);
+
+    double x4[C + 4], u4[C + 4];
+    tl_sub<C>(u3, x3, a);
+    if (STREAM) {
+      R.load_halo(Xs + 3 * n, x4);
+    } else {
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        kk[j] = l96_f(x3[j + 3], x3[j], x3[j + 1], x3[j + 2], F);
+        x4[j + 2] = axpy_rn(X[j + 2], dt, kk[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      acc[j] = acc[j] + 2.0 * a[j];
+      u4[j + 2] = v[j + 2] + dt * a[j];
+    }
+    if (STREAM) xchg1(R, xb, buf, u4); else xchg2(R, xb, buf, x4, u4);
+
+    tl_sub<C>(u4, x4, a);
+#pragma unroll
+    for (int j = 0; j < C; ++j) v[j + 2] = v[j + 2] + c6 * (acc[j] + a[j]);
+    capture(s + 1);
+  }
+}
+
+// ------------------------------------------------------------------- AD --
+
+template <int C>
+__device__ __forceinline__ void ad_sub(const double (&w)[C + 4], const double (&x)[C + 4], double (&u)[C]) {
+#pragma unroll
+  for (int j = 0; j < C; ++j)
+    u[j] = l96_ad(x[j], x[j + 1], x[j + 3], x[j + 4], w[j + 1], w[j + 2], w[j + 3], w[j + 4]);
+}
+
+template <int C, int NT, bool STREAM>
+__global__ void __launch_bounds__(NT) k_ad(edak_problem P, const double* __restrict__ forcing,
+                                           double* __restrict__ gout, const int32_t* __restrict__ col_traj,
+                                           SweepGeom geo) {
+  extern __shared__ __align__(16) double dsm_[];
+  XBuf<NT>& xb = *reinterpret_cast<XBuf<NT>*>(dsm_);
+  Ring<C, NT> R;
+  const int n = P.n, N = P.n_steps;
+  const int i0 = blockIdx.x * geo.W;
+  R.init(n, geo.periodic ? 0 : i0 - geo.HL, geo.nact, geo.periodic);
+  const int col = blockIdx.y;
+  const int wlo = geo.periodic ? 0 : geo.HL;
+  const int whi = geo.periodic ? n : geo.HL + min(geo.W, n - i0);
+  const int traj = col_traj ? col_traj[col] : 0;
+  const double* tr = (STREAM ? P.stages : P.states) + (size_t)traj * P.traj_stride;
+  const int G = P.G;
+  const double* fc = forcing + (size_t)col * G * P.T;
+  const double dt = P.dt, h = 0.5 * dt, F = P.forcing;
+  const double c6 = dt / 6.0, c3 = 2.0 * dt / 6.0, s2 = P.sigma2;
+  int buf = 0;
+
+  // forcing w_all[level] at own elements: R^-1 d at observed points
+  // (obs.py:54-56 with covariance.py:71: w / sigma**2), 0 elsewhere
+  int gp[C];
+#pragma unroll
+  for (int j = 0; j < C; ++j) gp[j] = __ldg(P.gpos + R.gidx(j));
+  auto force = [&](int level, int j) -> double {
+    const int tp = __ldg(P.tpos + level);
+    if (tp < 0 || gp[j] < 0) return 0.0;
+    return __ldg(fc + (size_t)tp * G + gp[j]) / s2;
+  };
+
+  double g[C + 4];
+#pragma unroll
+  for (int j = 0; j < C; ++j) g[j + 2] = force(N, j);
+
+  for (int s = N - 1; s >= 0; --s) {
+    const double* Xs = STREAM ? tr + (size_t)s * 4 * n : tr + (size_t)s * n;
+    double X[C + 4], x2[C + 4], x3[C + 4], x4[C + 4];
+    R.load_halo(Xs, X);
+    if (STREAM) {
+      R.load_halo(Xs + n, x2);
+      R.load_halo(Xs + 2 * n, x3);
+      R.load_halo(Xs + 3 * n, x4);
+      xchg1(R, xb, buf, g);
+    } else {
+#pragma unroll
+      for (int j = 0; j < C; ++j) x2[j + 2] = axpy_rn(X[j + 2], h, l96_f(X[j + 3], X[j], X[j + 1], X[j + 2], F));
+      xchg2(R, xb, buf, x2, g);
+#pragma unroll
+      for (int j = 0; j < C; ++j)
+        x3[j + 2] = axpy_rn(X[j + 2], h, l96_f(x2[j + 3], x2[j], x2[j + 1], x2[j + 2], F));
+      xchg1(R, xb, buf, x3);
+#pragma unroll
+      for (int j = 0; j < C; ++j)
+        x4[j + 2] = axpy_rn(X[j + 2], dt, l96_f(x3[j + 3], x3[j], x3[j + 1], x3[j + 2], F));
+      xchg1(R, xb, buf, x4);
+    }
+    // step_adj (model.py:66-84)
+    double vh[C], u[C], a[C + 4];
+#pragma unroll
+    for (int k = 0; k < C + 4; ++k) a[k] = c6 * g[k];  // a4 = (dt/6) w, halo included
+    ad_sub<C>(a, x4, u);
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      vh[j] = g[j + 2] + u[j];
+      a[j + 2] = c3 * g[j + 2] + dt * u[j];  // a3
+    }
+    xchg1(R, xb, buf, a);
+    ad_sub<C>(a, x3, u);
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      vh[j] += u[j];
+      a[j + 2] = c3 * g[j + 2] + h * u[j];  // a2
+    }
+    xchg1(R, xb, buf, a);
+    ad_sub<C>(a, x2, u);
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      vh[j] += u[j];
+      a[j + 2] = c6 * g[j + 2] + h * u[j];  // a1
+    }
+    xchg1(R, xb, buf, a);
+    ad_sub<C>(a, X, u);
+#pragma unroll
+    for (int j = 0; j < C; ++j) g[j + 2] = (vh[j] + u[j]) + force(s, j);
+  }
+  if (R.t < R.nact) {
+    double* go = gout + (size_t)col * n;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int e = R.t * C + j;
+      if (e >= wlo && e < whi) go[R.gidx(j)] = g[j + 2];
+    }
+  }
+}
+
+// ------------------------------------------------------------ launchers --
+
+// opt a kernel into > 48 KB of dynamic shared memory (idempotent)
+template <int NT, typename K, typename... Args>
+static void go(K kernel, dim3 grid, cudaStream_t st, Args... args) {
+  const size_t bytes = sizeof(XBuf<NT>);
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  kernel<<<grid, NT, bytes, st>>>(args...);
+}
+
+// pick (C, NT) and tile geometry for a sweep with halos (hl, hr) per step
+static bool plan(int n, int hl_total, int hr_total, int& C, int& NT, SweepGeom& geo, int& ntiles) {
+  // periodic single tile: whole ring in one CTA
+  const int cand_p[][2] = {{4, 64}, {4, 128}, {4, 256}, {4, 512}, {2, 64}, {2, 128}, {2, 256}, {2, 512}};
+  for (auto& f : cand_p) {
+    if (n % f[0] == 0 && n / f[0] <= f[1] && n / f[0] >= 2) {
+      C = f[0];
+      NT = f[1];
+      geo.W = n;
+      geo.HL = 0;
+      geo.periodic = 1;
+      geo.nact = n / C;
+      ntiles = 1;
+      return true;
+    }
+  }
+  // tile mode: the largest family keeps redundancy lowest
+  C = 4;
+  NT = 512;
+  const int range = C * NT;
+  const int W = range - hl_total - hr_total;
+  if (W < 64) return false;
+  ntiles = (n + W - 1) / W;
+  geo.W = (n + ntiles - 1) / ntiles;  // balanced tiles
+  geo.HL = hl_total;
+  geo.periodic = 0;
+  geo.nact = NT;
+  return true;
+}
+
+#define EDAK_DISPATCH(C_, NT_, ...)                                   \
+  if (C_ == 4 && NT_ == 64) { constexpr int CC = 4, TT = 64; __VA_ARGS__; }   \
+  else if (C_ == 4 && NT_ == 128) { constexpr int CC = 4, TT = 128; __VA_ARGS__; } \
+  else if (C_ == 4 && NT_ == 256) { constexpr int CC = 4, TT = 256; __VA_ARGS__; } \
+  else if (C_ == 4 && NT_ == 512) { constexpr int CC = 4, TT = 512; __VA_ARGS__; } \
+  else if (C_ == 2 && NT_ == 64) { constexpr int CC = 2, TT = 64; __VA_ARGS__; }   \
+  else if (C_ == 2 && NT_ == 128) { constexpr int CC = 2, TT = 128; __VA_ARGS__; } \
+  else if (C_ == 2 && NT_ == 256) { constexpr int CC = 2, TT = 256; __VA_ARGS__; } \
+  else if (C_ == 2 && NT_ == 512) { constexpr int CC = 2, TT = 512; __VA_ARGS__; } \
+  else { set_error("no kernel family"); return EDAK_EUNSUPPORTED; }
+
+int launch_tl(const edak_problem* P, const double* v0, double* obs, int ncols, const int32_t* col_traj,
+              cudaStream_t st) {
+  int C, NT, nt;
+  SweepGeom geo;
+  // halos: stencil reach per step (TL 8 left / 4 right) plus the edge
+  // garbage of the exchanged stage recompute
+  if (!plan(P->n, 8 * P->n_steps + 4, 4 * P->n_steps + 4, C, NT, geo, nt)) {
+    set_error("window too long for the tile family");
+    return EDAK_EUNSUPPORTED;
+  }
+  dim3 grid(nt, ncols);
+  const bool stream = P->stage_mode == 1;
+  EDAK_DISPATCH(C, NT, {
+    if (stream) go<TT>(k_tl<CC, TT, true>, grid, st, *P, v0, obs, col_traj, geo);
+    else go<TT>(k_tl<CC, TT, false>, grid, st, *P, v0, obs, col_traj, geo);
+  });
+  count_launch();
+  return check_launch("k_tl");
+}
+
+int launch_ad(const edak_problem* P, const double* forcing, double* g, int ncols, const int32_t* col_traj,
+              cudaStream_t st) {
+  int C, NT, nt;
+  SweepGeom geo;
+  if (!plan(P->n, 4 * P->n_steps + 8, 8 * P->n_steps + 8, C, NT, geo, nt)) {
+    set_error("window too long for the tile family");
+    return EDAK_EUNSUPPORTED;
+  }
+  dim3 grid(nt, ncols);
+  const bool stream = P->stage_mode == 1;
+  EDAK_DISPATCH(C, NT, {
+    if (stream) go<TT>(k_ad<CC, TT, true>, grid, st, *P, forcing, g, col_traj, geo);
+    else go<TT>(k_ad<CC, TT, false>, grid, st, *P, forcing, g, col_traj, geo);
+  });
+  count_launch();
+  return check_launch("k_ad");
+}
+
+int launch_integrate(int n, int n_steps, double dt, double F, const double* x0, int ncols, double* states,
+                     int64_t st_stride, double* stages, int64_t sg_stride, cudaStream_t st) {
+  // chunks of K steps per launch (tile mode halo 8K left, 4K right)
+  int C, NT, nt;
+  SweepGeom geo;
+  const int Kmax = 16;
+  int s0 = 0;
+  // level 0 = x0
+  cudaError_t e = cudaMemcpy2DAsync(states, st_stride * sizeof(double), x0, (size_t)n * sizeof(double),
+                                    (size_t)n * sizeof(double), ncols, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) {
+    set_error(cudaGetErrorString(e));
+    return EDAK_ECUDA;
+  }
+  while (s0 < n_steps) {
+    int K = n_steps - s0;
+    if (!plan(n, 8 * K + 4, 4 * K + 4, C, NT, geo, nt) || (!geo.periodic && K > Kmax)) {
+      K = K < Kmax ? K : Kmax;
+      if (!plan(n, 8 * K + 4, 4 * K + 4, C, NT, geo, nt)) {
+        set_error("integrate: no tile plan");
+        return EDAK_EUNSUPPORTED;
+      }
+    }
+    dim3 grid(nt, ncols);
+    const double* xin = states + (size_t)s0 * n;
+    EDAK_DISPATCH(C, NT, {
+      go<TT>(k_integrate<CC, TT>, grid, st, n, K, s0, dt, F, xin, st_stride, states, st_stride, stages,
+                                               sg_stride, geo);
+    });
+    count_launch();
+    int rc = check_launch("k_integrate");
+    if (rc) return rc;
+    s0 += K;
+  }
+  return EDAK_OK;
+}
+
+// nonlinear observation G(x) (obs.py:43-45)
+__global__ void k_observe(const double* __restrict__ states, int64_t stride, int n,
+                          const int32_t* __restrict__ grid, int G, const int32_t* __restrict__ times, int T,
+                          double* __restrict__ y) {
+  const int col = blockIdx.y;
+  const int p = G * T;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < p; q += gridDim.x * blockDim.x) {
+    const int tp = q / G, g = q - tp * G;
+    y[(size_t)col * p + q] = states[(size_t)col * stride + (size_t)times[tp] * n + grid[g]];
+  }
+}
+
+int launch_observe(const double* states, int64_t stride, int n, const int32_t* grid, int G,
+                   const int32_t* times, int T, int ncols, double* y, cudaStream_t st) {
+  const int p = G * T;
+  dim3 gridd((p + 255) / 256 < 1024 ? (p + 255) / 256 : 1024, ncols);
+  k_observe<<<gridd, 256, 0, st>>>(states, stride, n, grid, G, times, T, y);
+  count_launch();
+  return check_launch("k_observe");
+}
+
+}  // namespace edak

@@ -1,0 +1,214 @@
+// Small dense (l x l, l <= 256) stages of the randomized Nystrom EVD, each a
+// single CTA working out of L2 (nystrom.py:67-93,118-131):
+//   k_potrf_shifted : upper Cholesky with the reference's shift schedule
+//   k_trinv_upper   : explicit inverse of an upper-triangular factor
+//   k_svd_jacobi    : one-sided (Hestenes) Jacobi SVD, descending order
+#include "common.cuh"
+
+namespace edak {
+
+// Upper Cholesky W = C^T C reading W's upper triangle (scipy.linalg.cholesky
+// lower=False -> LAPACK dpotrf 'U').  Breakdown test is dpotrf's: a pivot
+// that is <= 0 or NaN.  Schedule (nystrom.py:77-93): plain; then if mode != 0
+// nu = eps * scale (scale = trace(W) when mode == 1, else `scale`), up to 5
+// tries with nu *= 10.
+__global__ void __launch_bounds__(256) k_potrf_shifted(const double* __restrict__ W, int l, double* __restrict__ Cm,
+                                                       int mode, double scale, double* nu_out, int32_t* info) {
+  __shared__ double sh[32];
+  __shared__ int fail;
+  __shared__ double cjj;
+  const int t = threadIdx.x;
+  double sc = scale;
+  if (mode == 1) {  // np.trace(w)
+    sc = 0.0;
+    for (int j = 0; j < l; ++j) sc += W[j + (size_t)j * l];
+  }
+  double nu = 0.0;
+  int attempt = 0;
+  for (; attempt < 6; ++attempt) {
+    if (attempt == 1) {
+      nu = 2.220446049250313e-16 * sc;
+      if (mode == 0 || !(nu > 0.0)) break;
+    } else if (attempt > 1) {
+      nu *= 10.0;
+    }
+    if (t == 0) fail = 0;
+    __syncthreads();
+    for (int j = 0; j < l && !fail; ++j) {
+      // pivot: (W[j][j] + nu) - sum_{k<j} C[k][j]^2
+      double s = 0.0;
+      for (int k = t; k < j; k += 256) {
+        const double c = Cm[k + (size_t)j * l];
+        s += c * c;
+      }
+      s = block_sum<256>(s, sh);
+      if (t == 0) {
+        const double d = (W[j + (size_t)j * l] + nu) - s;
+        if (!(d > 0.0)) {
+          fail = 1;
+        } else {
+          cjj = sqrt(d);
+          Cm[j + (size_t)j * l] = cjj;
+        }
+      }
+      __syncthreads();
+      if (fail) break;
+      const double piv = cjj;
+      // row j of C: C[j][i] = (W[j][i] - sum_k C[k][j] C[k][i]) / C[j][j]
+      for (int i = j + 1 + t; i < l; i += 256) {
+        double acc = W[j + (size_t)i * l];
+        const double* cj = Cm + (size_t)j * l;
+        const double* ci = Cm + (size_t)i * l;
+        for (int k = 0; k < j; ++k) acc -= cj[k] * ci[k];
+        Cm[j + (size_t)i * l] = acc / piv;
+      }
+      // zero the strict lower part of column j
+      for (int i = j + 1 + t; i < l; i += 256) Cm[i + (size_t)j * l] = 0.0;
+      __syncthreads();
+    }
+    __syncthreads();
+    if (!fail) break;
+  }
+  if (t == 0) {
+    const bool ok = attempt < 6 && !fail && !(attempt >= 1 && mode == 0);
+    info[0] = attempt;
+    info[1] = ok ? 0 : 1;
+    nu_out[0] = ok ? nu : 0.0;
+  }
+}
+
+int launch_potrf_shifted(const double* W, int l, double* C, int mode, double scale, double* nu_out, int32_t* info,
+                         cudaStream_t st) {
+  k_potrf_shifted<<<1, 256, 0, st>>>(W, l, C, mode, scale, nu_out, info);
+  count_launch();
+  return check_launch("k_potrf_shifted");
+}
+
+// Rinv = R^-1, R upper triangular: one thread per column, back substitution.
+__global__ void k_trinv_upper(const double* __restrict__ R, int l, double* __restrict__ X) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= l) return;
+  double* x = X + (size_t)j * l;
+  for (int i = l - 1; i > j; --i) x[i] = 0.0;
+  x[j] = 1.0 / R[j + (size_t)j * l];
+  for (int i = j - 1; i >= 0; --i) {
+    double s = 0.0;
+    for (int k = i + 1; k <= j; ++k) s += R[i + (size_t)k * l] * x[k];
+    x[i] = -s / R[i + (size_t)i * l];
+  }
+}
+
+int launch_trinv_upper(const double* R, int l, double* X, cudaStream_t st) {
+  k_trinv_upper<<<(l + 127) / 128, 128, 0, st>>>(R, l, X);
+  count_launch();
+  return check_launch("k_trinv_upper");
+}
+
+// One-sided Jacobi SVD of M (rows x cols, rows >= cols, column-major).
+// work: rows*cols (A) + cols*cols (V) + cols doubles.  Outputs, sorted by
+// descending singular value: U (rows x cols, unit columns or 0), sig (cols),
+// V (cols x cols) if Vout != NULL.
+constexpr int JAC_NT = 1024;
+
+__global__ void __launch_bounds__(JAC_NT) k_svd_jacobi(const double* __restrict__ M, int rows, int cols,
+                                                       double* __restrict__ U, double* __restrict__ sig,
+                                                       double* __restrict__ Vout, double* __restrict__ work) {
+  __shared__ int rotated;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = JAC_NT / 32;
+  double* A = work;
+  double* V = work + (size_t)rows * cols;
+  double* nrm = V + (size_t)cols * cols;
+  for (size_t e = t; e < (size_t)rows * cols; e += JAC_NT) A[e] = M[e];
+  for (size_t e = t; e < (size_t)cols * cols; e += JAC_NT) V[e] = (e % cols == e / cols) ? 1.0 : 0.0;
+  __syncthreads();
+  const int m = cols + (cols & 1);  // even tournament size (index `cols` = dummy)
+  const double tol = 4.0 * 2.220446049250313e-16;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (t == 0) rotated = 0;
+    __syncthreads();
+    for (int rd = 0; rd < m - 1; ++rd) {
+      for (int k = warp; k < m / 2; k += nw) {
+        int p = k == 0 ? 0 : ((k - 1 + rd) % (m - 1)) + 1;
+        int q = ((m - 1 - k - 1 + rd) % (m - 1)) + 1;
+        if (p > q) { int tmp = p; p = q; q = tmp; }
+        if (q >= cols || p == q) continue;
+        double* ap = A + (size_t)p * rows;
+        double* aq = A + (size_t)q * rows;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < rows; i += 32) {
+          const double x = ap[i], y = aq[i];
+          al += x * x;
+          be += y * y;
+          ga += x * y;
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (al == 0.0 || be == 0.0 || fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
+        for (int i = lane; i < rows; i += 32) {
+          const double x = ap[i], y = aq[i];
+          ap[i] = c * x - s * y;
+          aq[i] = s * x + c * y;
+        }
+        double* vp = V + (size_t)p * cols;
+        double* vq = V + (size_t)q * cols;
+        for (int i = lane; i < cols; i += 32) {
+          const double x = vp[i], y = vq[i];
+          vp[i] = c * x - s * y;
+          vq[i] = s * x + c * y;
+        }
+        if (lane == 0) rotated = 1;
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  // column norms
+  for (int j = warp; j < cols; j += nw) {
+    double s = 0.0;
+    const double* a = A + (size_t)j * rows;
+    for (int i = lane; i < rows; i += 32) s += a[i] * a[i];
+    s = warp_sum(s);
+    if (lane == 0) nrm[j] = sqrt(s);
+  }
+  __syncthreads();
+  // rank by descending norm (ties by index), scatter
+  for (int j = warp; j < cols; j += nw) {
+    const double sj = nrm[j];
+    int rank = 0;
+    for (int i = lane; i < cols; i += 32) {
+      const double si = nrm[i];
+      rank += (si > sj || (si == sj && i < j)) ? 1 : 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
+    const double* a = A + (size_t)j * rows;
+    double* u = U + (size_t)rank * rows;
+    for (int i = lane; i < rows; i += 32) u[i] = a[i] * inv;
+    if (Vout) {
+      const double* v = V + (size_t)j * cols;
+      double* vo = Vout + (size_t)rank * cols;
+      for (int i = lane; i < cols; i += 32) vo[i] = v[i];
+    }
+    if (lane == 0) sig[rank] = sj;
+  }
+}
+
+int64_t svd_work_doubles(int rows, int cols) { return (int64_t)rows * cols + (int64_t)cols * cols + cols; }
+
+int launch_svd_jacobi(const double* M, int rows, int cols, double* U, double* sig, double* V, double* work,
+                      cudaStream_t st) {
+  if (rows < cols) {
+    set_error("svd_jacobi needs rows >= cols");
+    return EDAK_EINVAL;
+  }
+  k_svd_jacobi<<<1, JAC_NT, 0, st>>>(M, rows, cols, U, sig, V, work);
+  count_launch();
+  return check_launch("k_svd_jacobi");
+}
+
+}  // namespace edak

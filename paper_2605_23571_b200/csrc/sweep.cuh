@@ -1,0 +1,106 @@
+// Register-chunk / shared-memory halo machinery for periodic 1-D stencil
+// sweeps over the Lorenz-96 ring.
+//
+// A CTA owns a contiguous "range" of NT*C ring elements; thread t holds
+// elements [t*C, t*C + C) in registers, in arrays laid out with a 2-element
+// halo on each side: a[0..1] = elements -2,-1; a[2..C+1] = own; a[C+2..C+3] =
+// elements C, C+1.  One exchange round publishes every thread's first two and
+// last two own values to shared memory and fills the neighbours' halos, with a
+// single __syncthreads (double-buffered slots, so round k+1 can start before a
+// slow thread has finished reading round k).
+//
+// Tile mode: the range is a window of the ring [base, base + NT*C) with
+// redundant halos; values near the range edges go stale one stencil reach per
+// sub-stage, and the host sizes the halos so the output window stays exact.
+// Periodic mode: nact = n / C threads cover the whole ring and the halo of
+// thread 0 / nact-1 wraps.
+#pragma once
+#include "common.cuh"
+
+namespace edak {
+
+template <int C, int NT>
+struct Ring {
+  int t, prev, next, nact;
+  bool hp, hn;
+  int base;  // ring index of range element 0 (before wrap)
+  int n;
+
+  __device__ __forceinline__ void init(int n_, int base_, int nact_, bool periodic) {
+    n = n_;
+    t = threadIdx.x;
+    nact = nact_;
+    base = base_;
+    if (periodic) {
+      prev = t == 0 ? nact - 1 : t - 1;
+      next = t + 1 >= nact ? 0 : t + 1;
+      hp = hn = true;
+    } else {
+      prev = t - 1;
+      next = t + 1;
+      hp = t > 0;
+      hn = t + 1 < nact;
+    }
+  }
+  // ring index of own element j (j may be -2..C+1)
+  __device__ __forceinline__ int gidx(int j) const { return wrap(base + t * C + j, n); }
+
+  // load own elements and 2+2 halo of a ring vector straight from memory
+  __device__ __forceinline__ void load_halo(const double* __restrict__ src, double (&a)[C + 4]) const {
+    int g = wrap(base + t * C - 2, n);
+#pragma unroll
+    for (int k = 0; k < C + 4; ++k) {
+      a[k] = __ldg(src + g);
+      if (++g == n) g = 0;
+    }
+  }
+  __device__ __forceinline__ void load_own(const double* __restrict__ src, double (&a)[C + 4]) const {
+    int g = wrap(base + t * C, n);
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      a[k + 2] = __ldg(src + g);
+      if (++g == n) g = 0;
+    }
+  }
+
+  // publish first two / last two own values of up to two arrays into sh[4*A][NT]
+  __device__ __forceinline__ void put(double* sh, const double (&a)[C + 4]) const {
+    sh[0 * NT + t] = a[2];
+    sh[1 * NT + t] = a[3];
+    sh[2 * NT + t] = a[C];
+    sh[3 * NT + t] = a[C + 1];
+  }
+  __device__ __forceinline__ void get(const double* sh, double (&a)[C + 4]) const {
+    a[0] = hp ? sh[2 * NT + prev] : 0.0;
+    a[1] = hp ? sh[3 * NT + prev] : 0.0;
+    a[C + 2] = hn ? sh[0 * NT + next] : 0.0;
+    a[C + 3] = hn ? sh[1 * NT + next] : 0.0;
+  }
+};
+
+// shared-memory exchange buffers: [2 bufs][2 arrays][4 slots][NT]
+template <int NT>
+struct XBuf {
+  double v[2][2][4][NT];
+};
+
+template <int C, int NT>
+__device__ __forceinline__ void xchg1(const Ring<C, NT>& R, XBuf<NT>& X, int& buf, double (&a)[C + 4]) {
+  R.put(&X.v[buf][0][0][0], a);
+  __syncthreads();
+  R.get(&X.v[buf][0][0][0], a);
+  buf ^= 1;
+}
+
+template <int C, int NT>
+__device__ __forceinline__ void xchg2(const Ring<C, NT>& R, XBuf<NT>& X, int& buf, double (&a)[C + 4],
+                                      double (&b)[C + 4]) {
+  R.put(&X.v[buf][0][0][0], a);
+  R.put(&X.v[buf][1][0][0], b);
+  __syncthreads();
+  R.get(&X.v[buf][0][0][0], a);
+  R.get(&X.v[buf][1][0][0], b);
+  buf ^= 1;
+}
+
+}  // namespace edak

@@ -1,0 +1,80 @@
+"""Thin host wrappers over the dense fp64 entry points of libedak.so
+(DMMA GEMMs, Cholesky with the reference shift schedule, triangular
+inverse, one-sided Jacobi SVD, column dots).  Blocks are (ncols, rows)
+device tensors = column-major (rows x ncols) matrices."""
+
+import torch
+
+from . import _lib
+
+
+def _empty(*shape, like):
+    return torch.empty(shape, dtype=torch.float64, device=like.device)
+
+
+def gemm_tn(A, B):
+    """A^T B for column blocks A (m, K), B (nb, K) -> (nb, m) block, i.e. the
+    column-major (m x nb) matrix C[a, b] = A[a] . B[b]."""
+    A, B = A.contiguous(), B.contiguous()
+    m, K = A.shape
+    nb = B.shape[0]
+    C = _empty(nb, m, like=A)
+    part = _empty(int(_lib.lib().edak_gemm_tn_partials(m, nb, K)), like=A)
+    _lib.call("edak_gemm_tn", A.data_ptr(), K, B.data_ptr(), K, C.data_ptr(), m, m, nb, K,
+              part.data_ptr(), _lib.stream())
+    return C
+
+
+def gemm_nn(A, B, bscale=None, Cin=None, beta=1.0, out=None):
+    """out = beta * Cin + A diag(bscale) B with A a column block (kk, M)
+    (column-major M x kk) and B a column block (N, kk): result (N, M)."""
+    A, B = A.contiguous(), B.contiguous()
+    kk, M = A.shape
+    N = B.shape[0]
+    out = _empty(N, M, like=A) if out is None else out
+    _lib.call("edak_gemm_nn", A.data_ptr(), M, B.data_ptr(), kk, _lib.ptr(bscale),
+              _lib.ptr(Cin), M, float(beta), out.data_ptr(), M, M, N, kk, _lib.stream())
+    return out
+
+
+def col_dots(A, B):
+    A, B = A.contiguous(), B.contiguous()
+    out = _empty(A.shape[0], like=A)
+    _lib.call("edak_col_dots", A.shape[1], A.shape[0], A.data_ptr(), B.data_ptr(),
+              out.data_ptr(), _lib.stream())
+    return out
+
+
+def potrf_shifted(W, mode, scale=0.0):
+    """Upper Cholesky of the (l x l) column-major W (block (l, l)) with the
+    nystrom.py:67-93 schedule.  Returns (C block, nu tensor[1], info int32[2])
+    -- no host sync."""
+    W = W.contiguous()
+    l = W.shape[0]
+    Cm = torch.zeros_like(W)
+    nu = _empty(1, like=W)
+    info = torch.zeros(2, dtype=torch.int32, device=W.device)
+    _lib.call("edak_potrf_shifted", W.data_ptr(), l, Cm.data_ptr(), int(mode), float(scale),
+              nu.data_ptr(), info.data_ptr(), _lib.stream())
+    return Cm, nu, info
+
+
+def trinv_upper(R):
+    R = R.contiguous()
+    X = torch.empty_like(R)
+    _lib.call("edak_trinv_upper", R.data_ptr(), R.shape[0], X.data_ptr(), _lib.stream())
+    return X
+
+
+def svd_jacobi(M, want_v=False):
+    """One-sided Jacobi SVD of a column block M (cols, rows), rows >= cols:
+    returns U (cols, rows) block, sig (cols,) descending, V (cols, cols)."""
+    M = M.contiguous()
+    cols, rows = M.shape
+    U = torch.empty_like(M)
+    sig = _empty(cols, like=M)
+    V = _empty(cols, cols, like=M) if want_v else None
+    work = _empty(int(_lib.lib().edak_svd_work_doubles(rows, cols)), like=M)
+    _lib.call("edak_svd_jacobi", M.data_ptr(), rows, cols, U.data_ptr(), sig.data_ptr(),
+              _lib.ptr(V), work.data_ptr(), _lib.stream())
+    return U, sig, V

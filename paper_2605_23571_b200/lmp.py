@@ -1,0 +1,113 @@
+"""Scaled spectral LMP on the GPU (mirrors reference ``lmp.py``).
+
+P = I + S (theta (Lambda + I)^-1 - I) S^T with symmetric factor
+U = I + S (sqrt(theta) (Lambda + I)^-1/2 - I) S^T (lmp.py:1-16).
+Each factor application is two DMMA GEMMs (edak_lmp_apply: W = S^T R,
+Z = R + S diag(c) W) over a whole (ncols, n) block of member residuals.
+
+``apply`` keeps the reference's two-factor form P v = U (U v)
+(lmp.py:72-74) unless S is orthonormal to 1e-13 (checked once on the
+device), in which case it applies P in one pass with c = theta/(lam+1) - 1
+-- the fused "I + U diag(.) U^T" of the north star, equal to the two-pass
+form up to rounding.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .linalg import gemm_tn
+
+THETA_RULES = ("halfsum", "lambdak", "one")
+ORTHO_TOL = 1e-13
+
+
+def choose_theta(rule, lam_k_of_system):
+    """lmp.py:25-41."""
+    if lam_k_of_system < 1.0 - 1e-8:
+        raise ValueError(f"I + A has eigenvalues >= 1, got lam_k={lam_k_of_system}")
+    if rule == "halfsum":
+        return 0.5 * (lam_k_of_system + 1.0)
+    if rule == "lambdak":
+        return float(lam_k_of_system)
+    if rule == "one":
+        return 1.0
+    raise ValueError(f"unknown theta rule {rule!r}; expected {THETA_RULES}")
+
+
+@dataclass
+class SpectralLmp:
+    """Preconditioner data (lmp.py:44-74) with device-resident S."""
+
+    vectors: np.ndarray
+    values: np.ndarray
+    theta: float
+    device_vectors: object = None
+    fused: bool | None = None
+
+    def __post_init__(self):
+        if self.theta <= 0:
+            raise ValueError("theta must be positive")
+        self.values = np.asarray(self.values, dtype=float)
+        if np.any(self.values < -1e-12):
+            raise ValueError("eigenvalue estimates of A must be >= 0")
+        self._ready = False
+
+    @property
+    def k(self):
+        return self.values.size
+
+    def _prepare(self):
+        if self._ready:
+            return
+        S = self.device_vectors
+        if S is None:
+            S = _dev.to_cols(np.asarray(self.vectors, dtype=float), self.vectors.shape[0])[0]
+        self._S = S.contiguous()
+        lam = np.asarray(self.values, dtype=float)
+        self._c_sqrt = _dev.f64(np.sqrt(self.theta / (lam + 1.0)) - 1.0)
+        self._c_full = _dev.f64(self.theta / (lam + 1.0) - 1.0)
+        if self.fused is None:
+            g = gemm_tn(self._S, self._S)
+            eye = torch.eye(self.k, dtype=torch.float64, device=g.device)
+            self.fused = bool((g - eye).abs().max() <= ORTHO_TOL)
+        self._ready = True
+
+    def _project_cols(self, coef, R, out=None):
+        n, ncols = R.shape[1], R.shape[0]
+        R = R.contiguous()
+        out = torch.empty_like(R) if out is None else out
+        work = torch.empty(int(_lib.lib().edak_lmp_work_doubles(n, self.k, ncols)),
+                           dtype=torch.float64, device=R.device)
+        _lib.call("edak_lmp_apply", n, self.k, ncols, self._S.data_ptr(), coef.data_ptr(),
+                  R.data_ptr(), out.data_ptr(), work.data_ptr(), _lib.stream())
+        return out
+
+    def apply_sqrt_cols(self, R, out=None):
+        """U R for a (ncols, n) device block (lmp.py:67-70)."""
+        self._prepare()
+        return self._project_cols(self._c_sqrt, R, out)
+
+    def apply_cols(self, R, out=None):
+        """P R for a (ncols, n) device block (lmp.py:72-74)."""
+        self._prepare()
+        if self.fused:
+            return self._project_cols(self._c_full, R, out)
+        return self._project_cols(self._c_sqrt, self._project_cols(self._c_sqrt, R), out)
+
+    def apply_sqrt(self, v):
+        cols, vec, as_np = _dev.to_cols(v, self.vectors.shape[0])
+        return _dev.from_cols(self.apply_sqrt_cols(cols), vec, as_np)
+
+    def apply(self, v):
+        cols, vec, as_np = _dev.to_cols(v, self.vectors.shape[0])
+        return _dev.from_cols(self.apply_cols(cols), vec, as_np)
+
+
+def make_lmp(approx, rule):
+    """lmp.py:77-81."""
+    theta = choose_theta(rule, float(approx.values[-1]) + 1.0)
+    return SpectralLmp(approx.vectors, approx.values, theta,
+                       device_vectors=getattr(approx, "device_vectors", None))

@@ -1,0 +1,185 @@
+"""Randomized Nystrom EVD on the GPU (mirrors reference ``nystrom.py``).
+
+Same API, dataclasses, validation and exceptions as the reference
+(nystrom.py:31-145).  The algorithm is the reference's pass
+    Y = A Phi;  W = Phi^T Y;  W = C^T C (shifted on breakdown);
+    A_N = F F^T with F = Y C^-1;  S, D = leading left singular pairs of F
+(the reference reaches the same F through Q_Y (R_Y C^-1), nystrom.py:118-131)
+with every dense step on the device:
+
+* W = Phi^T Y, Gram matrices: DMMA split-K GEMM (edak_gemm_tn);
+* Cholesky with the identical nu schedule and dpotrf breakdown test
+  (edak_potrf_shifted), C^-1 (edak_trinv_upper);
+* tall, large n: CholeskyQR2 of Y (two DMMA Grams + two triangular
+  solves as GEMMs), T = R_Y C^-1, one-sided Jacobi SVD of the l x l T,
+  S = Q_Y U_T (DMMA GEMM);
+* small n, wide (l > n, cfg2) or when CholeskyQR2's Gram is not positive
+  definite: one-sided Jacobi SVD straight on F (or F^T when l > n),
+  which handles exact rank deficiency.
+The rank check (nystrom.py:136-140) raises for exactly-zero columns of Y,
+the case in which Householder's R_Y has an exactly zero diagonal.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _dev
+from .linalg import col_dots, gemm_nn, gemm_tn, potrf_shifted, svd_jacobi, trinv_upper
+
+SHIFT_MODES = (None, "trace", "ynorm")
+_MODE_CODE = {None: 0, "trace": 1, "ynorm": 2}
+JACOBI_DIRECT_MAX_N = 4096
+
+
+class NystromBreakdownError(RuntimeError):
+    """Sketch does not support a usable factorization (nystrom.py:31)."""
+
+
+@dataclass
+class NystromConfig:
+    """nystrom.py:35-50."""
+
+    ell: int
+    k: int
+    q: int = 1
+    shift_mode: str | None = None
+
+    def __post_init__(self):
+        if not 1 <= self.k <= self.ell:
+            raise ValueError(f"need 1 <= k <= ell, got k={self.k} ell={self.ell}")
+        if self.q < 1:
+            raise ValueError(f"need q >= 1, got {self.q}")
+        if self.shift_mode not in SHIFT_MODES:
+            raise ValueError(f"shift_mode must be one of {SHIFT_MODES}")
+
+
+@dataclass
+class EigenApproximation:
+    """nystrom.py:53-64; ``device_vectors`` keeps the (k, n) device block."""
+
+    vectors: np.ndarray
+    values: np.ndarray
+    shift: float = 0.0
+    n_build_matvecs: int = 0
+    device_vectors: object = None
+
+    @property
+    def k(self):
+        return self.values.size
+
+
+def _device_operator(a_apply):
+    """(linearization, owner) when a_apply is our MemberProblem's bound a_apply."""
+    owner = getattr(a_apply, "__self__", None)
+    lin = getattr(owner, "lin", None)
+    if lin is not None and getattr(a_apply, "__name__", "") == "a_apply":
+        return lin, owner
+    return None, None
+
+
+def _apply_block(a_apply, phi_cols, n):
+    lin, owner = _device_operator(a_apply)
+    if lin is not None:
+        if owner is not None and hasattr(owner, "n_matvecs"):
+            owner.n_matvecs += 1
+        return lin.hessian_cols(phi_cols)
+    y = a_apply(phi_cols.t().cpu().numpy())
+    cols, _, _ = _dev.to_cols(np.asarray(y, dtype=float).reshape(n, -1), n)
+    return cols
+
+
+def _check_rank(Y):
+    nrm = col_dots(Y, Y).cpu().numpy()
+    dead = np.flatnonzero(nrm == 0.0)
+    if dead.size:
+        raise NystromBreakdownError(f"sketch column {dead[0]} was annihilated by the operator")
+
+
+def _cholqr2(Y):
+    """Q (l, n) block and upper R (l, l) block with Y = Q R, or None when a
+    Gram matrix is not numerically positive definite."""
+    G1 = gemm_tn(Y, Y)
+    R1, _, info1 = potrf_shifted(G1, 0)
+    Q1 = gemm_nn(Y, trinv_upper(R1))
+    G2 = gemm_tn(Q1, Q1)
+    R2, _, info2 = potrf_shifted(G2, 0)
+    if int(info1[1]) or int(info2[1]):
+        return None
+    Q = gemm_nn(Q1, trinv_upper(R2))
+    R = gemm_nn(R2, R1)  # R2 R1 (upper)
+    return Q, R
+
+
+def _orthobasis(Y):
+    """Orthonormal basis of range(Y) for the q > 1 passes."""
+    n = Y.shape[1]
+    if n >= Y.shape[0] and n > JACOBI_DIRECT_MAX_N:
+        qr = _cholqr2(Y)
+        if qr is not None:
+            return qr[0]
+    if n >= Y.shape[0]:
+        return svd_jacobi(Y)[0]
+    U, _, V = svd_jacobi(Y.t().contiguous(), want_v=True)
+    return V
+
+
+def nystrom_evd(a_apply, sketch, cfg):
+    """Leading eigenpairs of an SPD operator (nystrom.py:96-133)."""
+    phi_in = getattr(sketch, "columns", sketch)
+    dev_phi = getattr(sketch, "device_columns", None)
+    if isinstance(phi_in, torch.Tensor):
+        n, ell = phi_in.shape
+        phi = phi_in.to(_dev.device(), torch.float64).t().contiguous()
+    else:
+        phi_np = np.asarray(phi_in, dtype=float)
+        n, ell = phi_np.shape
+        phi = dev_phi if dev_phi is not None else _dev.to_cols(phi_np, n)[0]
+    if ell != cfg.ell:
+        raise ValueError(f"sketch has {ell} columns, cfg.ell={cfg.ell}")
+    Y = _apply_block(a_apply, phi, n)
+    _check_rank(Y)
+    for _ in range(cfg.q - 1):
+        phi = _orthobasis(Y)
+        Y = _apply_block(a_apply, phi, n)
+        _check_rank(Y)
+    W = gemm_tn(phi, Y)  # block (l, l): W[a][b] = phi_a . y_b
+    mode = _MODE_CODE[cfg.shift_mode]
+    scale = 0.0
+    if cfg.shift_mode == "ynorm":
+        scale = float(torch.sqrt(col_dots(Y, Y).sum()))
+    Cm, nu, info = potrf_shifted(W, mode, scale)
+    info = info.cpu().numpy()
+    if info[1]:
+        if info[0] <= 1:
+            raise NystromBreakdownError(
+                "Cholesky of the sketched Gram matrix broke down and no "
+                "usable shift is available")
+        raise NystromBreakdownError("sketched Gram matrix stayed indefinite after shifting")
+    shift = float(nu[0])
+    Cinv = trinv_upper(Cm)
+    k_eff = min(cfg.k, ell, n)
+    qr = _cholqr2(Y) if (n >= ell and n > JACOBI_DIRECT_MAX_N) else None
+    if qr is not None:
+        Q, R = qr
+        T = gemm_nn(R, Cinv)                 # R_Y C^-1 (l x l)
+        U_T, sig, _ = svd_jacobi(T)
+        S = gemm_nn(Q, U_T[:k_eff])          # Q_Y U_T[:, :k]
+    else:
+        F = gemm_nn(Y, Cinv)                 # Y C^-1 (n x l)
+        if n >= ell:
+            U, sig, _ = svd_jacobi(F)
+            S = U[:k_eff]
+        else:
+            _, sig, V = svd_jacobi(F.t().contiguous(), want_v=True)
+            S = V[:k_eff]
+    S = S.contiguous()
+    values = (sig[:k_eff] ** 2).cpu().numpy()
+    return EigenApproximation(vectors=S.t().cpu().numpy(), values=values, shift=shift,
+                              n_build_matvecs=cfg.q, device_vectors=S)
+
+
+def reconstruct(approx):
+    """S diag(D) S^T (nystrom.py:143-145)."""
+    return (approx.vectors * approx.values) @ approx.vectors.T

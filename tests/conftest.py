@@ -37,3 +37,17 @@ def unpack_problem(g, prefix):
     ub = CirculantFactor(states.shape[1], g[prefix + "symbol"])
     rn = DiagonalNoise(float(g[prefix + "sigma_obs"]))
     return MemberProblem(traj, net, ub, rn, g[prefix + "innov"])
+
+
+def pytest_collection_modifyitems(config, items):
+    try:
+        import torch
+        has_gpu = torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        has_gpu = False
+    if has_gpu:
+        return
+    skip = pytest.mark.skip(reason="no CUDA device in this container")
+    for item in items:
+        if "gpu" in item.keywords:
+            item.add_marker(skip)

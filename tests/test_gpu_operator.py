@@ -1,0 +1,192 @@
+"""GPU parity of the window operator: producer, U_B, TL/AD sweeps, Hessian
+block, rhs and cost against the CPU oracle / reference golden vectors."""
+
+import numpy as np
+import numpy.testing as npt
+import pytest
+import torch
+
+from conftest import unpack_problem
+from oracle import l96 as ol96
+from oracle.cov import diffusion_factor as o_diffusion, gaussian_factor as o_gaussian
+from oracle.obs import ObsNetwork as OObs, strided_grid
+from oracle.problem import MemberProblem as OProblem
+from oracle.cov import DiagonalNoise as ONoise
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    import paper_2605_23571_b200 as pkg
+    pkg.build.build()
+    return pkg
+
+
+def test_integrate_bit_exact_golden(gpu, ref_model):
+    from paper_2605_23571_b200 import model
+    g = ref_model
+    traj = model.integrate(g["x"], 0.025, 8, 8.0)
+    npt.assert_array_equal(traj.states, g["int_states"])
+    npt.assert_array_equal(traj.stages, g["int_stages"])
+    x = model.deterministic_truth(40, 0.025, 8.0, 2000).cpu().numpy()
+    npt.assert_array_equal(x, g["truth40"])
+
+
+@pytest.mark.parametrize("n,steps", [(10, 4), (1024, 16), (4099, 20), (16384, 24)])
+def test_integrate_bit_exact_oracle(gpu, n, steps):
+    from paper_2605_23571_b200 import model
+    rng = np.random.default_rng(n)
+    x0 = 8.0 + 3.0 * rng.standard_normal((2, n))
+    states, stages = model.integrate_device(x0, 0.025, steps, 8.0, want_stages=True)
+    for c in range(2):
+        ref = ol96.integrate(x0[c], 0.025, steps, 8.0)
+        npt.assert_array_equal(states[c].cpu().numpy(), ref.states)
+        npt.assert_array_equal(stages[c].cpu().numpy(), ref.stages)
+
+
+@pytest.mark.parametrize("n,kind", [(40, "diff"), (40, "gauss"), (1024, "gauss"),
+                                    (16384, "gauss"), (1500, "diff")])
+def test_factor_apply(gpu, n, kind):
+    from paper_2605_23571_b200.covariance import CirculantFactor
+    of = o_gaussian(n, 0.8, {40: 2.0, 1024: 8.0, 16384: 16.0}.get(n, 6.0)) if kind == "gauss" \
+        else o_diffusion(n, 0.8, 6.0, 10)
+    f = CirculantFactor(n, of.symbol)
+    z = np.random.default_rng(1).standard_normal((n, 5))
+    assert rel(f.apply(z), of.apply(z)) < 1e-14
+    assert rel(f.apply(z[:, 0]), of.apply(z[:, 0])) < 1e-14
+
+
+def test_obs_time_zero_tl_ad(gpu, ref_model):
+    """Observation capture/injection incl. level 0 on a ring of 10."""
+    from paper_2605_23571_b200.assim import Linearization
+    from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
+    g = ref_model
+    net = OObs([0, 3, 7], [0, 2, 4])
+    ub = CirculantFactor(10, np.ones(6))
+    lin = Linearization(g["obs0_states"][None], 0.025, 8.0, net, ub, DiagonalNoise(1.0),
+                        g["obs0_stages"][None], "auto")
+    assert lin.stage_mode == "recompute"
+    v = torch.tensor(g["v"][:10][None], device="cuda")
+    obs = lin.tl_cols(v)[0].cpu().numpy()
+    assert rel(obs, g["obs0_tl"]) < 1e-13
+    w = torch.tensor(g["obs0_w"][None], device="cuda")
+    adj = lin.ad_cols(w)[0].cpu().numpy()
+    assert rel(adj, g["obs0_ad"]) < 1e-13
+
+
+def test_member_problem_golden(gpu, ref_problem):
+    from paper_2605_23571_b200.assim import MemberProblem
+    from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
+    g = ref_problem
+    op = unpack_problem(g, "tiny_")
+    prob = MemberProblem(op.traj, op.net, CirculantFactor(40, op.ub.symbol),
+                         DiagonalNoise(op.rn.sigma), op.innovation)
+    assert prob.lin.stage_mode == "recompute"
+    az = prob.a_apply(g["tiny_z"])
+    assert az.shape == (40, 6)
+    for j in range(6):
+        assert rel(az[:, j], g["tiny_az"][:, j]) < 1e-12
+    assert prob.n_matvecs == 1
+    assert rel(prob.a_apply(g["tiny_z"][:, 2]), g["tiny_az"][:, 2]) < 1e-12
+    assert rel(prob.rhs(), g["tiny_rhs"]) < 1e-12
+    for j in range(6):
+        assert prob.quadratic_cost(g["tiny_z"][:, j]) == pytest.approx(g["tiny_cost"][j], rel=1e-12)
+    assert prob.n_matvecs == 2
+    h = prob.hessian_apply(g["tiny_z"])
+    assert rel(h, g["tiny_z"] + g["tiny_az"]) < 1e-12
+    dense = prob.a_apply(np.eye(40))
+    assert rel(dense, g["tiny_dense_a"]) < 1e-12
+    assert rel(dense, dense.T) < 1e-12  # symmetric
+
+
+def test_cfg1_hessian_block(gpu, ref_problem):
+    from paper_2605_23571_b200.assim import MemberProblem
+    g = ref_problem
+    op = unpack_problem(g, "cfg1_")
+    prob = MemberProblem(op.traj, op.net, op.ub, op.rn, op.innovation)
+    az = prob.a_apply(g["cfg1_z"])
+    for j in range(10):
+        assert rel(az[:, j], g["cfg1_az"][:, j]) < 1e-12
+
+
+def _oracle_problem(n, N, stride, every, L, seed):
+    rng = np.random.default_rng(seed)
+    x0 = 8.0 + 3.0 * rng.standard_normal(n)
+    x0 = ol96.integrate(x0, 0.025, 50, 8.0).states[-1]
+    traj = ol96.integrate(x0, 0.025, N, 8.0)
+    net = OObs(strided_grid(n, n // stride), list(range(every, N + 1, every)))
+    ub = o_gaussian(n, 0.8, L)
+    d = rng.standard_normal(net.p)
+    return OProblem(traj, net, ub, ONoise(1.0), d)
+
+
+@pytest.mark.parametrize("n,N,stride,every,L", [(1024, 16, 4, 2, 8.0), (4099, 10, 3, 2, 8.0),
+                                                (16384, 24, 4, 3, 16.0)])
+def test_hessian_tile_modes(gpu, n, N, stride, every, L):
+    """Periodic single-tile (n=1024), ragged tiles with wrap (n=4099) and the
+    cfg4 tile geometry (n=16384, N=24) against the oracle."""
+    from paper_2605_23571_b200.assim import MemberProblem
+    from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
+    op = _oracle_problem(n, N, stride, every, L, n)
+    prob = MemberProblem(op.traj, op.net, CirculantFactor(n, op.ub.symbol), DiagonalNoise(1.0),
+                         op.innovation)
+    z = np.random.default_rng(3).standard_normal((n, 2))
+    az = prob.a_apply(z)
+    ref = op.a_apply(z)
+    for j in range(2):
+        assert rel(az[:, j], ref[:, j]) < 1e-12
+    assert rel(prob.rhs(), op.rhs()) < 1e-12
+    assert prob.quadratic_cost(z[:, 0]) == pytest.approx(op.quadratic_cost(z[:, 0]), rel=1e-12)
+
+
+def test_stream_equals_recompute(gpu):
+    """Recomputed stages are the stored stages bit for bit, so both stage
+    modes give identical Hessian blocks."""
+    from paper_2605_23571_b200.assim import Linearization
+    from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
+    op = _oracle_problem(16384, 24, 4, 3, 16.0, 5)
+    ub = CirculantFactor(16384, op.ub.symbol)
+    a = Linearization(op.traj.states[None], 0.025, 8.0, op.net, ub, DiagonalNoise(1.0),
+                      op.traj.stages[None], "recompute")
+    b = Linearization(op.traj.states[None], 0.025, 8.0, op.net, ub, DiagonalNoise(1.0),
+                      op.traj.stages[None], "stream")
+    z = torch.randn(3, 16384, dtype=torch.float64, device="cuda")
+    assert torch.equal(a.hessian_cols(z), b.hessian_cols(z))
+
+
+def test_adjoint_identity_gpu(gpu):
+    """<G v, w> = <v, G^T w> on the GPU halves (test_obs.py:41-66 pattern)."""
+    from paper_2605_23571_b200.assim import Linearization
+    from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
+    for n, N in [(40, 8), (16384, 24)]:
+        op = _oracle_problem(n, N, 4, 3, 2.0 if n == 40 else 16.0, 7)
+        lin = Linearization(op.traj.states[None], 0.025, 8.0, op.net,
+                            CirculantFactor(n, op.ub.symbol), DiagonalNoise(1.0))
+        v = torch.randn(4, n, dtype=torch.float64, device="cuda")
+        w = torch.randn(4, op.net.p, dtype=torch.float64, device="cuda")
+        lhs = (lin.tl_cols(v) * w).sum(1)
+        rhs = (v * lin.ad_cols(w)).sum(1)
+        assert torch.allclose(lhs, rhs, rtol=1e-11, atol=1e-11)
+
+
+def test_ensemble_per_member_trajectories(gpu):
+    from paper_2605_23571_b200.assim import Ensemble, MemberProblem
+    from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
+    ops = [_oracle_problem(1024, 16, 4, 2, 8.0, s) for s in range(3)]
+    ub = CirculantFactor(1024, ops[0].ub.symbol)
+    for o in ops[1:]:
+        o.net = ops[0].net
+    members = [MemberProblem(o.traj, ops[0].net, ub, DiagonalNoise(1.0), o.innovation) for o in ops]
+    ens = Ensemble.from_members(members)
+    B = ens.rhs_all().cpu().numpy()
+    for j, o in enumerate(ops):
+        assert rel(B[j], o.rhs()) < 1e-12
+    Z = torch.randn(3, 1024, dtype=torch.float64, device="cuda")
+    AZ = ens.a_apply_members(Z).cpu().numpy()
+    for j, o in enumerate(ops):
+        assert rel(AZ[j], o.a_apply(Z[j].cpu().numpy())) < 1e-12
