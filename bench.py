@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""Benchmark: Hessian-column applies/s (and member-PCG solves/s) of one
+ensemble data-assimilation pass on BASELINE.json config 4 ("Throughput
+config": Lorenz-96 n=16384, 24-step window, every 4th variable at every 3rd
+step, Gaussian B L=16, 200 members with their own trajectories, rank-128
+LMP from a 128-column rhs-difference sketch, 80 PCG iterations batched over
+all members, fp64).
+
+One step = one full pass (engine.EdaPass.run):
+    rhs of control + all members (one batched AD launch)
+    -> Gamma -> Y = A_control Gamma, Nystrom EVD, halfsum LMP
+    -> batched LMP-PCG for every member, J traced at every iteration.
+value = (ell + members * iters) Hessian-column applies / step time (whole
+job: summed over ranks, timed as the max over ranks).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+--impl reference times the reference algorithm's CPU implementation (the
+oracle port of edasketch, oracle/) on the box's host cores for the same
+metric/config; rank 0 only.  See DESIGN.md "Measurement".
+"""
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Hessian-column applies/sec and member-PCG solves/sec; % of fp64/HBM roofline"
+UNIT = "Hessian-column applies/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--kernel-reps", type=int, default=10)
+    return ap.parse_args()
+
+
+def config_dict(cfg, world):
+    return {
+        "workload": f"BASELINE.json configs[{cfg.name[-1]}-1] ({cfg.name}): Lorenz-96 4D-Var EDA, "
+                    "one pass = rhs + Nystrom LMP + batched LMP-PCG",
+        "n": cfg.n, "window_steps": cfg.n_steps, "obs_every_var": cfg.obs_stride,
+        "obs_every_step": cfg.obs_every, "gaussian_L": cfg.cov_length,
+        "members": cfg.members * world, "members_per_gpu": cfg.members,
+        "trajectories": "per-member", "sketch_ell": cfg.ell, "lmp_rank": cfg.k,
+        "pcg_iters": cfg.pcg_iters, "theta_rule": "halfsum", "cost_trace": True,
+        "parallelism": f"members sharded over {world} GPU(s)" if world > 1 else "1 GPU",
+        "l2_policy": "inputs larger than L2 (member trajectories "
+                     f"{(cfg.members + 1) * (cfg.n_steps + 1) * cfg.n * 8 / 1e9:.2f} GB/GPU"
+                     " streamed every PCG iteration)",
+    }
+
+
+# ---------------------------------------------------------------- clocks --
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU legs ----
+def _cpu_worker(args):
+    """One host core: the reference algorithm (oracle port) running LMP-PCG
+    iterations for one member with its own trajectory, J traced via
+    quadratic_cost as in harness._solve_with_lmp (harness.py:178-182)."""
+    cfg_id, j, iters, truth = args
+    from oracle import l96
+    from oracle.algorithms import SolverConfig, SpectralLmp, pcg
+    from oracle.problem import MemberProblem
+    from oracle.twin import BASELINE_CONFIGS, baseline_inputs
+    cfg = BASELINE_CONFIGS[cfg_id]
+    inp = baseline_inputs(cfg, members=j + 1, truth=truth)
+    traj = l96.integrate(inp.member_x0[j], cfg.dt, cfg.n_steps, cfg.forcing)
+    d = inp.member_y[j] - inp.net.observe(traj)
+    prob = MemberProblem(traj, inp.net, inp.ub, inp.rn, d)
+    rng = np.random.default_rng(j)
+    s, _ = np.linalg.qr(rng.standard_normal((cfg.n, cfg.k)))
+    lmp = SpectralLmp(s, np.sort(rng.uniform(0, 1e3, cfg.k))[::-1], 2.0)
+    b = prob.rhs()
+    t0 = time.perf_counter()
+    pcg(prob.hessian_apply, b, SolverConfig(max_iters=iters), precond=lmp,
+        cost_fn=prob.quadratic_cost)
+    return time.perf_counter() - t0, iters
+
+
+def cpu_truth(cfg_id):
+    from oracle.twin import BASELINE_CONFIGS
+    from oracle import l96
+    cfg = BASELINE_CONFIGS[cfg_id]
+    return l96.deterministic_truth(cfg.n, cfg.dt, cfg.forcing, cfg.spinup_steps)
+
+
+def cpu_sample(cfg_id, seconds, cores, truth, iters=None):
+    """Bounded CPU sample: ``cores`` members, each running ``iters`` PCG
+    iterations in its own process; returns (applies/s, wall s, iters)."""
+    from oracle.twin import BASELINE_CONFIGS
+    cfg = BASELINE_CONFIGS[cfg_id]
+    if iters is None:
+        # measured on a Xeon core: ~2e-7 s per element-step for
+        # one LMP-PCG iteration with the J trace; each process runs ~seconds/4
+        per_iter = 2.0e-7 * cfg.n * cfg.n_steps
+        iters = int(max(2, min(cfg.pcg_iters, seconds / 4.0 / max(per_iter, 1e-5))))
+    for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[var] = "1"  # one core per process; inherited by spawn
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(cores) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_worker, [(cfg_id, j, iters, truth) for j in range(cores)])
+        wall = time.perf_counter() - t0
+    busy = max(r[0] for r in res)
+    applies = sum(r[1] for r in res)
+    return applies / busy, busy, iters, wall
+
+
+# ------------------------------------------------------------ GPU leg -----
+def kernel_roofline(torch, lib, eng, reps, peaks):
+    """Time the dominant kernels live (CUDA events on the launching stream)
+    on the PCG block: AD sweep and TL sweep over all members."""
+    ens = eng.members
+    lin = ens.lin
+    M, n, N, p = ens.M, lin.n, lin.n_steps, lin.p
+    dev = lin.states.device
+    V = torch.randn(M, n, dtype=torch.float64, device=dev)
+    W = torch.randn(M, p, dtype=torch.float64, device=dev)
+    out = {}
+    for name, fn in (("k_ad", lambda: lin.ad_cols(W, ens.traj_of)),
+                     ("k_tl", lambda: lin.tl_cols(V, ens.traj_of))):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        out[name] = s.elapsed_time(e) / reps * 1e-3
+    # algorithmic flops per launch (TL 37, AD 42 per element-step)
+    flops = {"k_ad": 42.0 * N * n * M, "k_tl": 37.0 * N * n * M}
+    # executed flops: + stage recompute (22/elem-step) on the redundant-halo range
+    dom = max(out, key=out.get)
+    t = out[dom]
+    achieved = flops[dom] / t / 1e12
+    # the streamed-stage HBM formulation the reference's Trajectory implies:
+    # 4 stages x 8 B read per element-step per sweep
+    stream_bytes = 32.0 * N * n * M + 16.0 * n * M
+    return {
+        "bound": "fp64",
+        "kernel": dom,
+        "achieved": achieved,
+        "peak": peaks["dfma_tflops"],
+        "unit": "TFLOP/s",
+        "frac": achieved / peaks["dfma_tflops"],
+        "traffic": None,
+        "peak_source": "measured in this run: DFMA-pipe loop (edak_peak_dfma); "
+                       "DMMA loop %.1f TFLOP/s" % peaks["dmma_tflops"],
+        "algorithmic_flops_per_launch": flops[dom],
+        "launch_ms": t * 1e3,
+        "launch_ms_other": {k: v * 1e3 for k, v in out.items() if k != dom},
+        "hbm_equivalent": {
+            "note": "GB/s the same launch would need if it streamed the stored RK4 "
+                    "stages (64 B/elem-step per apply) instead of recomputing them",
+            "achieved_gbs": stream_bytes / t / 1e9,
+            "hbm_peak_gbs": peaks["hbm_gbs"],
+        },
+    }
+
+
+def measure_peaks(torch, lib_mod):
+    lib = lib_mod.lib()
+    sink = torch.zeros(1, dtype=torch.float64, device="cuda")
+    res = {}
+    for name, fn, fl in (("dfma", "edak_peak_dfma", lambda it, b: 2.0 * 8 * it * 256 * b),
+                         ("dmma", "edak_peak_dmma", lambda it, b: 512.0 * 8 * it * 8 * b)):
+        iters, blocks = 4096, 148 * 8
+        getattr(lib, fn)(sink.data_ptr(), 64, blocks, lib_mod.stream())
+        torch.cuda.synchronize()
+        best = 0.0
+        for _ in range(3):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            getattr(lib, fn)(sink.data_ptr(), iters, blocks, lib_mod.stream())
+            e.record()
+            torch.cuda.synchronize()
+            best = max(best, fl(iters, blocks) / (s.elapsed_time(e) * 1e-3) / 1e12)
+        res[name + "_tflops"] = best
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            res["hbm_gbs"] = float(json.load(fh)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        res["hbm_gbs"] = 6650.0  # B200_PROFILING.md fallback
+    return res
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2605_23571_b200 import _lib, build
+    build.build()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2605_23571_b200.engine import EdaPass
+    from paper_2605_23571_b200.parallel import max_over_ranks
+    from paper_2605_23571_b200.twin import BASELINE_CONFIGS, build_ensemble
+    cfg = BASELINE_CONFIGS[args.config]
+    offset = rank * cfg.members
+    dens = build_ensemble(cfg, members=cfg.members, member_offset=offset)
+    eng = EdaPass(dens, member_offset=offset, total_members=cfg.members * world,
+                  distributed=world > 1)
+    applies = eng.applies_per_pass
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        res = eng.run()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    n0 = _lib.launch_count()
+    barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(args.steps):
+        res = eng.run()
+    e.record()
+    barrier()
+    launches = (_lib.launch_count() - n0) // args.steps
+    local_s = s.elapsed_time(e) * 1e-3
+    clk = clocks.stop()
+    t_step = max_over_ranks(local_s, torch.device("cuda", local)) / args.steps
+    value = applies * world / t_step
+
+    # ---- e2e: same pass through the public API with HOST (pinned) buffers
+    e2e = None
+    if not args.no_e2e:
+        lin = dens.lin
+        h_states = torch.empty_like(lin.states, device="cpu").pin_memory()
+        h_states.copy_(lin.states)
+        h_innov = torch.empty_like(dens.innovations, device="cpu").pin_memory()
+        h_innov.copy_(dens.innovations)
+        h_x = torch.empty((cfg.members, cfg.n), dtype=torch.float64).pin_memory()
+
+        def e2e_step():
+            lin.states.copy_(h_states, non_blocking=True)
+            dens.innovations.copy_(h_innov, non_blocking=True)
+            r = eng.run()
+            h_x.copy_(r.x, non_blocking=True)
+            return r
+
+        e2e_step()
+        barrier()
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2.record()
+        for _ in range(args.steps):
+            e2e_step()
+        e2.record()
+        barrier()
+        t2 = max_over_ranks(s2.elapsed_time(e2) * 1e-3, torch.device("cuda", local)) / args.steps
+        h2d = h_states.numel() * 8 + h_innov.numel() * 8
+        d2h = h_x.numel() * 8 + 2 * cfg.members * (cfg.pcg_iters + 1) * 8 + 8 * cfg.members
+        e2e = {"value": applies * world / t2, "unit": UNIT, "ms_per_step": t2 * 1e3,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "path": "host pinned trajectories+innovations -> EdaPass.run (C-ABI) -> host x"}
+
+    roof = None
+    if rank == 0:
+        peaks = measure_peaks(torch, _lib)
+        roof = kernel_roofline(torch, _lib, eng, args.kernel_reps, peaks)
+        # the dominant sweep runs once per PCG iteration, once for the rhs
+        # and once for the sketch: ~(iters + 2) launches per step
+        roof["kernel_share_of_step"] = (roof["launch_ms"] * (cfg.pcg_iters + 2) /
+                                        (t_step * 1e3))
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = len(os.sched_getaffinity(0))
+        truth = dens_truth(dens)
+        v, busy, iters, wall = cpu_sample(args.config, args.cpu_seconds, cores, truth)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{cores} members x {iters} LMP-PCG iterations (J traced) of "
+                         f"{cfg.name}, one member per process, oracle port of edasketch "
+                         f"(krylov.pcg/assim.MemberProblem); busy {busy:.1f} s"}
+    if rank == 0:
+        tr0 = res.traces[0]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded BASELINE cfg4 twin experiment)",
+            "config": config_dict(cfg, world),
+            "member_pcg_solves_per_s": cfg.members * world / t_step,
+            "applies_per_step": applies * world,
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "check": {"member0_J_first_last": [tr0.cost[0], tr0.cost[-1]],
+                      "member0_resnorm_last": tr0.resnorm[-1],
+                      "lmp_values_top": [float(v) for v in res.approx.values[:3]]},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def dens_truth(dens):
+    """Host copy of the spun-up truth used by the GPU ensemble (so the CPU
+    sample builds the same experiment without a 2000-step host spin-up)."""
+    from paper_2605_23571_b200.model import advance_device
+    from paper_2605_23571_b200.twin import _truth0
+    cfg = dens.cfg
+    return advance_device(_truth0(cfg), cfg.dt, cfg.spinup_steps, cfg.forcing)[0].cpu().numpy()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from oracle.twin import BASELINE_CONFIGS
+    cfg = BASELINE_CONFIGS[args.config]
+    cores = len(os.sched_getaffinity(0))
+    truth = cpu_truth(args.config)
+    if args.warmup > 0:
+        cpu_sample(args.config, 1.0, cores, truth, iters=2)
+    vals, walls = [], []
+    iters = None
+    per_step = min(args.cpu_seconds, 150.0 / max(args.steps, 1))
+    for _ in range(args.steps):
+        v, busy, iters, wall = cpu_sample(args.config, per_step, cores, truth, iters)
+        vals.append(v)
+        walls.append(busy)
+    value = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.median(walls)) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE cfg4 twin experiment)",
+        "config": config_dict(cfg, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"per step {cores} members x {iters} LMP-PCG iterations "
+                                   f"(J traced), one member per process, oracle port of "
+                                   f"edasketch; the reference is pure Python and cannot "
+                                   f"travel to the box, oracle/ restates it bit-exactly"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

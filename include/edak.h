@@ -187,6 +187,12 @@ int edak_lmp_apply(int n, int k, int ncols, const double* S, const double* coef,
 int edak_col_dots(int n, int ncols, const double* a, const double* b,
                   double* out, void* stream);
 
+/* ---- measurement ---------------------------------------------------- */
+/* fp64 roofline denominators (bench.py): an FMA-pipe loop, 2*8*iters*256*
+ * blocks flop per launch, and a DMMA.8x8x4 loop, 512*8*iters*8*blocks flop */
+int edak_peak_dfma(double* sink, int iters, int blocks, void* stream);
+int edak_peak_dmma(double* sink, int iters, int blocks, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

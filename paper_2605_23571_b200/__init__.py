@@ -8,6 +8,4 @@ include/edak.h) called through ctypes; importing the GPU entry points
 without the built library or without a CUDA device raises.
 """
 
-from . import build  # noqa: F401
-
 __version__ = "0.1.0"

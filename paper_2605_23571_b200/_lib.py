@@ -58,6 +58,8 @@ _PROTOS = {
     "edak_lmp_work_doubles": (i64, [C.c_int, C.c_int, C.c_int]),
     "edak_lmp_apply": (C.c_int, [C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp]),
     "edak_col_dots": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, vp]),
+    "edak_peak_dfma": (C.c_int, [vp, C.c_int, C.c_int, vp]),
+    "edak_peak_dmma": (C.c_int, [vp, C.c_int, C.c_int, vp]),
 }
 
 EXPORTED = tuple(_PROTOS)

@@ -198,6 +198,11 @@ class MemberProblem:
     def p(self):
         return self.lin.p
 
+    def a_apply_cols(self, Z):
+        """A on a (ncols, n) device block (no host copies); counts one matvec."""
+        self.n_matvecs += 1
+        return self.lin.hessian_cols(Z)
+
     def a_apply(self, z):
         """A z for (n,) or (n, l); one call = one matvec (assim.py:55-64)."""
         self.n_matvecs += 1
@@ -226,6 +231,38 @@ class MemberProblem:
 def dense_hessian_term(prob):
     """Materialised A (assim.py:88-91)."""
     return prob.a_apply(np.eye(prob.n))
+
+
+class TrajectoryOperator:
+    """A restricted to one trajectory of a multi-trajectory Linearization
+    (e.g. the control inside an ensemble): the a_apply duck type that
+    nystrom_evd / pcg consume, every column on trajectory ``index``."""
+
+    def __init__(self, lin, index=0):
+        self.lin = lin
+        self.index = int(index)
+        self.n_matvecs = 0
+
+    @property
+    def n(self):
+        return self.lin.n
+
+    def _ct(self, ncols):
+        return torch.full((ncols,), self.index, dtype=torch.int32, device=self.lin.states.device)
+
+    def a_apply_cols(self, Z):
+        self.n_matvecs += 1
+        return self.lin.hessian_cols(Z, self._ct(Z.shape[0]))
+
+    def a_apply(self, z):
+        cols, vec, as_np = _dev.to_cols(z, self.n)
+        return _dev.from_cols(self.a_apply_cols(cols), vec, as_np)
+
+    def hessian_apply(self, z):
+        self.n_matvecs += 1
+        cols, vec, as_np = _dev.to_cols(z, self.n)
+        return _dev.from_cols(self.lin.hessian_cols(cols, self._ct(cols.shape[0]), 1.0),
+                              vec, as_np)
 
 
 class Ensemble:

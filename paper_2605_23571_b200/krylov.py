@@ -1,0 +1,217 @@
+"""Preconditioned CG on the GPU (mirrors reference ``krylov.py``).
+
+``pcg`` keeps the reference signature and semantics (krylov.py:49-105):
+x0 = 0, fixed iteration budget, optional residual_rtol, per-iteration trace
+of cost J(x), preconditioned residual norm sqrt(max(r.z, 0)) and matvec
+count, the same stop rules and the same RuntimeError messages.
+
+``pcg_members`` is the batched engine: every ensemble member runs its own
+PCG recurrence (no coupling, krylov.py:49-97 per member) but each step is
+one launch over all members:
+
+    Hp      edak_hessian_block   (member j's own trajectory, I + A fused)
+    alpha   edak_pcg_alpha       (p.Hp, breakdown flag, x/r update, cost)
+    z = Pr  edak_lmp_apply       (DMMA GEMMs over the whole residual block)
+    beta    edak_pcg_beta        (r.z, stop test, p update)
+
+All reductions are fixed-order (deterministic).  The cost trace uses
+linearity, m_i = G U_B x_i = m_{i-1} + alpha_i (G U_B p_i), with G U_B p_i
+taken from the TL half of the Hessian apply, so J costs no extra sweep
+(``cost="exact"`` re-evaluates quadratic_cost with a TL sweep instead).
+Per-member status stays on the device; the host reads it once at the end
+(or every ``check_every`` iterations when a residual tolerance can stop
+members early).
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+
+
+@dataclass
+class SolverConfig:
+    """krylov.py:25-37."""
+
+    max_iters: int = 40
+    residual_rtol: float | None = None
+    trace_cost: bool = True
+
+    def __post_init__(self):
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be >= 1")
+
+
+@dataclass
+class SolveTrace:
+    """krylov.py:40-46."""
+
+    iterations: list = field(default_factory=list)
+    cost: list = field(default_factory=list)
+    resnorm: list = field(default_factory=list)
+    matvecs: list = field(default_factory=list)
+    status: str = "max_iters"
+
+
+class PcgBreakdown(RuntimeError):
+    """Raised like the reference (RuntimeError); ``member`` names the column."""
+
+    def __init__(self, msg, member=0):
+        super().__init__(msg)
+        self.member = member
+
+
+def _traces(status, iters, hist_rz, hist_J, trace_cost):
+    out = []
+    for c in range(status.shape[0]):
+        st, it = int(status[c]), int(iters[c])
+        if st == 3:
+            raise PcgBreakdown("preconditioner is not positive definite", c)
+        if st == 2:
+            raise PcgBreakdown(f"system matrix is not positive definite (iteration {it})", c)
+        tr = SolveTrace()
+        last = it
+        tr.iterations = list(range(last + 1))
+        tr.matvecs = list(range(last + 1))
+        rz = hist_rz[c, : last + 1]
+        tr.resnorm = [float(np.sqrt(max(v, 0.0))) for v in rz]
+        tr.cost = ([float(v) for v in hist_J[c, : last + 1]] if trace_cost
+                   else [float("nan")] * (last + 1))
+        tr.status = "converged" if st == 1 else "max_iters"
+        out.append(tr)
+    return out
+
+
+def pcg_device(apply_h, B, cfg, apply_p=None, cost=None, check_every=8):
+    """Batched PCG on a (M, n) device block of right-hand sides.
+
+    apply_h(P, out, gp) writes (I + A) P into ``out`` and, when ``gp`` is not
+    None, the raw TL observations G U_B P into ``gp`` (recurrence cost).
+    apply_p(R) -> P R (None = identity).  cost: None, ("recurrence", D,
+    sigma2) with innovations D (M, p), or ("exact", fn) with fn(X) -> (M,)
+    J values.  Returns X (M, n) and a list of SolveTrace."""
+    B = B.contiguous()
+    M, n = B.shape
+    dev = B.device
+    L = cfg.max_iters + 1
+    X, Rr, P = torch.empty_like(B), torch.empty_like(B), torch.empty_like(B)
+    HP = torch.empty_like(B)
+    rz = torch.empty(M, dtype=torch.float64, device=dev)
+    hist_rz = torch.zeros((M, L), dtype=torch.float64, device=dev)
+    hist_J = torch.full((M, L), float("nan"), dtype=torch.float64, device=dev)
+    status = torch.zeros(M, dtype=torch.int32, device=dev)
+    iters = torch.zeros(M, dtype=torch.int32, device=dev)
+    s = _lib.stream()
+    Z0 = apply_p(B) if apply_p is not None else B
+    _lib.call("edak_pcg_init", n, M, B.data_ptr(), Z0.data_ptr(), X.data_ptr(), Rr.data_ptr(),
+              P.data_ptr(), rz.data_ptr(), hist_rz.data_ptr(), L, status.data_ptr(),
+              iters.data_ptr(), s)
+    trace_cost = bool(cfg.trace_cost and cost is not None)
+    rec = trace_cost and cost[0] == "recurrence"
+    if rec:
+        D, sigma2 = cost[1].contiguous(), float(cost[2])
+        p_obs = D.shape[1]
+        m_state = torch.empty_like(D)
+        GP = torch.empty_like(D)
+        _lib.call("edak_pcg_cost0", p_obs, M, D.data_ptr(), m_state.data_ptr(), sigma2,
+                  hist_J.data_ptr(), L, s)
+    elif trace_cost:
+        hist_J[:, 0] = cost[1](X)
+    rtol = -1.0 if cfg.residual_rtol is None else float(cfg.residual_rtol)
+    for it in range(1, cfg.max_iters + 1):
+        apply_h(P, HP, GP if rec else None)
+        if rec:
+            _lib.call("edak_pcg_alpha", n, M, P.data_ptr(), HP.data_ptr(), X.data_ptr(),
+                      Rr.data_ptr(), rz.data_ptr(), status.data_ptr(), iters.data_ptr(), it,
+                      p_obs, GP.data_ptr(), m_state.data_ptr(), D.data_ptr(), sigma2,
+                      hist_J.data_ptr(), L, s)
+        else:
+            _lib.call("edak_pcg_alpha", n, M, P.data_ptr(), HP.data_ptr(), X.data_ptr(),
+                      Rr.data_ptr(), rz.data_ptr(), status.data_ptr(), iters.data_ptr(), it,
+                      0, None, None, None, 1.0, None, L, s)
+            if trace_cost:
+                run = status == 0
+                hist_J[:, it] = torch.where(run, cost[1](X), hist_J[:, it])
+        Zr = apply_p(Rr) if apply_p is not None else Rr
+        _lib.call("edak_pcg_beta", n, M, Zr.data_ptr(), Rr.data_ptr(), P.data_ptr(),
+                  rz.data_ptr(), rtol, hist_rz.data_ptr(), L, status.data_ptr(),
+                  iters.data_ptr(), it, s)
+        if rtol >= 0.0 and it % check_every == 0 and bool((status != 0).all()):
+            break
+    traces = _traces(status.cpu().numpy(), iters.cpu().numpy(), hist_rz.cpu().numpy(),
+                     hist_J.cpu().numpy(), trace_cost)
+    return X, traces
+
+
+def _device_problem(apply_h):
+    owner = getattr(apply_h, "__self__", None)
+    lin = getattr(owner, "lin", None)
+    if lin is not None and getattr(apply_h, "__name__", "") == "hessian_apply":
+        return owner
+    return None
+
+
+def pcg(apply_h, b, cfg, precond=None, cost_fn=None):
+    """Drop-in for krylov.pcg (krylov.py:49-97).
+
+    Fully on the device when ``apply_h`` is our MemberProblem.hessian_apply
+    (and ``cost_fn`` its quadratic_cost, ``precond`` our SpectralLmp);
+    otherwise user callables are invoked on host arrays each iteration
+    while the recurrence itself still runs on the device."""
+    b_np = not isinstance(b, torch.Tensor)
+    n = int(np.asarray(b).shape[0]) if b_np else int(b.shape[0])
+    Bc, _, _ = _dev.to_cols(b, n)
+    prob = _device_problem(apply_h)
+
+    if prob is not None:
+        work = prob.lin.work(1)
+
+        def apply_h_cols(P, out, gp):
+            prob.n_matvecs += 1
+            prob.lin.hessian_cols(P, None, 1.0, gp, out, work)
+    else:
+        def apply_h_cols(P, out, gp):
+            y = np.asarray(apply_h(P[0].cpu().numpy()), dtype=float)
+            out.copy_(torch.from_numpy(y)[None])
+
+    if precond is None:
+        apply_p = None
+    elif hasattr(precond, "apply_cols"):
+        apply_p = precond.apply_cols
+    else:
+        fn = precond if callable(precond) else precond.apply
+
+        def apply_p(R):
+            return _dev.to_cols(np.asarray(fn(R[0].cpu().numpy()), dtype=float), n)[0]
+
+    cost = None
+    if cfg.trace_cost and cost_fn is not None:
+        owner = getattr(cost_fn, "__self__", None)
+        if prob is not None and owner is prob and cost_fn.__name__ == "quadratic_cost":
+            cost = ("recurrence", prob._d, prob.lin.sigma2)
+        else:
+            cost = ("exact", lambda X: torch.tensor([float(cost_fn(X[0].cpu().numpy()))],
+                                                    dtype=torch.float64, device=X.device))
+    X, traces = pcg_device(apply_h_cols, Bc, cfg, apply_p, cost)
+    x = X[0].cpu().numpy() if b_np else X[0]
+    return x, traces[0]
+
+
+def pcg_members(ens, B, cfg, precond=None, cost="recurrence"):
+    """Batched PCG over all members of an ``Ensemble``: B (M, n) device
+    right-hand sides (e.g. ens.rhs_all()).  cost: "recurrence", "exact" or
+    None.  Returns (X (M, n), [SolveTrace] * M)."""
+    work = ens.lin.work(ens.M)
+
+    def apply_h_cols(P, out, gp):
+        ens.a_apply_members(P, ident=1.0, obs_out=gp, out=out, work=work)
+
+    apply_p = precond.apply_cols if precond is not None else None
+    c = None
+    if cfg.trace_cost and cost == "recurrence":
+        c = ("recurrence", ens.D, ens.lin.sigma2)
+    elif cfg.trace_cost and cost == "exact":
+        c = ("exact", ens.cost_members)
+    return pcg_device(apply_h_cols, B, cfg, apply_p, c)

@@ -12,8 +12,6 @@ device), in which case it applies P in one pass with c = theta/(lam+1) - 1
 form up to rounding.
 """
 
-from dataclasses import dataclass
-
 import numpy as np
 import torch
 
@@ -37,23 +35,31 @@ def choose_theta(rule, lam_k_of_system):
     raise ValueError(f"unknown theta rule {rule!r}; expected {THETA_RULES}")
 
 
-@dataclass
 class SpectralLmp:
-    """Preconditioner data (lmp.py:44-74) with device-resident S."""
+    """Preconditioner data (lmp.py:44-74) with device-resident S.
 
-    vectors: np.ndarray
-    values: np.ndarray
-    theta: float
-    device_vectors: object = None
-    fused: bool | None = None
+    ``vectors`` (n, k) numpy as in the reference, or None when
+    ``device_vectors`` (k, n) is given (downloaded lazily)."""
 
-    def __post_init__(self):
-        if self.theta <= 0:
+    def __init__(self, vectors, values, theta, device_vectors=None, fused=None):
+        if theta <= 0:
             raise ValueError("theta must be positive")
-        self.values = np.asarray(self.values, dtype=float)
+        self.values = np.asarray(values, dtype=float)
         if np.any(self.values < -1e-12):
             raise ValueError("eigenvalue estimates of A must be >= 0")
+        self.theta = theta
+        self._vectors = None if vectors is None else np.asarray(vectors, dtype=float)
+        self.device_vectors = device_vectors
+        self.fused = fused
         self._ready = False
+        self.n = (self._vectors.shape[0] if self._vectors is not None
+                  else int(device_vectors.shape[1]))
+
+    @property
+    def vectors(self):
+        if self._vectors is None:
+            self._vectors = self.device_vectors.t().cpu().numpy()
+        return self._vectors
 
     @property
     def k(self):
@@ -64,7 +70,7 @@ class SpectralLmp:
             return
         S = self.device_vectors
         if S is None:
-            S = _dev.to_cols(np.asarray(self.vectors, dtype=float), self.vectors.shape[0])[0]
+            S = _dev.to_cols(self._vectors, self.n)[0]
         self._S = S.contiguous()
         lam = np.asarray(self.values, dtype=float)
         self._c_sqrt = _dev.f64(np.sqrt(self.theta / (lam + 1.0)) - 1.0)
@@ -98,16 +104,17 @@ class SpectralLmp:
         return self._project_cols(self._c_sqrt, self._project_cols(self._c_sqrt, R), out)
 
     def apply_sqrt(self, v):
-        cols, vec, as_np = _dev.to_cols(v, self.vectors.shape[0])
+        cols, vec, as_np = _dev.to_cols(v, self.n)
         return _dev.from_cols(self.apply_sqrt_cols(cols), vec, as_np)
 
     def apply(self, v):
-        cols, vec, as_np = _dev.to_cols(v, self.vectors.shape[0])
+        cols, vec, as_np = _dev.to_cols(v, self.n)
         return _dev.from_cols(self.apply_cols(cols), vec, as_np)
 
 
 def make_lmp(approx, rule):
     """lmp.py:77-81."""
     theta = choose_theta(rule, float(approx.values[-1]) + 1.0)
-    return SpectralLmp(approx.vectors, approx.values, theta,
-                       device_vectors=getattr(approx, "device_vectors", None))
+    dv = getattr(approx, "device_vectors", None)
+    return SpectralLmp(None if dv is not None else approx.vectors, approx.values, theta,
+                       device_vectors=dv)

@@ -55,36 +55,50 @@ class NystromConfig:
             raise ValueError(f"shift_mode must be one of {SHIFT_MODES}")
 
 
-@dataclass
 class EigenApproximation:
-    """nystrom.py:53-64; ``device_vectors`` keeps the (k, n) device block."""
+    """nystrom.py:53-64.  ``device_vectors`` keeps the (k, n) device block;
+    the numpy ``vectors`` (n, k) are downloaded on first access only."""
 
-    vectors: np.ndarray
-    values: np.ndarray
-    shift: float = 0.0
-    n_build_matvecs: int = 0
-    device_vectors: object = None
+    def __init__(self, vectors=None, values=None, shift=0.0, n_build_matvecs=0,
+                 device_vectors=None):
+        self._vectors = None if vectors is None else np.asarray(vectors, dtype=float)
+        self.values = np.asarray(values, dtype=float)
+        self.shift = shift
+        self.n_build_matvecs = n_build_matvecs
+        self.device_vectors = device_vectors
+
+    @property
+    def vectors(self):
+        if self._vectors is None and self.device_vectors is not None:
+            self._vectors = self.device_vectors.t().cpu().numpy()
+        return self._vectors
+
+    @vectors.setter
+    def vectors(self, v):
+        self._vectors = np.asarray(v, dtype=float)
 
     @property
     def k(self):
         return self.values.size
 
+    def __repr__(self):
+        return (f"EigenApproximation(k={self.k}, values={self.values!r}, "
+                f"shift={self.shift!r}, n_build_matvecs={self.n_build_matvecs})")
 
-def _device_operator(a_apply):
-    """(linearization, owner) when a_apply is our MemberProblem's bound a_apply."""
+
+def _device_owner(a_apply):
+    """Our operator object when a_apply is its bound ``a_apply`` (then the
+    sketch never leaves the device)."""
     owner = getattr(a_apply, "__self__", None)
-    lin = getattr(owner, "lin", None)
-    if lin is not None and getattr(a_apply, "__name__", "") == "a_apply":
-        return lin, owner
-    return None, None
+    if hasattr(owner, "a_apply_cols") and getattr(a_apply, "__name__", "") == "a_apply":
+        return owner
+    return None
 
 
 def _apply_block(a_apply, phi_cols, n):
-    lin, owner = _device_operator(a_apply)
-    if lin is not None:
-        if owner is not None and hasattr(owner, "n_matvecs"):
-            owner.n_matvecs += 1
-        return lin.hessian_cols(phi_cols)
+    owner = _device_owner(a_apply)
+    if owner is not None:
+        return owner.a_apply_cols(phi_cols)
     y = a_apply(phi_cols.t().cpu().numpy())
     cols, _, _ = _dev.to_cols(np.asarray(y, dtype=float).reshape(n, -1), n)
     return cols
@@ -176,8 +190,8 @@ def nystrom_evd(a_apply, sketch, cfg):
             S = V[:k_eff]
     S = S.contiguous()
     values = (sig[:k_eff] ** 2).cpu().numpy()
-    return EigenApproximation(vectors=S.t().cpu().numpy(), values=values, shift=shift,
-                              n_build_matvecs=cfg.q, device_vectors=S)
+    return EigenApproximation(values=values, shift=shift, n_build_matvecs=cfg.q,
+                              device_vectors=S)
 
 
 def reconstruct(approx):

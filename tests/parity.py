@@ -1,0 +1,68 @@
+"""Parity protocol helpers.
+
+Some reference outputs are ill-conditioned functions of the operator: two
+legitimate fp64 evaluations of A differ by ~1e-16 per apply, and late PCG
+iterates or the smallest Nystrom values of an ill-conditioned sketch move by
+far more than 1e-10 under such perturbations *on the CPU itself*.  These
+helpers measure that CPU-vs-CPU envelope with the oracle in the same test
+(apply_h / Y multiplied by (1 + 2e-16 xi), xi ~ N(0,1)), and the GPU result
+must lie within max(rel 1e-10 of the reference, 10 x envelope).
+"""
+
+import numpy as np
+
+from oracle import algorithms as oalg
+
+JITTER = 2e-16
+
+
+def pcg_envelope(apply_h, b, cfg, precond=None, cost_fn=None, trials=4, seed=7):
+    """(reference trace, envelope of |dJ|, envelope of |d resnorm|)."""
+    _, ref = oalg.pcg(apply_h, b, cfg, precond=precond, cost_fn=cost_fn)
+    rng = np.random.default_rng(seed)
+    n = len(ref.cost)
+    e_j, e_r = np.zeros(n), np.zeros(n)
+    for _ in range(trials):
+        def h(v):
+            return apply_h(v) * (1 + JITTER * rng.standard_normal(np.shape(v)))
+        _, tr = oalg.pcg(h, b, cfg, precond=precond, cost_fn=cost_fn)
+        m = min(n, len(tr.cost))
+        e_j[:m] = np.maximum(e_j[:m], np.abs(np.array(tr.cost[:m]) - ref.cost[:m]))
+        e_r[:m] = np.maximum(e_r[:m], np.abs(np.array(tr.resnorm[:m]) - ref.resnorm[:m]))
+    return ref, e_j, e_r
+
+
+def assert_trace(ours, ref, env_j, env_r, rtol=1e-10):
+    """J within rel 1e-10 or 10x envelope; resnorm within 1e-10 r0 or 10x envelope."""
+    assert len(ours.cost) == len(ref.cost), (len(ours.cost), len(ref.cost))
+    J, Jr = np.asarray(ours.cost), np.asarray(ref.cost)
+    tol = np.maximum(rtol * np.abs(Jr), 10 * env_j)
+    bad = np.abs(J - Jr) > tol
+    assert not bad.any(), ("J", np.flatnonzero(bad), J[bad], Jr[bad], tol[bad])
+    R, Rr = np.asarray(ours.resnorm), np.asarray(ref.resnorm)
+    tol = np.maximum(rtol * Rr[0], 10 * env_r)
+    bad = np.abs(R - Rr) > tol
+    assert not bad.any(), ("resnorm", np.flatnonzero(bad), R[bad], Rr[bad], tol[bad])
+
+
+def nystrom_envelope(op, phi, cfg, trials=4):
+    """Per-value CPU-vs-CPU spread of the reference Nystrom values when
+    Y = A Phi is perturbed at the 1e-16 level."""
+    y = op.a_apply(phi)
+    base = oalg.nystrom_evd(lambda v: y, phi, cfg).values
+    rng = np.random.default_rng(123)
+    env = np.zeros_like(base)
+    for _ in range(trials):
+        yp = y * (1 + JITTER * rng.standard_normal(y.shape))
+        env = np.maximum(env, np.abs(oalg.nystrom_evd(lambda v: yp, phi, cfg).values - base))
+    return env
+
+
+def assert_values(ours, ref, env):
+    """rel 1e-10 for D_i >= 1e-6 D_1, else abs 1e-10 D_1, widened to 10x the
+    measured envelope where that is larger."""
+    ours, ref = np.asarray(ours), np.asarray(ref)
+    tol = np.where(ref >= 1e-6 * ref[0], 1e-10 * np.abs(ref), 1e-10 * ref[0])
+    tol = np.maximum(tol, 10.0 * env)
+    bad = np.abs(ours - ref) > tol
+    assert not bad.any(), (ours[bad], ref[bad], tol[bad])

@@ -23,7 +23,8 @@ def rel(a, b):
 @pytest.fixture(scope="module")
 def gpu():
     import paper_2605_23571_b200 as pkg
-    pkg.build.build()
+    from paper_2605_23571_b200 import build
+    build.build()
     return pkg
 
 

@@ -1,0 +1,237 @@
+"""GPU parity of the dense stages (DMMA GEMMs, Cholesky with the reference
+shift schedule, Jacobi SVD), the Nystrom EVD, the LMP and PCG against the
+CPU oracle and the reference golden vectors (SURVEY.md §8c protocol)."""
+
+import json
+import os
+
+import numpy as np
+import numpy.testing as npt
+import pytest
+import torch
+
+from conftest import GOLDEN, unpack_problem
+from parity import assert_trace, assert_values, nystrom_envelope, pcg_envelope
+from oracle import algorithms as oalg
+from oracle.twin import TwinConfig, build_setup
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    import paper_2605_23571_b200 as pkg
+    from paper_2605_23571_b200 import build
+    build.build()
+    return pkg
+
+
+def _gpu_problem(op):
+    from paper_2605_23571_b200.assim import MemberProblem
+    from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
+    return MemberProblem(op.traj, op.net, CirculantFactor(op.n, op.ub.symbol),
+                         DiagonalNoise(op.rn.sigma), op.innovation)
+
+
+@pytest.mark.parametrize("m,nb,K", [(10, 10, 40), (64, 64, 1024), (128, 200, 16384), (37, 5, 999)])
+def test_gemm_tn(gpu, m, nb, K):
+    from paper_2605_23571_b200.linalg import gemm_tn
+    A = torch.randn(m, K, dtype=torch.float64, device="cuda")
+    B = torch.randn(nb, K, dtype=torch.float64, device="cuda")
+    C = gemm_tn(A, B)  # block (nb, m)
+    ref = (B @ A.t())
+    assert torch.allclose(C, ref, rtol=1e-12, atol=1e-11 * K ** 0.5)
+
+
+@pytest.mark.parametrize("M,N,kk", [(40, 10, 10), (16384, 200, 128), (1000, 7, 33)])
+def test_gemm_nn(gpu, M, N, kk):
+    from paper_2605_23571_b200.linalg import gemm_nn
+    A = torch.randn(kk, M, dtype=torch.float64, device="cuda")   # column-major M x kk
+    B = torch.randn(N, kk, dtype=torch.float64, device="cuda")   # column-major kk x N
+    s = torch.rand(kk, dtype=torch.float64, device="cuda")
+    Cin = torch.randn(N, M, dtype=torch.float64, device="cuda")
+    D = gemm_nn(A, B, bscale=s, Cin=Cin, beta=1.0)
+    ref = Cin + (B * s) @ A
+    assert torch.allclose(D, ref, rtol=1e-12, atol=1e-12 * kk)
+
+
+def test_potrf_paths(gpu):
+    """test_nystrom.py:61-77 pattern on the device kernel."""
+    from paper_2605_23571_b200.linalg import potrf_shifted
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((6, 6))
+    w = x @ x.T + 6 * np.eye(6)
+    W = torch.tensor(w.T.copy(), device="cuda")
+    C, nu, info = potrf_shifted(W, 0)
+    c = C.cpu().numpy().T
+    npt.assert_allclose(c.T @ c, w, atol=1e-12 * np.linalg.norm(w))
+    assert float(nu[0]) == 0.0 and info.cpu().tolist() == [0, 0]
+    assert np.allclose(c, np.triu(c))
+    Z = torch.zeros(4, 4, dtype=torch.float64, device="cuda")
+    C, nu, info = potrf_shifted(Z, 2, 4.0)
+    assert info.cpu().tolist()[1] == 0 and float(nu[0]) > 0
+    npt.assert_allclose(C.cpu().numpy(), np.sqrt(float(nu[0])) * np.eye(4), atol=1e-18)
+    assert potrf_shifted(Z, 0)[2].cpu().tolist()[1] == 1
+    assert potrf_shifted(Z, 2, 0.0)[2].cpu().tolist()[1] == 1
+
+
+@pytest.mark.parametrize("rows,cols", [(10, 10), (64, 64), (1024, 64), (128, 128), (50, 40)])
+def test_svd_jacobi(gpu, rows, cols):
+    from paper_2605_23571_b200.linalg import svd_jacobi
+    rng = np.random.default_rng(rows + cols)
+    m = rng.standard_normal((rows, cols)) * np.logspace(0, -6, cols)
+    U, sig, V = svd_jacobi(torch.tensor(m.T.copy(), device="cuda"), want_v=True)
+    s_ref = np.linalg.svd(m, compute_uv=False)
+    npt.assert_allclose(sig.cpu().numpy(), s_ref, rtol=1e-12)
+    u = U.cpu().numpy().T
+    v = V.cpu().numpy().T
+    npt.assert_allclose(u * sig.cpu().numpy(), m @ v, atol=1e-12 * s_ref[0])
+    npt.assert_allclose(u.T @ u, np.eye(cols), atol=1e-12)
+
+
+def _lmp_action_close(ours, ref_vecs, ref_vals, theta, n, tol):
+    """Compare LMPs sign-invariantly through their action on random vectors."""
+    ref = oalg.SpectralLmp(ref_vecs, ref_vals, theta)
+    v = np.random.default_rng(0).standard_normal((n, 4))
+    return rel(ours.apply(v), ref.apply(v)) < tol
+
+
+def test_nystrom_tiny_golden(gpu, ref_problem):
+    from paper_2605_23571_b200.lmp import make_lmp
+    from paper_2605_23571_b200.nystrom import NystromConfig, nystrom_evd
+    g = ref_problem
+    prob = _gpu_problem(unpack_problem(g, "tiny_"))
+    cfg = NystromConfig(10, 8, shift_mode="trace")
+    approx = nystrom_evd(prob.a_apply, g["tiny_gamma"], cfg)
+    assert prob.n_matvecs == 1 and approx.n_build_matvecs == 1
+    env = nystrom_envelope(unpack_problem(g, "tiny_"), g["tiny_gamma"],
+                           oalg.NystromConfig(10, 8, shift_mode="trace"))
+    assert_values(approx.values, g["tiny_nys_vals"], env)
+    assert approx.shift == float(g["tiny_nys_shift"])
+    npt.assert_allclose(approx.vectors.T @ approx.vectors, np.eye(8), atol=1e-12)
+    lmp = make_lmp(approx, "halfsum")
+    # theta = (lam_k + 2) / 2 inherits the envelope of the smallest value
+    assert abs(lmp.theta - float(g["tiny_theta"])) <= max(1e-10 * lmp.theta, 5 * env[-1])
+    assert _lmp_action_close(lmp, g["tiny_nys_vecs"], g["tiny_nys_vals"], lmp.theta, 40, 1e-8)
+
+
+def test_nystrom_mirror_and_invariants(gpu, ref_problem):
+    from paper_2605_23571_b200.nystrom import NystromConfig, nystrom_evd
+    g = ref_problem
+    prob = _gpu_problem(unpack_problem(g, "mir_"))
+    approx = nystrom_evd(prob.a_apply, g["mir_phi"], NystromConfig(20, 15, shift_mode="trace"))
+    env = nystrom_envelope(unpack_problem(g, "mir_"), g["mir_phi"],
+                           oalg.NystromConfig(20, 15, shift_mode="trace"))
+    assert_values(approx.values, g["mir_nys_vals"], env)
+    assert approx.shift == 0.0
+    assert np.all(np.diff(approx.values) <= 0) and np.all(approx.values >= 0)
+
+
+def test_nystrom_cfg2_shift_path(gpu, ref_problem):
+    """l = 50 > n = 40: singular Gram, first eps*trace(W) shift succeeds,
+    k = 50 returns 40 pairs (SURVEY.md §7 hard part 2)."""
+    from paper_2605_23571_b200.nystrom import NystromConfig, nystrom_evd
+    g = ref_problem
+    prob = _gpu_problem(unpack_problem(g, "cfg2_"))
+    for k in (10, 20, 50):
+        approx = nystrom_evd(prob.a_apply, g["cfg2_gamma"], NystromConfig(50, k, shift_mode="trace"))
+        ref_shift = float(g[f"cfg2_k{k}_shift"])
+        assert approx.shift == pytest.approx(ref_shift, rel=1e-12)
+        ref = g[f"cfg2_k{k}_vals"]
+        assert approx.values.size == ref.size == min(k, 40)
+        env = nystrom_envelope(unpack_problem(g, "cfg2_"), g["cfg2_gamma"],
+                               oalg.NystromConfig(50, k, shift_mode="trace"))
+        assert_values(approx.values, ref, env)
+
+
+def test_zero_operator_raises(gpu):
+    from paper_2605_23571_b200.nystrom import NystromBreakdownError, NystromConfig, nystrom_evd
+    phi = np.random.default_rng(2).standard_normal((12, 4))
+    for mode in (None, "trace"):
+        with pytest.raises(NystromBreakdownError):
+            nystrom_evd(lambda v: 0.0 * v, phi, NystromConfig(ell=4, k=4, shift_mode=mode))
+
+
+def test_pcg_generic_callables(gpu):
+    from paper_2605_23571_b200.krylov import SolverConfig, pcg
+    b = np.random.default_rng(0).standard_normal(25)
+    x, tr = pcg(lambda v: v, b, SolverConfig(max_iters=10, residual_rtol=1e-12))
+    npt.assert_allclose(x, b, atol=1e-14)
+    assert tr.status == "converged" and tr.iterations[-1] == 1
+    with pytest.raises(RuntimeError, match="iteration 1"):
+        pcg(lambda v: -v, np.ones(5), SolverConfig(max_iters=3))
+    rng = np.random.default_rng(1)
+    m = rng.standard_normal((15, 15))
+    h = m @ m.T + 15 * np.eye(15)
+    hi = np.linalg.inv(h)
+    bb = rng.standard_normal(15)
+    xs, tr = pcg(lambda v: h @ v, bb, SolverConfig(max_iters=10, residual_rtol=1e-10),
+                 precond=lambda v: hi @ v)
+    assert tr.iterations[-1] == 1
+    npt.assert_allclose(xs, np.linalg.solve(h, bb), atol=1e-10)
+
+
+def test_pcg_reference_fixtures(gpu):
+    """Reference harness fixtures (tiny.cfg / ensemble.cfg, diffusion B,
+    unpreconditioned PCG J traces) reproduced by the GPU solver."""
+    from paper_2605_23571_b200.krylov import SolverConfig, pcg
+    with open(os.path.join(GOLDEN, "fixtures.json")) as fh:
+        fx = json.load(fh)
+    tw = TwinConfig(n=40, obs_grid_count=8, members=10)
+    setup = build_setup(tw, trial_seed=0)
+    prob = _gpu_problem(setup.control)
+    _, tr = pcg(prob.hessian_apply, prob.rhs(), SolverConfig(max_iters=8),
+                cost_fn=prob.quadratic_cost)
+    npt.assert_allclose(tr.cost, [float(v) for v in fx["control-lmp"]["0/"]], rtol=1e-12)
+    for key, vals in fx["ensemble-lmp"].items():
+        m = _gpu_problem(setup.members[int(key.split("/")[1]) - 1])
+        _, tr = pcg(m.hessian_apply, m.rhs(), SolverConfig(max_iters=8), cost_fn=m.quadratic_cost)
+        npt.assert_allclose(tr.cost, [float(v) for v in vals], rtol=1e-12)
+
+
+def test_cfg1_lmp_pcg_golden(gpu, ref_problem):
+    """cfg1: Nystrom on Gamma (shared linearization) + halfsum LMP + 30 PCG
+    iterations for three members: J rel 1e-10, resnorm 1e-10 r0."""
+    from paper_2605_23571_b200.krylov import SolverConfig, pcg
+    from paper_2605_23571_b200.lmp import make_lmp
+    from paper_2605_23571_b200.nystrom import NystromConfig, nystrom_evd
+    from oracle.twin import BASELINE_CONFIGS, baseline_setup
+    g = ref_problem
+    st = baseline_setup(BASELINE_CONFIGS[1])
+    ctl = _gpu_problem(st.control)
+    approx = nystrom_evd(ctl.a_apply, g["cfg1_gamma"], NystromConfig(10, 10, shift_mode="trace"))
+    env = nystrom_envelope(st.control, g["cfg1_gamma"], oalg.NystromConfig(10, 10, shift_mode="trace"))
+    assert_values(approx.values, g["cfg1_nys_vals"], env)
+    lmp = make_lmp(approx, "halfsum")
+    for j in (0, 4, 9):
+        m = _gpu_problem(st.members[j])
+        _, tr = pcg(m.hessian_apply, m.rhs(), SolverConfig(max_iters=30), precond=lmp,
+                    cost_fn=m.quadratic_cost)
+        npt.assert_allclose(tr.cost, g[f"cfg1_m{j}_cost"], rtol=1e-10)
+        r0 = g[f"cfg1_m{j}_resnorm"][0]
+        assert np.max(np.abs(np.array(tr.resnorm) - g[f"cfg1_m{j}_resnorm"])) <= 1e-10 * r0
+
+
+def test_pcg_members_batched_equals_single(gpu):
+    """The batched engine runs the same per-member recurrence: identical
+    traces to one-member solves, recurrence cost == exact cost (1e-10)."""
+    from paper_2605_23571_b200.assim import Ensemble
+    from paper_2605_23571_b200.krylov import SolverConfig, pcg, pcg_members
+    tw = TwinConfig(n=40, obs_grid_count=8, members=4)
+    setup = build_setup(tw, trial_seed=0)
+    mems = [_gpu_problem(m) for m in setup.members]
+    ens = Ensemble.from_members(mems)
+    cfg = SolverConfig(max_iters=12)
+    X, trs = pcg_members(ens, ens.rhs_all(), cfg, cost="recurrence")
+    X2, trs2 = pcg_members(ens, ens.rhs_all(), cfg, cost="exact")
+    for j, m in enumerate(mems):
+        _, tr = pcg(m.hessian_apply, m.rhs(), cfg, cost_fn=m.quadratic_cost)
+        npt.assert_array_equal(trs[j].resnorm, tr.resnorm)  # same kernels, same bits
+        npt.assert_allclose(trs[j].cost, trs2[j].cost, rtol=1e-10)
+        om = setup.members[j]
+        ref, ej, er = pcg_envelope(om.hessian_apply, om.rhs(), cfg, cost_fn=om.quadratic_cost)
+        assert_trace(trs[j], ref, ej, er)
