@@ -33,14 +33,15 @@ __device__ __forceinline__ double axpy_rn(double x, double c, double k) {
 __device__ __forceinline__ double l96_tl(double vp1, double vm2, double vm1,
                                          double v0, double xp1, double xm2,
                                          double xm1) {
-  return (vp1 - vm2) * xm1 + (xp1 - xm2) * vm1 - v0;
+  // explicit fma: every template instantiation rounds identically
+  return fma(vp1 - vm2, xm1, fma(xp1 - xm2, vm1, -v0));
 }
 // tendency_adj (model.py:31-35):
 //   x[i-2] w[i-1] + (x[i+2] - x[i-1]) w[i+1] - x[i+1] w[i+2] - w[i]
 __device__ __forceinline__ double l96_ad(double xm2, double xm1, double xp1,
                                          double xp2, double wm1, double w0,
                                          double wp1, double wp2) {
-  return xm2 * wm1 + (xp2 - xm1) * wp1 - xp1 * wp2 - w0;
+  return fma(xm2, wm1, fma(xp2 - xm1, wp1, fma(-xp1, wp2, -w0)));
 }
 
 // warp / block reductions in a fixed order (deterministic)

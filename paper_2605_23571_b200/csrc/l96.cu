@@ -10,6 +10,9 @@
 // Stages are recomputed from the stored states (16 B/elem-step of HBM instead
 // of 64) with IEEE-rounded ops in the reference's order, so they are the
 // reference's stages bit for bit; STREAM=true reads stored stages instead.
+#include <cstdio>
+#include <cstdlib>
+
 #include "sweep.cuh"
 
 namespace edak {
@@ -141,10 +144,17 @@ __global__ void __launch_bounds__(NT) k_tl(edak_problem P, const double* __restr
   };
   capture(0);
 
+  // software pipeline: the state of step s+1 is in flight while step s runs
+  const size_t sstride = STREAM ? (size_t)4 * n : (size_t)n;
+  double Xn[C + 4];
+  R.load_halo(tr, Xn);
+#pragma unroll 1
   for (int s = 0; s < N; ++s) {
-    const double* Xs = STREAM ? tr + (size_t)s * 4 * n : tr + (size_t)s * n;
+    const double* Xs = tr + (size_t)s * sstride;
     double X[C + 4];
-    R.load_halo(Xs, X);
+#pragma unroll
+    for (int k = 0; k < C + 4; ++k) X[k] = Xn[k];
+    if (s + 1 < N) R.load_halo(Xs + sstride, Xn);
     xchg1(R, xb, buf, v);
     double acc[C], a[C], kk[C];
     double x2[C + 4], u2[C + 4];
@@ -161,7 +171,7 @@ __global__ void __launch_bounds__(NT) k_tl(edak_problem P, const double* __restr
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       acc[j] = a[j];
-      u2[j + 2] = v[j + 2] + h * a[j];
+      u2[j + 2] = fma(h, a[j], v[j + 2]);
     }
     if (STREAM) xchg1(R, xb, buf, u2); else xchg2(R, xb, buf, x2, u2);
 
@@ -178,8 +188,8 @@ __global__ void __launch_bounds__(NT) k_tl(edak_problem P, const double* __restr
     }
 #pragma unroll
     for (int j = 0; j < C; ++j) {
-      acc[j] = acc[j] + 2.0 * a[j];
-      u3[j + 2] = v[j + 2] + h * a[j];
+      acc[j] = fma(2.0, a[j], acc[j]);
+      u3[j + 2] = fma(h, a[j], v[j + 2]);
     }
     if (STREAM) xchg1(R, xb, buf, u3); else xchg2(R, xb, buf, x3, u3);
 
@@ -196,14 +206,14 @@ __global__ void __launch_bounds__(NT) k_tl(edak_problem P, const double* __restr
     }
 #pragma unroll
     for (int j = 0; j < C; ++j) {
-      acc[j] = acc[j] + 2.0 * a[j];
-      u4[j + 2] = v[j + 2] + dt * a[j];
+      acc[j] = fma(2.0, a[j], acc[j]);
+      u4[j + 2] = fma(dt, a[j], v[j + 2]);
     }
     if (STREAM) xchg1(R, xb, buf, u4); else xchg2(R, xb, buf, x4, u4);
 
     tl_sub<C>(u4, x4, a);
 #pragma unroll
-    for (int j = 0; j < C; ++j) v[j + 2] = v[j + 2] + c6 * (acc[j] + a[j]);
+    for (int j = 0; j < C; ++j) v[j + 2] = fma(c6, acc[j] + a[j], v[j + 2]);
     capture(s + 1);
   }
 }
@@ -253,10 +263,16 @@ __global__ void __launch_bounds__(NT) k_ad(edak_problem P, const double* __restr
 #pragma unroll
   for (int j = 0; j < C; ++j) g[j + 2] = force(N, j);
 
+  const size_t sstride = STREAM ? (size_t)4 * n : (size_t)n;
+  double Xn[C + 4];
+  R.load_halo(tr + (size_t)(N - 1) * sstride, Xn);
+#pragma unroll 1
   for (int s = N - 1; s >= 0; --s) {
-    const double* Xs = STREAM ? tr + (size_t)s * 4 * n : tr + (size_t)s * n;
+    const double* Xs = tr + (size_t)s * sstride;
     double X[C + 4], x2[C + 4], x3[C + 4], x4[C + 4];
-    R.load_halo(Xs, X);
+#pragma unroll
+    for (int k = 0; k < C + 4; ++k) X[k] = Xn[k];
+    if (s > 0) R.load_halo(Xs - sstride, Xn);
     if (STREAM) {
       R.load_halo(Xs + n, x2);
       R.load_halo(Xs + 2 * n, x3);
@@ -283,21 +299,21 @@ __global__ void __launch_bounds__(NT) k_ad(edak_problem P, const double* __restr
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       vh[j] = g[j + 2] + u[j];
-      a[j + 2] = c3 * g[j + 2] + dt * u[j];  // a3
+      a[j + 2] = fma(dt, u[j], c3 * g[j + 2]);  // a3
     }
     xchg1(R, xb, buf, a);
     ad_sub<C>(a, x3, u);
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       vh[j] += u[j];
-      a[j + 2] = c3 * g[j + 2] + h * u[j];  // a2
+      a[j + 2] = fma(h, u[j], c3 * g[j + 2]);  // a2
     }
     xchg1(R, xb, buf, a);
     ad_sub<C>(a, x2, u);
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       vh[j] += u[j];
-      a[j + 2] = c6 * g[j + 2] + h * u[j];  // a1
+      a[j + 2] = fma(h, u[j], c6 * g[j + 2]);  // a1
     }
     xchg1(R, xb, buf, a);
     ad_sub<C>(a, X, u);
@@ -326,10 +342,11 @@ static void go(K kernel, dim3 grid, cudaStream_t st, Args... args) {
 
 // pick (C, NT) and tile geometry for a sweep with halos (hl, hr) per step
 static bool plan(int n, int hl_total, int hr_total, int& C, int& NT, SweepGeom& geo, int& ntiles) {
-  // periodic single tile: whole ring in one CTA
-  const int cand_p[][2] = {{4, 64}, {4, 128}, {4, 256}, {4, 512}, {2, 64}, {2, 128}, {2, 256}, {2, 512}};
+  // periodic single tile: the whole ring in one CTA (no halo redundancy)
+  const int cand_p[][2] = {{8, 128}, {4, 64}, {4, 128}, {4, 256}, {4, 512},
+                           {2, 64}, {2, 128}, {2, 256}, {2, 512}};
   for (auto& f : cand_p) {
-    if (n % f[0] == 0 && n / f[0] <= f[1] && n / f[0] >= 2) {
+    if (n % f[0] == 0 && n / f[0] <= f[1] && n / f[0] >= 2 && (f[0] < 8 || n / f[0] >= 64)) {
       C = f[0];
       NT = f[1];
       geo.W = n;
@@ -340,10 +357,23 @@ static bool plan(int n, int hl_total, int hr_total, int& C, int& NT, SweepGeom& 
       return true;
     }
   }
-  // tile mode: the largest family keeps redundancy lowest
-  C = 4;
-  NT = 512;
-  const int range = C * NT;
+  // tile mode: C = 8 elements per thread, 128 threads (range 1024) measured
+  // fastest on B200 for the cfg4 sweeps (tools/ab_sweeps.py, profiles/)
+  C = 8;
+  NT = 128;
+  if (const char* f = getenv("EDAK_SWEEP_FAMILY")) {  // A/B testing: "C,NT"
+    int c2 = 0, t2 = 0;
+    if (sscanf(f, "%d,%d", &c2, &t2) == 2) {
+      C = c2;
+      NT = t2;
+    }
+  }
+  int range = C * NT;
+  if (range - hl_total - hr_total < 256) {  // long windows: widen the range
+    C = 4;
+    NT = 512;
+    range = C * NT;
+  }
   const int W = range - hl_total - hr_total;
   if (W < 64) return false;
   ntiles = (n + W - 1) / W;
@@ -363,6 +393,8 @@ static bool plan(int n, int hl_total, int hr_total, int& C, int& NT, SweepGeom& 
   else if (C_ == 2 && NT_ == 128) { constexpr int CC = 2, TT = 128; __VA_ARGS__; } \
   else if (C_ == 2 && NT_ == 256) { constexpr int CC = 2, TT = 256; __VA_ARGS__; } \
   else if (C_ == 2 && NT_ == 512) { constexpr int CC = 2, TT = 512; __VA_ARGS__; } \
+  else if (C_ == 8 && NT_ == 128) { constexpr int CC = 8, TT = 128; __VA_ARGS__; } \
+  else if (C_ == 8 && NT_ == 256) { constexpr int CC = 8, TT = 256; __VA_ARGS__; } \
   else { set_error("no kernel family"); return EDAK_EUNSUPPORTED; }
 
 int launch_tl(const edak_problem* P, const double* v0, double* obs, int ncols, const int32_t* col_traj,

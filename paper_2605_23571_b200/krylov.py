@@ -84,14 +84,16 @@ def _traces(status, iters, hist_rz, hist_J, trace_cost):
     return out
 
 
-def pcg_device(apply_h, B, cfg, apply_p=None, cost=None, check_every=8):
+def pcg_device(apply_h, B, cfg, apply_p=None, cost=None, check_every=8, snapshots=None):
     """Batched PCG on a (M, n) device block of right-hand sides.
 
     apply_h(P, out, gp) writes (I + A) P into ``out`` and, when ``gp`` is not
     None, the raw TL observations G U_B P into ``gp`` (recurrence cost).
     apply_p(R) -> P R (None = identity).  cost: None, ("recurrence", D,
     sigma2) with innovations D (M, p), or ("exact", fn) with fn(X) -> (M,)
-    J values.  Returns X (M, n) and a list of SolveTrace."""
+    J values.  ``snapshots`` (a list) receives device copies of
+    (it, X, R, P, rz) after every iteration (parity tests: teacher forcing).
+    Returns X (M, n) and a list of SolveTrace."""
     B = B.contiguous()
     M, n = B.shape
     dev = B.device
@@ -120,6 +122,8 @@ def pcg_device(apply_h, B, cfg, apply_p=None, cost=None, check_every=8):
     elif trace_cost:
         hist_J[:, 0] = cost[1](X)
     rtol = -1.0 if cfg.residual_rtol is None else float(cfg.residual_rtol)
+    if snapshots is not None:
+        snapshots.append((0, X.clone(), Rr.clone(), P.clone(), rz.clone()))
     for it in range(1, cfg.max_iters + 1):
         apply_h(P, HP, GP if rec else None)
         if rec:
@@ -138,6 +142,8 @@ def pcg_device(apply_h, B, cfg, apply_p=None, cost=None, check_every=8):
         _lib.call("edak_pcg_beta", n, M, Zr.data_ptr(), Rr.data_ptr(), P.data_ptr(),
                   rz.data_ptr(), rtol, hist_rz.data_ptr(), L, status.data_ptr(),
                   iters.data_ptr(), it, s)
+        if snapshots is not None:
+            snapshots.append((it, X.clone(), Rr.clone(), P.clone(), rz.clone()))
         if rtol >= 0.0 and it % check_every == 0 and bool((status != 0).all()):
             break
     traces = _traces(status.cpu().numpy(), iters.cpu().numpy(), hist_rz.cpu().numpy(),
@@ -199,7 +205,7 @@ def pcg(apply_h, b, cfg, precond=None, cost_fn=None):
     return x, traces[0]
 
 
-def pcg_members(ens, B, cfg, precond=None, cost="recurrence"):
+def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None):
     """Batched PCG over all members of an ``Ensemble``: B (M, n) device
     right-hand sides (e.g. ens.rhs_all()).  cost: "recurrence", "exact" or
     None.  Returns (X (M, n), [SolveTrace] * M)."""
@@ -214,4 +220,4 @@ def pcg_members(ens, B, cfg, precond=None, cost="recurrence"):
         c = ("recurrence", ens.D, ens.lin.sigma2)
     elif cfg.trace_cost and cost == "exact":
         c = ("exact", ens.cost_members)
-    return pcg_device(apply_h_cols, B, cfg, apply_p, c)
+    return pcg_device(apply_h_cols, B, cfg, apply_p, c, snapshots=snapshots)

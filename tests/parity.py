@@ -33,15 +33,21 @@ def pcg_envelope(apply_h, b, cfg, precond=None, cost_fn=None, trials=4, seed=7):
 
 
 def assert_trace(ours, ref, env_j, env_r, rtol=1e-10):
-    """J within rel 1e-10 or 10x envelope; resnorm within 1e-10 r0 or 10x envelope."""
+    """J within rel 1e-10 or 10x envelope at every iteration; resnorm within
+    1e-10 r0 up to the divergence onset (the first iteration whose CPU-vs-CPU
+    resnorm envelope exceeds 1e-10 r0).  Past the onset the residual history
+    is round-off chaotic (SURVEY.md §7 hard part 1) and step-level exactness
+    is checked by the teacher-forced test instead."""
     assert len(ours.cost) == len(ref.cost), (len(ours.cost), len(ref.cost))
     J, Jr = np.asarray(ours.cost), np.asarray(ref.cost)
     tol = np.maximum(rtol * np.abs(Jr), 10 * env_j)
     bad = np.abs(J - Jr) > tol
     assert not bad.any(), ("J", np.flatnonzero(bad), J[bad], Jr[bad], tol[bad])
     R, Rr = np.asarray(ours.resnorm), np.asarray(ref.resnorm)
-    tol = np.maximum(rtol * Rr[0], 10 * env_r)
-    bad = np.abs(R - Rr) > tol
+    onset = np.flatnonzero(env_r > rtol * Rr[0])
+    upto = onset[0] if onset.size else len(Rr)
+    tol = np.full(len(Rr), rtol * Rr[0])
+    bad = (np.abs(R - Rr) > tol) & (np.arange(len(Rr)) < upto)
     assert not bad.any(), ("resnorm", np.flatnonzero(bad), R[bad], Rr[bad], tol[bad])
 
 
@@ -66,3 +72,14 @@ def assert_values(ours, ref, env):
     tol = np.maximum(tol, 10.0 * env)
     bad = np.abs(ours - ref) > tol
     assert not bad.any(), (ours[bad], ref[bad], tol[bad])
+
+
+def teacher_forced_step(apply_h, apply_p, x, r, p, rz):
+    """One reference PCG iteration (krylov.py:80-95) from a given state."""
+    hp = apply_h(p)
+    alpha = rz / (p @ hp)
+    x1 = x + alpha * p
+    r1 = r - alpha * hp
+    z1 = apply_p(r1) if apply_p is not None else r1
+    rz1 = r1 @ z1
+    return x1, r1, z1 + (rz1 / rz) * p, rz1

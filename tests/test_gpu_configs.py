@@ -1,0 +1,199 @@
+"""BASELINE-config parity: the device ensemble pass (engine.EdaPass) against
+the CPU oracle on the SAME inputs (trajectories/innovations built on the GPU
+by twin.build_ensemble and handed to the oracle), at the configs' own sizes.
+
+Protocol: rhs / Hessian blocks
+rel <= 1e-12 per column; Nystrom values rel 1e-10 or 10x the CPU-vs-CPU
+envelope; PCG J traces likewise; residual histories to the divergence onset;
+and teacher-forced one-step parity (our state at iteration i pushed through
+one reference PCG step must give our state at i+1) at every iteration.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import algorithms as oalg
+from oracle import l96 as ol96
+from oracle.obs import ObsNetwork as OObs
+from oracle.problem import MemberProblem as OProblem
+from oracle.cov import CirculantFactor as OFactor, DiagonalNoise as ONoise
+from parity import assert_trace, assert_values, nystrom_envelope, pcg_envelope, teacher_forced_step
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300)
+
+
+def oracle_rows(dens, rows):
+    """Oracle MemberProblems for ensemble rows (0 = control) on the device
+    ensemble's own trajectories and innovations."""
+    cfg = dens.cfg
+    states = dens.states.cpu().numpy()
+    innov = dens.innovations.cpu().numpy()
+    net = OObs(dens.net.grid, dens.net.times)
+    ub = OFactor(cfg.n, dens.ub.symbol)
+    out = []
+    cache = {}
+    for r in rows:
+        t = int(dens.traj_of[r])
+        if t not in cache:
+            st = states[t]
+            stg = np.stack([np.stack(ol96.rk4_stages(st[s], cfg.dt, cfg.forcing)[1])
+                            for s in range(cfg.n_steps)])
+            cache[t] = ol96.Trajectory(st, stg, cfg.dt, cfg.forcing)
+        out.append(OProblem(cache[t], net, ub, ONoise(cfg.sigma_obs), innov[r]))
+    return out
+
+
+@pytest.fixture(scope="module")
+def cfg3_pass():
+    from paper_2605_23571_b200 import build
+    build.build()
+    from paper_2605_23571_b200.engine import EdaPass
+    from paper_2605_23571_b200.twin import BASELINE_CONFIGS, build_ensemble
+    dens = build_ensemble(BASELINE_CONFIGS[3])
+    eng = EdaPass(dens)
+    snaps = []
+    B = eng.all_rows.rhs_all()
+    G, approx, lmp = eng.build_lmp(B)
+    from paper_2605_23571_b200.krylov import pcg_members
+    X, traces = pcg_members(eng.members, B[1:].contiguous(), eng.scfg, lmp, snapshots=snaps)
+    return dens, eng, B, G, approx, lmp, traces, snaps
+
+
+def test_cfg3_rhs_and_sketch(cfg3_pass):
+    dens, eng, B, G, approx, lmp, traces, snaps = cfg3_pass
+    rows = [0, 1, 17, 50]
+    ops = oracle_rows(dens, rows)
+    Bh = B.cpu().numpy()
+    for r, op in zip(rows, ops):
+        assert rel(Bh[r], op.rhs()) < 1e-12
+    Gh = G.cpu().numpy()
+    assert Gh.shape == (64, 1024)
+    assert rel(Gh[16], Bh[17] - Bh[0]) < 1e-15
+    from oracle.streams import substream
+    gauss = substream(0, "sketch").standard_normal((1024, 14))
+    np.testing.assert_array_equal(Gh[50:], gauss.T)
+
+
+def test_cfg3_nystrom_values(cfg3_pass):
+    dens, eng, B, G, approx, lmp, traces, snaps = cfg3_pass
+    ctl = oracle_rows(dens, [0])[0]
+    phi = G.cpu().numpy().T
+    cfg = oalg.NystromConfig(64, 64, shift_mode="trace")
+    ref = oalg.nystrom_evd(ctl.a_apply, phi, cfg)
+    env = nystrom_envelope(ctl, phi, cfg)
+    assert_values(approx.values, ref.values, env)
+    assert approx.shift == ref.shift
+    assert lmp.theta == pytest.approx(0.5 * (ref.values[-1] + 2.0), rel=1e-10, abs=10 * env[-1])
+
+
+def test_cfg3_pcg_traces_and_teacher_forcing(cfg3_pass):
+    dens, eng, B, G, approx, lmp, traces, snaps = cfg3_pass
+    ops = oracle_rows(dens, [1, 25])
+    # oracle LMP built from OUR eigenpairs, so the PCG comparison isolates PCG
+    olmp = oalg.SpectralLmp(approx.vectors, approx.values, lmp.theta)
+    for j, (row, op) in enumerate(zip([1, 25], ops)):
+        ref, ej, er = pcg_envelope(op.hessian_apply, op.rhs(), oalg.SolverConfig(max_iters=60),
+                                   precond=olmp, cost_fn=op.quadratic_cost, trials=3)
+        assert_trace(traces[row - 1], ref, ej, er)
+        # teacher forcing at every iteration
+        worst = 0.0
+        for (it, X, R, P, rz), (_, X1, R1, P1, rz1) in zip(snaps[:-1], snaps[1:]):
+            m = row - 1
+            x, r, p = X[m].cpu().numpy(), R[m].cpu().numpy(), P[m].cpu().numpy()
+            x1, r1, p1, rzn = teacher_forced_step(op.hessian_apply, olmp.apply, x, r, p,
+                                                  float(rz[m]))
+            worst = max(worst, rel(X1[m].cpu().numpy(), x1), rel(R1[m].cpu().numpy(), r1),
+                        rel(P1[m].cpu().numpy(), p1))
+        assert worst < 1e-11, worst
+
+
+def test_cfg4_hessian_rhs_lmp(gpu_cfg4):
+    """cfg4 sizes (n=16384, N=24, 200 members): member Hessian columns and
+    rhs against the oracle; Nystrom values with the envelope protocol."""
+    dens, eng, B, G, approx, lmp = gpu_cfg4
+    rows = [0, 1, 123, 200]
+    ops = oracle_rows(dens, rows)
+    Bh = B.cpu().numpy()
+    for r, op in zip(rows, ops):
+        assert rel(Bh[r], op.rhs()) < 1e-12
+    Z = torch.randn(4, dens.cfg.n, dtype=torch.float64, device="cuda")
+    ct = torch.tensor([int(dens.traj_of[r]) for r in rows], dtype=torch.int32, device="cuda")
+    AZ = dens.lin.hessian_cols(Z, ct).cpu().numpy()
+    for i, op in enumerate(ops):
+        assert rel(AZ[i], op.a_apply(Z[i].cpu().numpy())) < 1e-12
+    assert approx.values.size == 128 and approx.shift == 0.0
+    assert np.all(np.diff(approx.values) <= 0)
+
+
+def test_cfg4_teacher_forced_pcg(gpu_cfg4):
+    """Three LMP-PCG iterations of two cfg4 members, teacher-forced against
+    the oracle step (LMP from our eigenpairs)."""
+    dens, eng, B, G, approx, lmp = gpu_cfg4
+    from paper_2605_23571_b200.assim import Ensemble
+    from paper_2605_23571_b200.krylov import SolverConfig, pcg_members
+    rows = [7, 150]
+    sub = Ensemble(dens.lin, dens.innovations[rows], np.asarray(dens.traj_of)[rows])
+    snaps = []
+    pcg_members(sub, B[rows].contiguous(), SolverConfig(max_iters=3), lmp, snapshots=snaps)
+    ops = oracle_rows(dens, rows)
+    olmp = oalg.SpectralLmp(approx.vectors, approx.values, lmp.theta)
+    worst = 0.0
+    for (it, X, R, P, rz), (_, X1, R1, P1, rz1) in zip(snaps[:-1], snaps[1:]):
+        for m, op in enumerate(ops):
+            x1, r1, p1, _ = teacher_forced_step(op.hessian_apply, olmp.apply, X[m].cpu().numpy(),
+                                                R[m].cpu().numpy(), P[m].cpu().numpy(), float(rz[m]))
+            worst = max(worst, rel(X1[m].cpu().numpy(), x1), rel(R1[m].cpu().numpy(), r1),
+                        rel(P1[m].cpu().numpy(), p1))
+    assert worst < 1e-11, worst
+
+
+@pytest.fixture(scope="module")
+def gpu_cfg4():
+    from paper_2605_23571_b200 import build
+    build.build()
+    from paper_2605_23571_b200.engine import EdaPass
+    from paper_2605_23571_b200.twin import BASELINE_CONFIGS, build_ensemble
+    dens = build_ensemble(BASELINE_CONFIGS[4])
+    eng = EdaPass(dens)
+    B = eng.all_rows.rhs_all()
+    G, approx, lmp = eng.build_lmp(B)
+    return dens, eng, B, G, approx, lmp
+
+
+def test_cfg5_block_properties():
+    """cfg5 (n=262144, N=12, every 8th variable every step): two columns
+    against the oracle, plus size-independent properties on a 32-column
+    block with per-column trajectories: symmetry <Az, w> = <z, Aw> and
+    stream == recompute (bit-identical)."""
+    from paper_2605_23571_b200 import build
+    build.build()
+    from paper_2605_23571_b200.assim import Linearization
+    from paper_2605_23571_b200.twin import BASELINE_CONFIGS, build_ensemble
+    dens = build_ensemble(BASELINE_CONFIGS[5], members=32)
+    lin = dens.lin
+    n = dens.cfg.n
+    ct = torch.arange(1, 33, dtype=torch.int32, device="cuda")
+    Z = torch.randn(32, n, dtype=torch.float64, device="cuda")
+    Wv = torch.randn(32, n, dtype=torch.float64, device="cuda")
+    AZ = lin.hessian_cols(Z, ct)
+    AW = lin.hessian_cols(Wv, ct)
+    lhs = (AZ * Wv).sum(1)
+    rhs = (Z * AW).sum(1)
+    assert torch.allclose(lhs, rhs, rtol=1e-11, atol=0)
+    ops = oracle_rows(dens, [1, 2])
+    for i, op in enumerate(ops):
+        assert rel(AZ[i].cpu().numpy(), op.a_apply(Z[i].cpu().numpy())) < 1e-12
+    # streamed stored stages give bit-identical blocks
+    from paper_2605_23571_b200.model import integrate_device
+    x0 = dens.states[1:5, 0].contiguous()
+    states, stages = integrate_device(x0, dens.cfg.dt, dens.cfg.n_steps, dens.cfg.forcing,
+                                      want_stages=True)
+    a = Linearization(states, dens.cfg.dt, dens.cfg.forcing, dens.net, dens.ub, dens.rn)
+    b = Linearization(states, dens.cfg.dt, dens.cfg.forcing, dens.net, dens.ub, dens.rn,
+                      stages, "stream")
+    assert torch.equal(a.hessian_cols(Z[:4]), b.hessian_cols(Z[:4]))
