@@ -157,26 +157,29 @@ int edak_svd_jacobi(const double* M, int rows, int cols, double* U, double* sig,
  * status: 0 running, 1 stopped (converged), 2 p.Hp <= 0 at iters[c]
  * (krylov.py:82-84), 3 r.Pr < 0 at start (krylov.py:73-74).  hist_* are
  * (ncols x hist_ld) row-major histories indexed by iteration. */
+/* workspace (doubles) of the batched PCG: per-member tile partials of the
+ * fixed-order dot products and the double-buffered r.z */
+int64_t edak_pcg_work_doubles(int n, int ncols);
 /* x = 0, r = b, p = z (= P b), rz = r.z, hist_rz[.,0] = rz (krylov.py:68-78) */
 int edak_pcg_init(int n, int ncols, const double* b, const double* z, double* x,
-                  double* r, double* p, double* rz, double* hist_rz, int hist_ld,
+                  double* r, double* p, double* work, double* hist_rz, int hist_ld,
                   int32_t* status, int32_t* iters, void* stream);
-/* J(0) = 1/2 d.R^-1 d and m = G U_B x = 0 (cost recurrence state) */
-int edak_pcg_cost0(int p_obs, int ncols, const double* d, double* m,
-                   double sigma2, double* hist_J, int hist_ld, void* stream);
+/* hist_J[., 0] = J(0) = 1/2 d.R^-1 d (assim.py:79-82 at z = 0) */
+int edak_pcg_cost0(int p_obs, int ncols, const double* d, double sigma2,
+                   double* hist_J, int hist_ld, void* stream);
 /* php = p.hp, breakdown test, alpha = rz/php, x += alpha p, r -= alpha hp;
- * if hist_J: m += alpha * gp (gp = G U_B p, raw TL obs of the Hessian apply)
- * and hist_J[., it] = 1/2 x.x + 1/2 (m-d).R^-1(m-d)  (krylov.py:79-89,108-113) */
+ * if b (the rhs block) is not NULL, the partials of x.(b + r) that give
+ * J(x_it) = J(0) - 1/2 x.(b + r) (J identity, (I+A)x = b - r;
+ * krylov.py:79-89,108-113) */
 int edak_pcg_alpha(int n, int ncols, const double* p, const double* hp,
-                   double* x, double* r, const double* rz, int32_t* status,
-                   int32_t* iters, int it, int p_obs, const double* gp, double* m,
-                   const double* d, double sigma2, double* hist_J, int hist_ld,
-                   void* stream);
-/* rz_new = r.z, hist_rz[., it], stop test (rtol < 0 = None), p = z + beta p
- * (krylov.py:86-96) */
+                   double* x, double* r, double* work, int32_t* status,
+                   int32_t* iters, int it, const double* b, void* stream);
+/* rz_new = r.z, hist_rz[., it] (+ hist_J[., it] when not NULL), stop test
+ * (rtol < 0 = None), p = z + beta p (krylov.py:86-96) */
 int edak_pcg_beta(int n, int ncols, const double* z, const double* r, double* p,
-                  double* rz, double rtol, double* hist_rz, int hist_ld,
-                  int32_t* status, int32_t* iters, int it, void* stream);
+                  double* work, double rtol, double* hist_rz, double* hist_J,
+                  int hist_ld, int32_t* status, int32_t* iters, int it,
+                  void* stream);
 /* z = r + S diag(coef) S^T r -- one symmetric factor of the spectral LMP
  * (SpectralLmp._project / apply_sqrt, lmp.py:62-70); with coef =
  * theta/(lam+1) - 1 and orthonormal S it is P itself (lmp.py:72-74). */

@@ -49,11 +49,11 @@ _PROTOS = {
     "edak_trinv_upper": (C.c_int, [vp, C.c_int, vp, vp]),
     "edak_svd_work_doubles": (i64, [C.c_int, C.c_int]),
     "edak_svd_jacobi": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, vp, vp, vp]),
+    "edak_pcg_work_doubles": (i64, [C.c_int, C.c_int]),
     "edak_pcg_init": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, vp, C.c_int, vp, vp, vp]),
-    "edak_pcg_cost0": (C.c_int, [C.c_int, C.c_int, vp, vp, f64, vp, C.c_int, vp]),
-    "edak_pcg_alpha": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int,
-                                 vp, vp, vp, f64, vp, C.c_int, vp]),
-    "edak_pcg_beta": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, vp, f64, vp, C.c_int, vp, vp,
+    "edak_pcg_cost0": (C.c_int, [C.c_int, C.c_int, vp, f64, vp, C.c_int, vp]),
+    "edak_pcg_alpha": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]),
+    "edak_pcg_beta": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, vp, f64, vp, vp, C.c_int, vp, vp,
                                 C.c_int, vp]),
     "edak_lmp_work_doubles": (i64, [C.c_int, C.c_int, C.c_int]),
     "edak_lmp_apply": (C.c_int, [C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp]),

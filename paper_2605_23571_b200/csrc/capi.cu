@@ -42,13 +42,14 @@ int launch_potrf_shifted(const double*, int, double*, int, double, double*, int3
 int launch_trinv_upper(const double*, int, double*, cudaStream_t);
 int64_t svd_work_doubles(int, int);
 int launch_svd_jacobi(const double*, int, int, double*, double*, double*, double*, cudaStream_t);
+int64_t pcg_work_doubles(int, int);
 int launch_pcg_init(int, int, const double*, const double*, double*, double*, double*, double*, double*, int,
                     int32_t*, int32_t*, cudaStream_t);
-int launch_pcg_alpha(int, int, const double*, const double*, double*, double*, const double*, int32_t*, int32_t*,
-                     int, int, const double*, double*, const double*, double, double*, int, cudaStream_t);
-int launch_pcg_beta(int, int, const double*, const double*, double*, double*, double, double*, int, int32_t*,
-                    int32_t*, int, cudaStream_t);
-int launch_pcg_cost0(int, int, const double*, double*, double, double*, int, cudaStream_t);
+int launch_pcg_alpha(int, int, const double*, const double*, double*, double*, double*, int32_t*, int32_t*, int,
+                     const double*, cudaStream_t);
+int launch_pcg_beta(int, int, const double*, const double*, double*, double*, double, double*, double*, int,
+                    int32_t*, int32_t*, int, cudaStream_t);
+int launch_pcg_cost0(int, int, const double*, double, double*, int, cudaStream_t);
 int launch_cost(int, int, int, const double*, const double*, const double*, double, double*, cudaStream_t);
 
 static bool bad_problem(const edak_problem* P) {
@@ -192,30 +193,33 @@ int edak_svd_jacobi(const double* M, int rows, int cols, double* U, double* sig,
   return launch_svd_jacobi(M, rows, cols, U, sig, V, work, as_stream(stream));
 }
 
-int edak_pcg_init(int n, int ncols, const double* b, const double* z, double* x, double* r, double* p, double* rz,
+int64_t edak_pcg_work_doubles(int n, int ncols) { return pcg_work_doubles(n, ncols); }
+
+int edak_pcg_init(int n, int ncols, const double* b, const double* z, double* x, double* r, double* p, double* work,
                   double* hist_rz, int hist_ld, int32_t* status, int32_t* iters, void* stream) {
   if (ncols == 0) return EDAK_OK;
-  return launch_pcg_init(n, ncols, b, z, x, r, p, rz, hist_rz, hist_ld, status, iters, as_stream(stream));
+  if (!b || !z || !x || !r || !p || !work || !hist_rz || !status || !iters) return EDAK_EINVAL;
+  return launch_pcg_init(n, ncols, b, z, x, r, p, work, hist_rz, hist_ld, status, iters, as_stream(stream));
 }
 
-int edak_pcg_cost0(int p_obs, int ncols, const double* d, double* m, double sigma2, double* hist_J, int hist_ld,
+int edak_pcg_cost0(int p_obs, int ncols, const double* d, double sigma2, double* hist_J, int hist_ld,
                    void* stream) {
   if (ncols == 0) return EDAK_OK;
-  return launch_pcg_cost0(p_obs, ncols, d, m, sigma2, hist_J, hist_ld, as_stream(stream));
+  return launch_pcg_cost0(p_obs, ncols, d, sigma2, hist_J, hist_ld, as_stream(stream));
 }
 
-int edak_pcg_alpha(int n, int ncols, const double* p, const double* hp, double* x, double* r, const double* rz,
-                   int32_t* status, int32_t* iters, int it, int p_obs, const double* gp, double* m, const double* d,
-                   double sigma2, double* hist_J, int hist_ld, void* stream) {
+int edak_pcg_alpha(int n, int ncols, const double* p, const double* hp, double* x, double* r, double* work,
+                   int32_t* status, int32_t* iters, int it, const double* b, void* stream) {
   if (ncols == 0) return EDAK_OK;
-  return launch_pcg_alpha(n, ncols, p, hp, x, r, rz, status, iters, it, p_obs, gp, m, d, sigma2, hist_J, hist_ld,
-                          as_stream(stream));
+  return launch_pcg_alpha(n, ncols, p, hp, x, r, work, status, iters, it, b, as_stream(stream));
 }
 
-int edak_pcg_beta(int n, int ncols, const double* z, const double* r, double* p, double* rz, double rtol,
-                  double* hist_rz, int hist_ld, int32_t* status, int32_t* iters, int it, void* stream) {
+int edak_pcg_beta(int n, int ncols, const double* z, const double* r, double* p, double* work, double rtol,
+                  double* hist_rz, double* hist_J, int hist_ld, int32_t* status, int32_t* iters, int it,
+                  void* stream) {
   if (ncols == 0) return EDAK_OK;
-  return launch_pcg_beta(n, ncols, z, r, p, rz, rtol, hist_rz, hist_ld, status, iters, it, as_stream(stream));
+  return launch_pcg_beta(n, ncols, z, r, p, work, rtol, hist_rz, hist_J, hist_ld, status, iters, it,
+                         as_stream(stream));
 }
 
 int64_t edak_lmp_work_doubles(int n, int k, int ncols) {

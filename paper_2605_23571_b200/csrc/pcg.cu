@@ -1,23 +1,49 @@
 // Batched PCG across ensemble members (krylov.pcg, krylov.py:49-97).
-// One CTA per member column; every reduction is a fixed-order block tree
-// (deterministic).  Per-member status mirrors the reference control flow:
+// Grid = (2048-element tiles) x members; every reduction is a fixed-order
+// tree over tile partials that each CTA recomputes identically (deterministic,
+// no atomics, no inter-CTA races).  Per-member status mirrors the reference control flow:
 //   0 running, 1 stopped ("converged": rz_new <= 0 or residual_rtol met,
 //   krylov.py:90-93), 2 breakdown (p.Hp <= 0 -> the reference raises
 //   "system matrix is not positive definite (iteration it)", krylov.py:82-84),
 //   3 preconditioner not positive definite (krylov.py:73-74).
-// The cost trace J(x_it) (krylov.py:108-113 with assim.py:79-82) is carried
-// by linearity: m_it = G U_B x_it = m_{it-1} + alpha * (G U_B p), where
-// G U_B p is the raw TL observation vector the Hessian apply already made.
+// The cost trace J(x_it) (krylov.py:108-113 with assim.py:79-82) comes from
+// the J identity J(x) = J(0) - 1/2 x.(b + r) (no extra TL sweep).
 #include "common.cuh"
 
 namespace edak {
 
 constexpr int PCG_NT = 256;
+constexpr int PCG_EPT = 8;                   // elements per thread per tile
+constexpr int PCG_TILE = PCG_NT * PCG_EPT;   // 2048 ring elements per CTA
+
+static inline int pcg_tiles(int n) { return (n + PCG_TILE - 1) / PCG_TILE; }
+
+// fixed-order sum of a member's T tile partials: every CTA that needs the
+// value computes it identically (lane-strided then a fixed xor tree)
+__device__ __forceinline__ double sum_parts(const double* __restrict__ part, int T) {
+  double s = 0.0;
+  for (int u = threadIdx.x & 31; u < T; u += 32) s += part[u];
+  return warp_sum(s);
+}
+
+// part[c*T + t] = sum over tile t of a[c][i] * b[c][i]
+__global__ void __launch_bounds__(PCG_NT) k_dot_partial(int n, int T, const double* __restrict__ a,
+                                                        const double* __restrict__ b, double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int c = blockIdx.y, t = blockIdx.x;
+  const size_t o = (size_t)c * n;
+  const int i0 = t * PCG_TILE;
+  const int i1 = min(n, i0 + PCG_TILE);
+  double s = 0.0;
+  for (int i = i0 + threadIdx.x; i < i1; i += PCG_NT) s += a[o + i] * b[o + i];
+  s = block_sum<PCG_NT>(s, sh);
+  if (threadIdx.x == 0) part[(size_t)c * T + t] = s;
+}
 
 __global__ void __launch_bounds__(PCG_NT) k_pcg_init(int n, const double* __restrict__ b,
                                                      const double* __restrict__ z, double* __restrict__ x,
                                                      double* __restrict__ r, double* __restrict__ p,
-                                                     double* __restrict__ rz, double* __restrict__ hist_rz,
+                                                     double* __restrict__ rzb, double* __restrict__ hist_rz,
                                                      int hist_ld, int32_t* __restrict__ status,
                                                      int32_t* __restrict__ iters) {
   __shared__ double sh[32];
@@ -33,104 +59,107 @@ __global__ void __launch_bounds__(PCG_NT) k_pcg_init(int n, const double* __rest
   }
   s = block_sum<PCG_NT>(s, sh);
   if (threadIdx.x == 0) {
-    rz[c] = s;
+    rzb[c] = s;  // buffer 0 = iteration 0
     hist_rz[(size_t)c * hist_ld] = s;
     status[c] = s < 0.0 ? 3 : 0;
     iters[c] = 0;
   }
 }
 
-// php = p.hp; breakdown check; alpha; x += alpha p; r -= alpha hp; cost.
-__global__ void __launch_bounds__(PCG_NT) k_pcg_alpha(int n, const double* __restrict__ p,
+// after p.hp partials: breakdown test, alpha, x += alpha p, r -= alpha hp on
+// this tile; if b != NULL also the tile partial of x.(b + r) for the cost:
+//   J(x) = 1/2 x.(I+A)x - b.x + 1/2 d.R^-1 d  (the J identity of
+//   test_assim.py:52-63) with (I+A)x = b - r  =>  J = J(0) - 1/2 x.(b + r)
+__global__ void __launch_bounds__(PCG_NT) k_pcg_upd_x(int n, int T, int M, const double* __restrict__ p,
                                                       const double* __restrict__ hp, double* __restrict__ x,
-                                                      double* __restrict__ r, const double* __restrict__ rz,
+                                                      double* __restrict__ r, const double* __restrict__ rzb,
                                                       int32_t* __restrict__ status, int32_t* __restrict__ iters,
-                                                      int it, int np_obs, const double* __restrict__ gp,
-                                                      double* __restrict__ m, const double* __restrict__ d,
-                                                      double sigma2, double* __restrict__ hist_J, int hist_ld) {
+                                                      int it, const double* __restrict__ part_a,
+                                                      double* __restrict__ part_x, const double* __restrict__ b) {
   __shared__ double sh[32];
-  __shared__ double s_alpha;
-  __shared__ int s_stop;
-  const int c = blockIdx.x;
+  __shared__ double s_php;
+  const int c = blockIdx.y, t = blockIdx.x;
   if (status[c] != 0) return;
-  const size_t o = (size_t)c * n;
-  double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += PCG_NT) s += p[o + i] * hp[o + i];
-  s = block_sum<PCG_NT>(s, sh);
-  if (threadIdx.x == 0) {
-    s_stop = s <= 0.0;  // krylov.py:82 (NaN does not raise)
-    if (s_stop) {
+  if (threadIdx.x < 32) {
+    const double v = sum_parts(part_a + (size_t)c * T, T);
+    if (threadIdx.x == 0) s_php = v;
+  }
+  __syncthreads();
+  const double php = s_php;
+  if (php <= 0.0) {  // krylov.py:82-84 (NaN does not raise)
+    if (t == 0 && threadIdx.x == 0) {
       status[c] = 2;
       iters[c] = it;
     }
-    s_alpha = rz[c] / s;
+    return;
   }
-  __syncthreads();
-  if (s_stop) return;
-  const double alpha = s_alpha;
-  double xx = 0.0;
-  for (int i = threadIdx.x; i < n; i += PCG_NT) {
-    const double xi = x[o + i] + alpha * p[o + i];
-    x[o + i] = xi;
-    r[o + i] = r[o + i] - alpha * hp[o + i];
-    xx += xi * xi;
-  }
-  if (hist_J) {
-    double mm = 0.0;
-    const size_t q0 = (size_t)c * np_obs;
-    for (int q = threadIdx.x; q < np_obs; q += PCG_NT) {
-      const double mq = m[q0 + q] + alpha * gp[q0 + q];
-      m[q0 + q] = mq;
-      const double e = mq - d[q0 + q];
-      mm += e * (e / sigma2);
-    }
-    xx = block_sum<PCG_NT>(xx, sh);
-    mm = block_sum<PCG_NT>(mm, sh);
-    if (threadIdx.x == 0) hist_J[(size_t)c * hist_ld + it] = 0.5 * xx + 0.5 * mm;
-  }
-}
-
-// rz_new = r.z; record; stop test; p = z + (rz_new / rz) p
-__global__ void __launch_bounds__(PCG_NT) k_pcg_beta(int n, const double* __restrict__ z,
-                                                     const double* __restrict__ r, double* __restrict__ p,
-                                                     double* __restrict__ rz, 
-                                                     double rtol, double* __restrict__ hist_rz, int hist_ld,
-                                                     int32_t* __restrict__ status, int32_t* __restrict__ iters,
-                                                     int it) {
-  __shared__ double sh[32];
-  __shared__ int s_stop;
-  __shared__ double s_beta;
-  const int c = blockIdx.x;
-  if (status[c] != 0) return;
+  const double alpha = rzb[(size_t)((it - 1) & 1) * M + c] / php;
   const size_t o = (size_t)c * n;
-  double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += PCG_NT) s += r[o + i] * z[o + i];
-  s = block_sum<PCG_NT>(s, sh);
-  if (threadIdx.x == 0) {
-    hist_rz[(size_t)c * hist_ld + it] = s;
-    iters[c] = it;
-    const bool stop = s <= 0.0 || (rtol >= 0.0 && sqrt(s) <= rtol * sqrt(hist_rz[(size_t)c * hist_ld]));
-    s_stop = stop;
-    if (stop) status[c] = 1;
-    s_beta = s / rz[c];
-    if (!stop) rz[c] = s;
+  const int i0 = t * PCG_TILE, i1 = min(n, i0 + PCG_TILE);
+  double xbr = 0.0;
+  for (int i = i0 + threadIdx.x; i < i1; i += PCG_NT) {
+    const double xi = x[o + i] + alpha * p[o + i];
+    const double ri = r[o + i] - alpha * hp[o + i];
+    x[o + i] = xi;
+    r[o + i] = ri;
+    if (b) xbr += xi * (b[o + i] + ri);
   }
-  __syncthreads();
-  if (s_stop) return;
-  const double beta = s_beta;
-  for (int i = threadIdx.x; i < n; i += PCG_NT) p[o + i] = z[o + i] + beta * p[o + i];
+  if (b) {
+    xbr = block_sum<PCG_NT>(xbr, sh);
+    if (threadIdx.x == 0) part_x[(size_t)c * T + t] = xbr;
+  }
 }
 
-// initial cost J(0) = 1/2 d.R^-1 d  (misfit = -d, assim.py:81-82) and m = 0
-__global__ void __launch_bounds__(PCG_NT) k_pcg_cost0(int np_obs, const double* __restrict__ d,
-                                                      double* __restrict__ m, double sigma2,
+// after r.z partials: record, stop test, p = z + beta p on this tile
+__global__ void __launch_bounds__(PCG_NT) k_pcg_upd_p(int n, int T, int M, const double* __restrict__ z,
+                                                      double* __restrict__ p, double* __restrict__ rzb,
+                                                      double rtol, double* __restrict__ hist_rz,
+                                                      double* __restrict__ hist_J, int hist_ld,
+                                                      int32_t* __restrict__ status, int32_t* __restrict__ iters,
+                                                      int it, const double* __restrict__ part_r,
+                                                      const double* __restrict__ part_x) {
+  __shared__ double s_rz, s_J;
+  const int c = blockIdx.y, t = blockIdx.x;
+  if (status[c] != 0) return;
+  if (threadIdx.x < 32) {
+    const double v = sum_parts(part_r + (size_t)c * T, T);
+    double J = 0.0;
+    if (hist_J && t == 0) {
+      const double xbr = sum_parts(part_x + (size_t)c * T, T);
+      J = hist_J[(size_t)c * hist_ld] - 0.5 * xbr;
+    }
+    if (threadIdx.x == 0) {
+      s_rz = v;
+      s_J = J;
+    }
+  }
+  __syncthreads();
+  const double rz_new = s_rz;
+  const double rz_old = rzb[(size_t)((it - 1) & 1) * M + c];
+  const bool stop = rz_new <= 0.0 ||
+                    (rtol >= 0.0 && sqrt(rz_new) <= rtol * sqrt(hist_rz[(size_t)c * hist_ld]));
+  if (t == 0 && threadIdx.x == 0) {
+    hist_rz[(size_t)c * hist_ld + it] = rz_new;
+    if (hist_J) hist_J[(size_t)c * hist_ld + it] = s_J;
+    iters[c] = it;
+    rzb[(size_t)(it & 1) * M + c] = rz_new;
+    if (stop) status[c] = 1;
+  }
+  if (stop) return;
+  const double beta = rz_new / rz_old;
+  const size_t o = (size_t)c * n;
+  const int i0 = t * PCG_TILE, i1 = min(n, i0 + PCG_TILE);
+  for (int i = i0 + threadIdx.x; i < i1; i += PCG_NT) p[o + i] = z[o + i] + beta * p[o + i];
+}
+
+// initial cost J(0) = 1/2 d.R^-1 d  (misfit = -d, assim.py:81-82)
+__global__ void __launch_bounds__(PCG_NT) k_pcg_cost0(int np_obs, const double* __restrict__ d, double sigma2,
                                                       double* __restrict__ hist_J, int hist_ld) {
   __shared__ double sh[32];
   const int c = blockIdx.x;
   const size_t q0 = (size_t)c * np_obs;
   double mm = 0.0;
   for (int q = threadIdx.x; q < np_obs; q += PCG_NT) {
-    m[q0 + q] = 0.0;
     const double e = -d[q0 + q];
     mm += e * (e / sigma2);
   }
@@ -138,32 +167,48 @@ __global__ void __launch_bounds__(PCG_NT) k_pcg_cost0(int np_obs, const double* 
   if (threadIdx.x == 0) hist_J[(size_t)c * hist_ld] = 0.5 * mm;
 }
 
-int launch_pcg_init(int n, int ncols, const double* b, const double* z, double* x, double* r, double* p, double* rz,
+// work layout: part_a | part_x | part_m | part_r (M*T each) | rzb (2*M)
+int64_t pcg_work_doubles(int n, int M) { return 4LL * M * pcg_tiles(n) + 2LL * M; }
+
+int launch_pcg_init(int n, int M, const double* b, const double* z, double* x, double* r, double* p, double* work,
                     double* hist_rz, int hist_ld, int32_t* status, int32_t* iters, cudaStream_t st) {
-  k_pcg_init<<<ncols, PCG_NT, 0, st>>>(n, b, z, x, r, p, rz, hist_rz, hist_ld, status, iters);
+  double* rzb = work + 4LL * M * pcg_tiles(n);
+  k_pcg_init<<<M, PCG_NT, 0, st>>>(n, b, z, x, r, p, rzb, hist_rz, hist_ld, status, iters);
   count_launch();
   return check_launch("k_pcg_init");
 }
 
-int launch_pcg_alpha(int n, int ncols, const double* p, const double* hp, double* x, double* r, const double* rz,
-                     int32_t* status, int32_t* iters, int it, int np_obs, const double* gp, double* m,
-                     const double* d, double sigma2, double* hist_J, int hist_ld, cudaStream_t st) {
-  k_pcg_alpha<<<ncols, PCG_NT, 0, st>>>(n, p, hp, x, r, rz, status, iters, it, np_obs, gp, m, d, sigma2, hist_J,
-                                        hist_ld);
-  count_launch();
-  return check_launch("k_pcg_alpha");
+int launch_pcg_alpha(int n, int M, const double* p, const double* hp, double* x, double* r, double* work,
+                     int32_t* status, int32_t* iters, int it, const double* b, cudaStream_t st) {
+  const int T = pcg_tiles(n);
+  double* part_a = work;
+  double* part_x = work + (size_t)M * T;
+  double* rzb = work + 4 * (size_t)M * T;
+  dim3 grid(T, M);
+  k_dot_partial<<<grid, PCG_NT, 0, st>>>(n, T, p, hp, part_a);
+  k_pcg_upd_x<<<grid, PCG_NT, 0, st>>>(n, T, M, p, hp, x, r, rzb, status, iters, it, part_a, part_x, b);
+  count_launch(2);
+  return check_launch("k_pcg_upd_x");
 }
 
-int launch_pcg_beta(int n, int ncols, const double* z, const double* r, double* p, double* rz, double rtol, double* hist_rz, int hist_ld, int32_t* status, int32_t* iters, int it,
+int launch_pcg_beta(int n, int M, const double* z, const double* r, double* p, double* work, double rtol,
+                    double* hist_rz, double* hist_J, int hist_ld, int32_t* status, int32_t* iters, int it,
                     cudaStream_t st) {
-  k_pcg_beta<<<ncols, PCG_NT, 0, st>>>(n, z, r, p, rz, rtol, hist_rz, hist_ld, status, iters, it);
-  count_launch();
-  return check_launch("k_pcg_beta");
+  const int T = pcg_tiles(n);
+  double* part_x = work + (size_t)M * T;
+  double* part_r = work + 3 * (size_t)M * T;
+  double* rzb = work + 4 * (size_t)M * T;
+  dim3 grid(T, M);
+  k_dot_partial<<<grid, PCG_NT, 0, st>>>(n, T, r, z, part_r);
+  k_pcg_upd_p<<<grid, PCG_NT, 0, st>>>(n, T, M, z, p, rzb, rtol, hist_rz, hist_J, hist_ld, status, iters, it,
+                                       part_r, part_x);
+  count_launch(2);
+  return check_launch("k_pcg_upd_p");
 }
 
-int launch_pcg_cost0(int np_obs, int ncols, const double* d, double* m, double sigma2, double* hist_J, int hist_ld,
+int launch_pcg_cost0(int np_obs, int ncols, const double* d, double sigma2, double* hist_J, int hist_ld,
                      cudaStream_t st) {
-  k_pcg_cost0<<<ncols, PCG_NT, 0, st>>>(np_obs, d, m, sigma2, hist_J, hist_ld);
+  k_pcg_cost0<<<ncols, PCG_NT, 0, st>>>(np_obs, d, sigma2, hist_J, hist_ld);
   count_launch();
   return check_launch("k_pcg_cost0");
 }

@@ -110,57 +110,79 @@ int launch_trinv_upper(const double* R, int l, double* X, cudaStream_t st) {
 // V (cols x cols) if Vout != NULL.
 constexpr int JAC_NT = 1024;
 
+// smem_mode: 0 = everything in the global workspace (L2); 1 = A in shared
+// memory; 2 = A and V in shared memory (l <= 128 fits: 128 KB)
 __global__ void __launch_bounds__(JAC_NT) k_svd_jacobi(const double* __restrict__ M, int rows, int cols,
                                                        double* __restrict__ U, double* __restrict__ sig,
-                                                       double* __restrict__ Vout, double* __restrict__ work) {
+                                                       double* __restrict__ Vout, double* __restrict__ work,
+                                                       int smem_mode) {
   __shared__ int rotated;
+  extern __shared__ __align__(16) double jsm[];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = JAC_NT / 32;
-  double* A = work;
-  double* V = work + (size_t)rows * cols;
-  double* nrm = V + (size_t)cols * cols;
+  double* A = smem_mode >= 1 ? jsm : work;
+  double* V = smem_mode >= 2 ? jsm + (size_t)rows * cols : work + (size_t)rows * cols;
+  double* nrm = work + (size_t)rows * cols + (size_t)cols * cols;
   for (size_t e = t; e < (size_t)rows * cols; e += JAC_NT) A[e] = M[e];
-  for (size_t e = t; e < (size_t)cols * cols; e += JAC_NT) V[e] = (e % cols == e / cols) ? 1.0 : 0.0;
+  if (Vout)
+    for (size_t e = t; e < (size_t)cols * cols; e += JAC_NT) V[e] = (e % cols == e / cols) ? 1.0 : 0.0;
   __syncthreads();
   const int m = cols + (cols & 1);  // even tournament size (index `cols` = dummy)
-  const double tol = 4.0 * 2.220446049250313e-16;
+  // LAPACK dgesvj's convergence threshold: sqrt(rows) * eps
+  const double tol = sqrt((double)rows) * 2.220446049250313e-16;
+  // one half-warp (16 lanes) per column pair: 64 pairs in flight per pass.
+  // Both halves of a warp always run the same loop trip count (shuffles use
+  // the full mask); idle halves carry live = false.
+  const int hl = t & 15, half = (t >> 4) & 1;
   for (int sweep = 0; sweep < 40; ++sweep) {
     if (t == 0) rotated = 0;
     __syncthreads();
     for (int rd = 0; rd < m - 1; ++rd) {
-      for (int k = warp; k < m / 2; k += nw) {
-        int p = k == 0 ? 0 : ((k - 1 + rd) % (m - 1)) + 1;
-        int q = ((m - 1 - k - 1 + rd) % (m - 1)) + 1;
-        if (p > q) { int tmp = p; p = q; q = tmp; }
-        if (q >= cols || p == q) continue;
+      for (int k0 = warp * 2; k0 < m / 2; k0 += nw * 2) {
+        const int k = k0 + half;
+        int p = 0, q = 0;
+        bool live = k < m / 2;
+        if (live) {
+          p = k == 0 ? 0 : ((k - 1 + rd) % (m - 1)) + 1;
+          q = ((m - 1 - k - 1 + rd) % (m - 1)) + 1;
+          if (p > q) { int tmp = p; p = q; q = tmp; }
+          live = q < cols && p != q;
+        }
         double* ap = A + (size_t)p * rows;
         double* aq = A + (size_t)q * rows;
         double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = lane; i < rows; i += 32) {
-          const double x = ap[i], y = aq[i];
-          al += x * x;
-          be += y * y;
-          ga += x * y;
+        if (live) {
+          for (int i = hl; i < rows; i += 16) {
+            const double x = ap[i], y = aq[i];
+            al = fma(x, x, al);
+            be = fma(y, y, be);
+            ga = fma(x, y, ga);
+          }
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
-        if (al == 0.0 || be == 0.0 || fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (!live || al == 0.0 || be == 0.0 || fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
         const double zeta = (be - al) / (2.0 * ga);
         const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
-        for (int i = lane; i < rows; i += 32) {
+        for (int i = hl; i < rows; i += 16) {
           const double x = ap[i], y = aq[i];
           ap[i] = c * x - s * y;
           aq[i] = s * x + c * y;
         }
-        double* vp = V + (size_t)p * cols;
-        double* vq = V + (size_t)q * cols;
-        for (int i = lane; i < cols; i += 32) {
-          const double x = vp[i], y = vq[i];
-          vp[i] = c * x - s * y;
-          vq[i] = s * x + c * y;
+        if (Vout) {
+          double* vp = V + (size_t)p * cols;
+          double* vq = V + (size_t)q * cols;
+          for (int i = hl; i < cols; i += 16) {
+            const double x = vp[i], y = vq[i];
+            vp[i] = c * x - s * y;
+            vq[i] = s * x + c * y;
+          }
         }
-        if (lane == 0) rotated = 1;
+        if (hl == 0) rotated = 1;
       }
       __syncthreads();
     }
@@ -206,7 +228,24 @@ int launch_svd_jacobi(const double* M, int rows, int cols, double* U, double* si
     set_error("svd_jacobi needs rows >= cols");
     return EDAK_EINVAL;
   }
-  k_svd_jacobi<<<1, JAC_NT, 0, st>>>(M, rows, cols, U, sig, V, work);
+  const size_t a_bytes = (size_t)rows * cols * sizeof(double);
+  const size_t v_bytes = (size_t)cols * cols * sizeof(double);
+  const size_t limit = 200 * 1024;
+  int mode = 0;
+  size_t smem = 0;
+  if (a_bytes + (V ? v_bytes : 0) <= limit) {
+    mode = 2;
+    smem = a_bytes + (V ? v_bytes : 0);
+  } else if (a_bytes <= limit) {
+    mode = 1;
+    smem = a_bytes;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_svd_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
+    attr = true;
+  }
+  k_svd_jacobi<<<1, JAC_NT, smem, st>>>(M, rows, cols, U, sig, V, work, mode);
   count_launch();
   return check_launch("k_svd_jacobi");
 }

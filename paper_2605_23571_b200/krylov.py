@@ -14,10 +14,11 @@ one launch over all members:
     z = Pr  edak_lmp_apply       (DMMA GEMMs over the whole residual block)
     beta    edak_pcg_beta        (r.z, stop test, p update)
 
-All reductions are fixed-order (deterministic).  The cost trace uses
-linearity, m_i = G U_B x_i = m_{i-1} + alpha_i (G U_B p_i), with G U_B p_i
-taken from the TL half of the Hessian apply, so J costs no extra sweep
-(``cost="exact"`` re-evaluates quadratic_cost with a TL sweep instead).
+All reductions are fixed-order (deterministic).  The cost trace uses the J
+identity J(x) = 1/2 x.(I+A)x - b.x + 1/2 d.R^-1 d (test_assim.py:52-63) with
+(I+A)x = b - r, i.e. J(x_i) = J(0) - 1/2 x_i.(b + r_i): one fused dot in the
+x/r update instead of a TL sweep per iteration (``cost="exact"`` re-evaluates
+quadratic_cost with a TL sweep instead; tests hold the two to 1e-10).
 Per-member status stays on the device; the host reads it once at the end
 (or every ``check_every`` iterations when a residual tolerance can stop
 members early).
@@ -87,8 +88,8 @@ def _traces(status, iters, hist_rz, hist_J, trace_cost):
 def pcg_device(apply_h, B, cfg, apply_p=None, cost=None, check_every=8, snapshots=None):
     """Batched PCG on a (M, n) device block of right-hand sides.
 
-    apply_h(P, out, gp) writes (I + A) P into ``out`` and, when ``gp`` is not
-    None, the raw TL observations G U_B P into ``gp`` (recurrence cost).
+    apply_h(P, out, gp) writes (I + A) P into ``out`` (``gp`` is unused and
+    passed as None).
     apply_p(R) -> P R (None = identity).  cost: None, ("recurrence", D,
     sigma2) with innovations D (M, p), or ("exact", fn) with fn(X) -> (M,)
     J values.  ``snapshots`` (a list) receives device copies of
@@ -100,7 +101,8 @@ def pcg_device(apply_h, B, cfg, apply_p=None, cost=None, check_every=8, snapshot
     L = cfg.max_iters + 1
     X, Rr, P = torch.empty_like(B), torch.empty_like(B), torch.empty_like(B)
     HP = torch.empty_like(B)
-    rz = torch.empty(M, dtype=torch.float64, device=dev)
+    work = torch.empty(int(_lib.lib().edak_pcg_work_doubles(n, M)), dtype=torch.float64,
+                       device=dev)
     hist_rz = torch.zeros((M, L), dtype=torch.float64, device=dev)
     hist_J = torch.full((M, L), float("nan"), dtype=torch.float64, device=dev)
     status = torch.zeros(M, dtype=torch.int32, device=dev)
@@ -108,42 +110,36 @@ def pcg_device(apply_h, B, cfg, apply_p=None, cost=None, check_every=8, snapshot
     s = _lib.stream()
     Z0 = apply_p(B) if apply_p is not None else B
     _lib.call("edak_pcg_init", n, M, B.data_ptr(), Z0.data_ptr(), X.data_ptr(), Rr.data_ptr(),
-              P.data_ptr(), rz.data_ptr(), hist_rz.data_ptr(), L, status.data_ptr(),
+              P.data_ptr(), work.data_ptr(), hist_rz.data_ptr(), L, status.data_ptr(),
               iters.data_ptr(), s)
+    rzb = work[-2 * M:]
     trace_cost = bool(cfg.trace_cost and cost is not None)
     rec = trace_cost and cost[0] == "recurrence"
     if rec:
         D, sigma2 = cost[1].contiguous(), float(cost[2])
-        p_obs = D.shape[1]
-        m_state = torch.empty_like(D)
-        GP = torch.empty_like(D)
-        _lib.call("edak_pcg_cost0", p_obs, M, D.data_ptr(), m_state.data_ptr(), sigma2,
-                  hist_J.data_ptr(), L, s)
+        _lib.call("edak_pcg_cost0", D.shape[1], M, D.data_ptr(), sigma2, hist_J.data_ptr(), L, s)
     elif trace_cost:
         hist_J[:, 0] = cost[1](X)
     rtol = -1.0 if cfg.residual_rtol is None else float(cfg.residual_rtol)
     if snapshots is not None:
-        snapshots.append((0, X.clone(), Rr.clone(), P.clone(), rz.clone()))
+        snapshots.append((0, X.clone(), Rr.clone(), P.clone(), rzb[:M].clone()))
     for it in range(1, cfg.max_iters + 1):
-        apply_h(P, HP, GP if rec else None)
-        if rec:
-            _lib.call("edak_pcg_alpha", n, M, P.data_ptr(), HP.data_ptr(), X.data_ptr(),
-                      Rr.data_ptr(), rz.data_ptr(), status.data_ptr(), iters.data_ptr(), it,
-                      p_obs, GP.data_ptr(), m_state.data_ptr(), D.data_ptr(), sigma2,
-                      hist_J.data_ptr(), L, s)
-        else:
-            _lib.call("edak_pcg_alpha", n, M, P.data_ptr(), HP.data_ptr(), X.data_ptr(),
-                      Rr.data_ptr(), rz.data_ptr(), status.data_ptr(), iters.data_ptr(), it,
-                      0, None, None, None, 1.0, None, L, s)
+        apply_h(P, HP, None)
+        _lib.call("edak_pcg_alpha", n, M, P.data_ptr(), HP.data_ptr(), X.data_ptr(),
+                  Rr.data_ptr(), work.data_ptr(), status.data_ptr(), iters.data_ptr(), it,
+                  B.data_ptr() if rec else None, s)
+        if not rec:
             if trace_cost:
                 run = status == 0
                 hist_J[:, it] = torch.where(run, cost[1](X), hist_J[:, it])
         Zr = apply_p(Rr) if apply_p is not None else Rr
         _lib.call("edak_pcg_beta", n, M, Zr.data_ptr(), Rr.data_ptr(), P.data_ptr(),
-                  rz.data_ptr(), rtol, hist_rz.data_ptr(), L, status.data_ptr(),
-                  iters.data_ptr(), it, s)
+                  work.data_ptr(), rtol, hist_rz.data_ptr(),
+                  hist_J.data_ptr() if rec else None, L, status.data_ptr(), iters.data_ptr(),
+                  it, s)
         if snapshots is not None:
-            snapshots.append((it, X.clone(), Rr.clone(), P.clone(), rz.clone()))
+            snapshots.append((it, X.clone(), Rr.clone(), P.clone(),
+                              rzb[(it & 1) * M:(it & 1) * M + M].clone()))
         if rtol >= 0.0 and it % check_every == 0 and bool((status != 0).all()):
             break
     traces = _traces(status.cpu().numpy(), iters.cpu().numpy(), hist_rz.cpu().numpy(),

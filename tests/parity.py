@@ -14,18 +14,27 @@ import numpy as np
 from oracle import algorithms as oalg
 
 JITTER = 2e-16
+# PCG envelope: two legitimate fp64 PCG implementations differ in the operator
+# (~1e-16 per element) AND in every dot product's summation order (relative
+# error ~ sqrt(n) eps); both are emulated by jittering H p and P r at 1e-15.
+PCG_JITTER = 1e-15
 
 
-def pcg_envelope(apply_h, b, cfg, precond=None, cost_fn=None, trials=4, seed=7):
+def pcg_envelope(apply_h, b, cfg, precond=None, cost_fn=None, trials=6, seed=7):
     """(reference trace, envelope of |dJ|, envelope of |d resnorm|)."""
     _, ref = oalg.pcg(apply_h, b, cfg, precond=precond, cost_fn=cost_fn)
     rng = np.random.default_rng(seed)
     n = len(ref.cost)
     e_j, e_r = np.zeros(n), np.zeros(n)
+    papply = None if precond is None else (precond if callable(precond) else precond.apply)
     for _ in range(trials):
         def h(v):
-            return apply_h(v) * (1 + JITTER * rng.standard_normal(np.shape(v)))
-        _, tr = oalg.pcg(h, b, cfg, precond=precond, cost_fn=cost_fn)
+            return apply_h(v) * (1 + PCG_JITTER * rng.standard_normal(np.shape(v)))
+
+        def pc(v):
+            w = v if papply is None else papply(v)
+            return w * (1 + PCG_JITTER * rng.standard_normal(np.shape(v)))
+        _, tr = oalg.pcg(h, b, cfg, precond=pc, cost_fn=cost_fn)
         m = min(n, len(tr.cost))
         e_j[:m] = np.maximum(e_j[:m], np.abs(np.array(tr.cost[:m]) - ref.cost[:m]))
         e_r[:m] = np.maximum(e_r[:m], np.abs(np.array(tr.resnorm[:m]) - ref.resnorm[:m]))
