@@ -90,13 +90,16 @@ int edak_circ_apply(const edak_problem* P, const double* in, double* out,
                     int ncols, void* stream);
 
 /* ---- window operator halves (obs.py:47-57 over model.py:134-157) ------ */
+/* Sweep workspace: edak_sweep_work_doubles doubles lets long windows run
+ * as chunks of <= 8 steps (smaller redundant halos); NULL = one chunk. */
+int64_t edak_sweep_work_doubles(const edak_problem* P, int ncols);
 /* obs[c] = G_traj(c) v0[c]  (observe_tlm, obs.py:47-50): raw, not R^-1-scaled */
 int edak_tl_sweep(const edak_problem* P, const double* v0, double* obs,
-                  int ncols, const int32_t* col_traj, void* stream);
+                  int ncols, const int32_t* col_traj, double* work, void* stream);
 /* g[c] = G_traj(c)^T (forcing[c] / sigma2)  (observe_adj(rn.solve(.)),
  * obs.py:52-57 with covariance.py:69-71) */
 int edak_ad_sweep(const edak_problem* P, const double* forcing, double* g,
-                  int ncols, const int32_t* col_traj, void* stream);
+                  int ncols, const int32_t* col_traj, double* work, void* stream);
 
 /* ---- member problem (assim.py) -------------------------------------- */
 /* workspace (doubles) needed by edak_hessian_block / edak_rhs / edak_cost */

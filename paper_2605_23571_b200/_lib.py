@@ -35,8 +35,9 @@ _PROTOS = {
     "edak_integrate": (C.c_int, [C.c_int, C.c_int, f64, f64, vp, C.c_int, vp, i64, vp, i64, vp]),
     "edak_observe": (C.c_int, [vp, i64, C.c_int, vp, C.c_int, vp, C.c_int, C.c_int, vp, vp]),
     "edak_circ_apply": (C.c_int, [C.POINTER(Problem), vp, vp, C.c_int, vp]),
-    "edak_tl_sweep": (C.c_int, [C.POINTER(Problem), vp, vp, C.c_int, vp, vp]),
-    "edak_ad_sweep": (C.c_int, [C.POINTER(Problem), vp, vp, C.c_int, vp, vp]),
+    "edak_sweep_work_doubles": (i64, [C.POINTER(Problem), C.c_int]),
+    "edak_tl_sweep": (C.c_int, [C.POINTER(Problem), vp, vp, C.c_int, vp, vp, vp]),
+    "edak_ad_sweep": (C.c_int, [C.POINTER(Problem), vp, vp, C.c_int, vp, vp, vp]),
     "edak_work_doubles": (i64, [C.POINTER(Problem), C.c_int]),
     "edak_hessian_block": (C.c_int, [C.POINTER(Problem), vp, vp, C.c_int, vp, f64, vp, vp, vp]),
     "edak_rhs": (C.c_int, [C.POINTER(Problem), vp, vp, C.c_int, vp, vp, vp]),

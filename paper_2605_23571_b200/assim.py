@@ -114,6 +114,10 @@ class Linearization:
         return torch.empty(int(_lib.lib().edak_work_doubles(_lib.C.byref(self._P), ncols)),
                            dtype=torch.float64, device=self.states.device)
 
+    def sweep_work(self, ncols):
+        k = int(_lib.lib().edak_sweep_work_doubles(_lib.C.byref(self._P), ncols))
+        return torch.empty(k, dtype=torch.float64, device=self.states.device)
+
     def hessian_cols(self, Z, col_traj=None, ident=0.0, obs_out=None, out=None, work=None):
         """out = ident * Z + A Z for a (ncols, n) device block."""
         Z = Z.contiguous()
@@ -132,7 +136,7 @@ class Linearization:
         ncols = D.shape[0]
         ct = self._map(col_traj, ncols)
         out = torch.empty((ncols, self.n), dtype=torch.float64, device=D.device)
-        work = torch.empty((ncols, self.n), dtype=torch.float64, device=D.device)
+        work = torch.empty((3 * ncols, self.n), dtype=torch.float64, device=D.device)
         _lib.call("edak_rhs", _lib.C.byref(self._P), D.data_ptr(), out.data_ptr(), ncols,
                   _lib.ptr(ct), work.data_ptr(), _lib.stream())
         return out
@@ -154,7 +158,7 @@ class Linearization:
         ct = self._map(col_traj, ncols)
         obs = torch.empty((ncols, self.p), dtype=torch.float64, device=V0.device)
         _lib.call("edak_tl_sweep", _lib.C.byref(self._P), V0.data_ptr(), obs.data_ptr(), ncols,
-                  _lib.ptr(ct), _lib.stream())
+                  _lib.ptr(ct), self.sweep_work(ncols).data_ptr(), _lib.stream())
         return obs
 
     def ad_cols(self, W, col_traj=None):
@@ -164,7 +168,7 @@ class Linearization:
         ct = self._map(col_traj, ncols)
         g = torch.empty((ncols, self.n), dtype=torch.float64, device=W.device)
         _lib.call("edak_ad_sweep", _lib.C.byref(self._P), W.data_ptr(), g.data_ptr(), ncols,
-                  _lib.ptr(ct), _lib.stream())
+                  _lib.ptr(ct), self.sweep_work(ncols).data_ptr(), _lib.stream())
         return g
 
 

@@ -25,8 +25,8 @@ int check_launch(const char* what) {
 }
 
 // launchers (l96.cu, circ.cu, blas.cu, small.cu, pcg.cu)
-int launch_tl(const edak_problem*, const double*, double*, int, const int32_t*, cudaStream_t);
-int launch_ad(const edak_problem*, const double*, double*, int, const int32_t*, cudaStream_t);
+int launch_tl(const edak_problem*, const double*, double*, int, const int32_t*, cudaStream_t, double*);
+int launch_ad(const edak_problem*, const double*, double*, int, const int32_t*, cudaStream_t, double*);
 int launch_integrate(int, int, double, double, const double*, int, double*, int64_t, double*, int64_t,
                      cudaStream_t);
 int launch_observe(const double*, int64_t, int, const int32_t*, int, const int32_t*, int, int, double*,
@@ -99,23 +99,29 @@ int edak_circ_apply(const edak_problem* P, const double* in, double* out, int nc
   return launch_circ(P, in, out, ncols, 0.0, nullptr, as_stream(stream));
 }
 
+int64_t edak_sweep_work_doubles(const edak_problem* P, int ncols) {
+  if (!P) return -1;
+  return 2 * (int64_t)ncols * P->n;
+}
+
 int edak_tl_sweep(const edak_problem* P, const double* v0, double* obs, int ncols, const int32_t* col_traj,
-                  void* stream) {
+                  double* work, void* stream) {
   if (bad_problem(P) || !v0 || !obs) return EDAK_EINVAL;
   if (ncols == 0) return EDAK_OK;
-  return launch_tl(P, v0, obs, ncols, col_traj, as_stream(stream));
+  return launch_tl(P, v0, obs, ncols, col_traj, as_stream(stream), work);
 }
 
 int edak_ad_sweep(const edak_problem* P, const double* forcing, double* g, int ncols, const int32_t* col_traj,
-                  void* stream) {
+                  double* work, void* stream) {
   if (bad_problem(P) || !forcing || !g) return EDAK_EINVAL;
   if (ncols == 0) return EDAK_OK;
-  return launch_ad(P, forcing, g, ncols, col_traj, as_stream(stream));
+  return launch_ad(P, forcing, g, ncols, col_traj, as_stream(stream), work);
 }
 
+// v0 | obs | g | sweep chunk hand-over (2 blocks)
 int64_t edak_work_doubles(const edak_problem* P, int ncols) {
   if (!P) return -1;
-  return (int64_t)ncols * (2 * (int64_t)P->n + (int64_t)P->G * P->T);
+  return (int64_t)ncols * (4 * (int64_t)P->n + (int64_t)P->G * P->T);
 }
 
 int edak_hessian_block(const edak_problem* P, const double* z, double* az, int ncols, const int32_t* col_traj,
@@ -127,11 +133,12 @@ int edak_hessian_block(const edak_problem* P, const double* z, double* az, int n
   double* v0 = work;
   double* obs = obs_out ? obs_out : work + ncols * n;
   double* g = work + ncols * (n + p);
+  double* w2 = g + ncols * n;
   int rc;
   // A z = U_B^T G^T R^-1 G U_B z (assim.py:66-68); I + A (assim.py:70-72)
   if ((rc = launch_circ(P, z, v0, ncols, 0.0, nullptr, st))) return rc;
-  if ((rc = launch_tl(P, v0, obs, ncols, col_traj, st))) return rc;
-  if ((rc = launch_ad(P, obs, g, ncols, col_traj, st))) return rc;
+  if ((rc = launch_tl(P, v0, obs, ncols, col_traj, st, w2))) return rc;
+  if ((rc = launch_ad(P, obs, g, ncols, col_traj, st, w2))) return rc;
   return launch_circ(P, g, az, ncols, ident, ident != 0.0 ? z : nullptr, st);
 }
 
@@ -141,7 +148,7 @@ int edak_rhs(const edak_problem* P, const double* innov, double* b, int ncols, c
   if (ncols == 0) return EDAK_OK;
   cudaStream_t st = as_stream(stream);
   int rc;
-  if ((rc = launch_ad(P, innov, work, ncols, col_traj, st))) return rc;
+  if ((rc = launch_ad(P, innov, work, ncols, col_traj, st, work + (size_t)ncols * P->n))) return rc;
   return launch_circ(P, work, b, ncols, 0.0, nullptr, st);
 }
 
@@ -154,9 +161,10 @@ int edak_cost(const edak_problem* P, const double* z, const double* innov, doubl
   const int p = P->G * P->T;
   double* v0 = work;
   double* obs = work + ncols * n;
+  double* w2 = obs + (size_t)ncols * p;
   int rc;
   if ((rc = launch_circ(P, z, v0, ncols, 0.0, nullptr, st))) return rc;
-  if ((rc = launch_tl(P, v0, obs, ncols, col_traj, st))) return rc;
+  if ((rc = launch_tl(P, v0, obs, ncols, col_traj, st, w2))) return rc;
   return launch_cost(P->n, p, ncols, z, obs, innov, P->sigma2, J, st);
 }
 

@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(NT) k_integrate(int n, int K, int s0, double d
                                                   SweepGeom geo) {
   extern __shared__ __align__(16) double dsm_[];
   XBuf<NT>& xb = *reinterpret_cast<XBuf<NT>*>(dsm_);
+  xb.init_pads();
   Ring<C, NT> R;
   const int i0 = blockIdx.x * geo.W;
   R.init(n, geo.periodic ? 0 : i0 - geo.HL, geo.nact, geo.periodic);
@@ -108,13 +109,14 @@ __device__ __forceinline__ void tl_sub(const double (&u)[C + 4], const double (&
 }
 
 template <int C, int NT, bool STREAM>
-__global__ void __launch_bounds__(NT) k_tl(edak_problem P, const double* __restrict__ v0,
+__global__ void __launch_bounds__(NT) k_tl(edak_problem P, const double* __restrict__ vin,
                                            double* __restrict__ obs, const int32_t* __restrict__ col_traj,
-                                           SweepGeom geo) {
+                                           SweepGeom geo, int s0, int s1, double* __restrict__ vout) {
   extern __shared__ __align__(16) double dsm_[];
   XBuf<NT>& xb = *reinterpret_cast<XBuf<NT>*>(dsm_);
+  xb.init_pads();
   Ring<C, NT> R;
-  const int n = P.n, N = P.n_steps;
+  const int n = P.n;
   const int i0 = blockIdx.x * geo.W;
   R.init(n, geo.periodic ? 0 : i0 - geo.HL, geo.nact, geo.periodic);
   const int col = blockIdx.y;
@@ -127,34 +129,37 @@ __global__ void __launch_bounds__(NT) k_tl(edak_problem P, const double* __restr
   const double dt = P.dt, h = 0.5 * dt, c6 = dt / 6.0, F = P.forcing;
   int buf = 0;
 
+  // window chunk [s0, s1): v enters at level s0 and leaves at level s1
   double v[C + 4];
-  R.load_own(v0 + (size_t)col * n, v);
+  R.load_own(vin + (size_t)col * n, v);
 
+  // observed own elements inside the output window: grid position or -1
+  int gw[C];
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    const int e = R.t * C + j;
+    gw[j] = (R.t < R.nact && e >= wlo && e < whi) ? __ldg(P.gpos + R.gidx(j)) : -1;
+  }
   auto capture = [&](int level) {
     const int tp = __ldg(P.tpos + level);
-    if (tp < 0 || R.t >= R.nact) return;
+    if (tp < 0) return;
 #pragma unroll
-    for (int j = 0; j < C; ++j) {
-      const int e = R.t * C + j;
-      if (e >= wlo && e < whi) {
-        const int gp = __ldg(P.gpos + R.gidx(j));
-        if (gp >= 0) ob[(size_t)tp * G + gp] = v[j + 2];
-      }
-    }
+    for (int j = 0; j < C; ++j)
+      if (gw[j] >= 0) ob[(size_t)tp * G + gw[j]] = v[j + 2];
   };
-  capture(0);
+  if (s0 == 0) capture(0);
 
   // software pipeline: the state of step s+1 is in flight while step s runs
   const size_t sstride = STREAM ? (size_t)4 * n : (size_t)n;
   double Xn[C + 4];
-  R.load_halo(tr, Xn);
+  R.load_halo(tr + (size_t)s0 * sstride, Xn);
 #pragma unroll 1
-  for (int s = 0; s < N; ++s) {
+  for (int s = s0; s < s1; ++s) {
     const double* Xs = tr + (size_t)s * sstride;
     double X[C + 4];
 #pragma unroll
     for (int k = 0; k < C + 4; ++k) X[k] = Xn[k];
-    if (s + 1 < N) R.load_halo(Xs + sstride, Xn);
+    if (s + 1 < s1) R.load_halo(Xs + sstride, Xn);
     xchg1(R, xb, buf, v);
     double acc[C], a[C], kk[C];
     double x2[C + 4], u2[C + 4];
@@ -216,6 +221,14 @@ __global__ void __launch_bounds__(NT) k_tl(edak_problem P, const double* __restr
     for (int j = 0; j < C; ++j) v[j + 2] = fma(c6, acc[j] + a[j], v[j + 2]);
     capture(s + 1);
   }
+  if (vout && R.t < R.nact) {
+    double* vo = vout + (size_t)col * n;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int e = R.t * C + j;
+      if (e >= wlo && e < whi) vo[R.gidx(j)] = v[j + 2];
+    }
+  }
 }
 
 // ------------------------------------------------------------------- AD --
@@ -230,9 +243,10 @@ __device__ __forceinline__ void ad_sub(const double (&w)[C + 4], const double (&
 template <int C, int NT, bool STREAM>
 __global__ void __launch_bounds__(NT) k_ad(edak_problem P, const double* __restrict__ forcing,
                                            double* __restrict__ gout, const int32_t* __restrict__ col_traj,
-                                           SweepGeom geo) {
+                                           SweepGeom geo, int s0, int s1, const double* __restrict__ gin) {
   extern __shared__ __align__(16) double dsm_[];
   XBuf<NT>& xb = *reinterpret_cast<XBuf<NT>*>(dsm_);
+  xb.init_pads();
   Ring<C, NT> R;
   const int n = P.n, N = P.n_steps;
   const int i0 = blockIdx.x * geo.W;
@@ -259,20 +273,26 @@ __global__ void __launch_bounds__(NT) k_ad(edak_problem P, const double* __restr
     return __ldg(fc + (size_t)tp * G + gp[j]) / s2;
   };
 
+  // window chunk [s0, s1), swept backward: g enters at level s1 (w_all[N]
+  // when s1 == N, model.py:154) and leaves at level s0
   double g[C + 4];
+  if (gin) {
+    R.load_own(gin + (size_t)col * n, g);
+  } else {
 #pragma unroll
-  for (int j = 0; j < C; ++j) g[j + 2] = force(N, j);
+    for (int j = 0; j < C; ++j) g[j + 2] = force(N, j);
+  }
 
   const size_t sstride = STREAM ? (size_t)4 * n : (size_t)n;
   double Xn[C + 4];
-  R.load_halo(tr + (size_t)(N - 1) * sstride, Xn);
+  R.load_halo(tr + (size_t)(s1 - 1) * sstride, Xn);
 #pragma unroll 1
-  for (int s = N - 1; s >= 0; --s) {
+  for (int s = s1 - 1; s >= s0; --s) {
     const double* Xs = tr + (size_t)s * sstride;
     double X[C + 4], x2[C + 4], x3[C + 4], x4[C + 4];
 #pragma unroll
     for (int k = 0; k < C + 4; ++k) X[k] = Xn[k];
-    if (s > 0) R.load_halo(Xs - sstride, Xn);
+    if (s > s0) R.load_halo(Xs - sstride, Xn);
     if (STREAM) {
       R.load_halo(Xs + n, x2);
       R.load_halo(Xs + 2 * n, x3);
@@ -397,42 +417,122 @@ static bool plan(int n, int hl_total, int hr_total, int& C, int& NT, SweepGeom& 
   else if (C_ == 8 && NT_ == 256) { constexpr int CC = 8, TT = 256; __VA_ARGS__; } \
   else { set_error("no kernel family"); return EDAK_EUNSUPPORTED; }
 
+// window chunking: a tile sweep of K steps needs redundant halos ~12K wide;
+// splitting the window into chunks of <= SWEEP_CHUNK steps (ring state
+// handed over through HBM between chunks: 16 B/element per boundary) keeps
+// the halo small.  work2 = 2 * ncols * n doubles (NULL: one chunk).
+constexpr int SWEEP_CHUNK = 8;
+
+static int plan_chunks(int N, bool periodic, const double* work2) {
+  if (periodic || !work2 || N <= SWEEP_CHUNK) return 1;
+  if (const char* e = getenv("EDAK_SWEEP_NOCHUNK")) return 1;
+  return (N + SWEEP_CHUNK - 1) / SWEEP_CHUNK;
+}
+
+int sweep2_mode(const edak_problem* P, int K);
+int launch_tl2(const edak_problem*, const double*, double*, int, const int32_t*, int, int, double*, cudaStream_t);
+int launch_ad2(const edak_problem*, const double*, double*, int, const int32_t*, int, int, const double*,
+               cudaStream_t);
+
 int launch_tl(const edak_problem* P, const double* v0, double* obs, int ncols, const int32_t* col_traj,
-              cudaStream_t st) {
+              cudaStream_t st, double* work2) {
   int C, NT, nt;
   SweepGeom geo;
-  // halos: stencil reach per step (TL 8 left / 4 right) plus the edge
-  // garbage of the exchanged stage recompute
-  if (!plan(P->n, 8 * P->n_steps + 4, 4 * P->n_steps + 4, C, NT, geo, nt)) {
+  const int N = P->n_steps;
+  if (const int m2 = sweep2_mode(P, SWEEP_CHUNK)) {  // shared-memory-staged kernels
+    const int nch = (m2 == 1 || !work2 || N <= SWEEP_CHUNK || getenv("EDAK_SWEEP_NOCHUNK"))
+                        ? 1 : (N + SWEEP_CHUNK - 1) / SWEEP_CHUNK;
+    if (m2 == 2 && nch == 1 && N > SWEEP_CHUNK && sweep2_mode(P, N) == 0) goto v1;
+    {
+      const size_t blk = (size_t)ncols * P->n;
+      for (int c = 0; c < nch; ++c) {
+        const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch);
+        const double* vin = c == 0 ? v0 : work2 + (size_t)((c - 1) & 1) * blk;
+        double* vout = c + 1 < nch ? work2 + (size_t)(c & 1) * blk : nullptr;
+        int rc = launch_tl2(P, vin, obs, ncols, col_traj, s0, s1, vout, st);
+        if (rc) return rc;
+      }
+      return EDAK_OK;
+    }
+  }
+v1:
+  // probe geometry with the full window to learn the mode
+  if (!plan(P->n, 8 * N + 4, 4 * N + 4, C, NT, geo, nt) && !work2) {
     set_error("window too long for the tile family");
     return EDAK_EUNSUPPORTED;
   }
-  dim3 grid(nt, ncols);
+  const int nch = plan_chunks(N, geo.periodic && nt == 1, work2);
   const bool stream = P->stage_mode == 1;
-  EDAK_DISPATCH(C, NT, {
-    if (stream) go<TT>(k_tl<CC, TT, true>, grid, st, *P, v0, obs, col_traj, geo);
-    else go<TT>(k_tl<CC, TT, false>, grid, st, *P, v0, obs, col_traj, geo);
-  });
-  count_launch();
-  return check_launch("k_tl");
+  const size_t blk = (size_t)ncols * P->n;
+  for (int c = 0; c < nch; ++c) {
+    const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch), K = s1 - s0;
+    // halos: stencil reach per step (TL 8 left / 4 right) plus the edge
+    // garbage of the exchanged stage recompute
+    if (!plan(P->n, 8 * K + 4, 4 * K + 4, C, NT, geo, nt)) {
+      set_error("window chunk too long for the tile family");
+      return EDAK_EUNSUPPORTED;
+    }
+    const double* vin = c == 0 ? v0 : work2 + (size_t)((c - 1) & 1) * blk;
+    double* vout = c + 1 < nch ? work2 + (size_t)(c & 1) * blk : nullptr;
+    dim3 grid(nt, ncols);
+    EDAK_DISPATCH(C, NT, {
+      if (stream) go<TT>(k_tl<CC, TT, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
+      else go<TT>(k_tl<CC, TT, false>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
+    });
+    count_launch();
+    int rc = check_launch("k_tl");
+    if (rc) return rc;
+  }
+  return EDAK_OK;
 }
 
 int launch_ad(const edak_problem* P, const double* forcing, double* g, int ncols, const int32_t* col_traj,
-              cudaStream_t st) {
+              cudaStream_t st, double* work2) {
   int C, NT, nt;
   SweepGeom geo;
-  if (!plan(P->n, 4 * P->n_steps + 8, 8 * P->n_steps + 8, C, NT, geo, nt)) {
+  const int N = P->n_steps;
+  if (const int m2 = sweep2_mode(P, SWEEP_CHUNK)) {
+    const int nch = (m2 == 1 || !work2 || N <= SWEEP_CHUNK || getenv("EDAK_SWEEP_NOCHUNK"))
+                        ? 1 : (N + SWEEP_CHUNK - 1) / SWEEP_CHUNK;
+    if (m2 == 2 && nch == 1 && N > SWEEP_CHUNK && sweep2_mode(P, N) == 0) goto v1;
+    {
+      const size_t blk = (size_t)ncols * P->n;
+      for (int c = nch - 1, k = 0; c >= 0; --c, ++k) {
+        const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch);
+        const double* gin = k == 0 ? nullptr : work2 + (size_t)((k - 1) & 1) * blk;
+        double* gout = c == 0 ? g : work2 + (size_t)(k & 1) * blk;
+        int rc = launch_ad2(P, forcing, gout, ncols, col_traj, s0, s1, gin, st);
+        if (rc) return rc;
+      }
+      return EDAK_OK;
+    }
+  }
+v1:
+  if (!plan(P->n, 4 * N + 8, 8 * N + 8, C, NT, geo, nt) && !work2) {
     set_error("window too long for the tile family");
     return EDAK_EUNSUPPORTED;
   }
-  dim3 grid(nt, ncols);
+  const int nch = plan_chunks(N, geo.periodic && nt == 1, work2);
   const bool stream = P->stage_mode == 1;
-  EDAK_DISPATCH(C, NT, {
-    if (stream) go<TT>(k_ad<CC, TT, true>, grid, st, *P, forcing, g, col_traj, geo);
-    else go<TT>(k_ad<CC, TT, false>, grid, st, *P, forcing, g, col_traj, geo);
-  });
-  count_launch();
-  return check_launch("k_ad");
+  const size_t blk = (size_t)ncols * P->n;
+  for (int c = nch - 1, k = 0; c >= 0; --c, ++k) {
+    const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch), K = s1 - s0;
+    if (!plan(P->n, 4 * K + 8, 8 * K + 8, C, NT, geo, nt)) {
+      set_error("window chunk too long for the tile family");
+      return EDAK_EUNSUPPORTED;
+    }
+    const double* gin = k == 0 ? nullptr : work2 + (size_t)((k - 1) & 1) * blk;
+    double* gout = c == 0 ? g : work2 + (size_t)(k & 1) * blk;
+    dim3 grid(nt, ncols);
+    EDAK_DISPATCH(C, NT, {
+      if (stream) go<TT>(k_ad<CC, TT, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1, gin);
+      else go<TT>(k_ad<CC, TT, false>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1, gin);
+    });
+    count_launch();
+    int rc = check_launch("k_ad");
+    if (rc) return rc;
+  }
+  return EDAK_OK;
 }
 
 int launch_integrate(int n, int n_steps, double dt, double F, const double* x0, int ncols, double* states,

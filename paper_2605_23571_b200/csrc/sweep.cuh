@@ -25,12 +25,14 @@ struct Ring {
   bool hp, hn;
   int base;  // ring index of range element 0 (before wrap)
   int n;
+  int g0;    // ring index of own element 0 (wrapped)
 
   __device__ __forceinline__ void init(int n_, int base_, int nact_, bool periodic) {
     n = n_;
     t = threadIdx.x;
     nact = nact_;
     base = base_;
+    g0 = wrap(base + t * C, n);
     if (periodic) {
       prev = t == 0 ? nact - 1 : t - 1;
       next = t + 1 >= nact ? 0 : t + 1;
@@ -42,46 +44,63 @@ struct Ring {
       hn = t + 1 < nact;
     }
   }
-  // ring index of own element j (j may be -2..C+1)
-  __device__ __forceinline__ int gidx(int j) const { return wrap(base + t * C + j, n); }
+  // ring index of own element j (0 <= j < C; C <= n)
+  __device__ __forceinline__ int gidx(int j) const {
+    const int g = g0 + j;
+    return g >= n ? g - n : g;
+  }
 
   // load own elements and 2+2 halo of a ring vector straight from memory
   __device__ __forceinline__ void load_halo(const double* __restrict__ src, double (&a)[C + 4]) const {
-    int g = wrap(base + t * C - 2, n);
+    const int g = g0 >= 2 ? g0 - 2 : g0 - 2 + n;
+    if (g + C + 4 <= n) {  // window does not wrap: straight loads
 #pragma unroll
-    for (int k = 0; k < C + 4; ++k) {
-      a[k] = __ldg(src + g);
-      if (++g == n) g = 0;
+      for (int k = 0; k < C + 4; ++k) a[k] = __ldg(src + g + k);
+    } else {
+#pragma unroll
+      for (int k = 0; k < C + 4; ++k) a[k] = __ldg(src + wrap(g + k, n));
     }
   }
   __device__ __forceinline__ void load_own(const double* __restrict__ src, double (&a)[C + 4]) const {
-    int g = wrap(base + t * C, n);
+    if (g0 + C <= n) {
 #pragma unroll
-    for (int k = 0; k < C; ++k) {
-      a[k + 2] = __ldg(src + g);
-      if (++g == n) g = 0;
+      for (int k = 0; k < C; ++k) a[k + 2] = __ldg(src + g0 + k);
+    } else {
+#pragma unroll
+      for (int k = 0; k < C; ++k) a[k + 2] = __ldg(src + wrap(g0 + k, n));
     }
   }
 
-  // publish first two / last two own values of up to two arrays into sh[4*A][NT]
+  // publish first two / last two own values into sh[4][NT + 2] (slot t + 1);
+  // slots 0 and NT + 1 are zero pads, so a tile's edge threads read zeros
+  // without a branch (their halo is in the budgeted garbage zone anyway)
+  static constexpr int S = NT + 2;
   __device__ __forceinline__ void put(double* sh, const double (&a)[C + 4]) const {
-    sh[0 * NT + t] = a[2];
-    sh[1 * NT + t] = a[3];
-    sh[2 * NT + t] = a[C];
-    sh[3 * NT + t] = a[C + 1];
+    sh[0 * S + t + 1] = a[2];
+    sh[1 * S + t + 1] = a[3];
+    sh[2 * S + t + 1] = a[C];
+    sh[3 * S + t + 1] = a[C + 1];
   }
   __device__ __forceinline__ void get(const double* sh, double (&a)[C + 4]) const {
-    a[0] = hp ? sh[2 * NT + prev] : 0.0;
-    a[1] = hp ? sh[3 * NT + prev] : 0.0;
-    a[C + 2] = hn ? sh[0 * NT + next] : 0.0;
-    a[C + 3] = hn ? sh[1 * NT + next] : 0.0;
+    a[0] = sh[2 * S + prev + 1];
+    a[1] = sh[3 * S + prev + 1];
+    a[C + 2] = sh[0 * S + next + 1];
+    a[C + 3] = sh[1 * S + next + 1];
   }
 };
 
 // shared-memory exchange buffers: [2 bufs][2 arrays][4 slots][NT]
 template <int NT>
 struct XBuf {
-  double v[2][2][4][NT];
+  double v[2][2][4][NT + 2];
+  // zero the pad slots (call once before the first exchange's barrier)
+  __device__ __forceinline__ void init_pads() {
+    const int i = threadIdx.x;
+    if (i < 32) {
+      const int b = i >> 4, a = (i >> 3) & 1, k = (i >> 1) & 3, side = i & 1;
+      v[b][a][k][side ? NT + 1 : 0] = 0.0;
+    }
+  }
 };
 
 template <int C, int NT>
