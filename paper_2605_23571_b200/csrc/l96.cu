@@ -108,8 +108,8 @@ __device__ __forceinline__ void tl_sub(const double (&u)[C + 4], const double (&
     a[j] = l96_tl(u[j + 3], u[j], u[j + 1], u[j + 2], x[j + 3], x[j], x[j + 1]);
 }
 
-template <int C, int NT, bool STREAM>
-__global__ void __launch_bounds__(NT) k_tl(edak_problem P, const double* __restrict__ vin,
+template <int C, int NT, bool STREAM, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* __restrict__ vin,
                                            double* __restrict__ obs, const int32_t* __restrict__ col_traj,
                                            SweepGeom geo, int s0, int s1, double* __restrict__ vout) {
   extern __shared__ __align__(16) double dsm_[];
@@ -149,18 +149,28 @@ __global__ void __launch_bounds__(NT) k_tl(edak_problem P, const double* __restr
   };
   if (s0 == 0) capture(0);
 
-  // software pipeline: the state of step s+1 is in flight while step s runs
+  // software pipeline: the state of step s+1 is staged (cp.async, coalesced)
+  // into the other shared buffer while step s runs; STREAM reads stored
+  // stages straight from memory
+  using SS = Stage<C, NT>;
+  double* XB0 = dsm_ + sizeof(XBuf<NT>) / sizeof(double);
+  double* XB1 = XB0 + SS::PLEN;
+  const int used = R.nact * C;
+  const int gst = wrap(R.base - 2 + (int)threadIdx.x, n);
   const size_t sstride = STREAM ? (size_t)4 * n : (size_t)n;
-  double Xn[C + 4];
-  R.load_halo(tr + (size_t)s0 * sstride, Xn);
+  if (!STREAM) SS::stage((s0 & 1) ? XB1 : XB0, tr + (size_t)s0 * n, gst, n, used);
 #pragma unroll 1
   for (int s = s0; s < s1; ++s) {
     const double* Xs = tr + (size_t)s * sstride;
     double X[C + 4];
-#pragma unroll
-    for (int k = 0; k < C + 4; ++k) X[k] = Xn[k];
-    if (s + 1 < s1) R.load_halo(Xs + sstride, Xn);
-    xchg1(R, xb, buf, v);
+    if (!STREAM) cp_wait_all();
+    xchg1(R, xb, buf, v);  // barrier: staged X_s visible, X_{s-1}'s buffer free
+    if (STREAM) {
+      R.load_halo(Xs, X);
+    } else {
+      if (s + 1 < s1) SS::stage(((s + 1) & 1) ? XB1 : XB0, Xs + n, gst, n, used);
+      SS::win((s & 1) ? XB1 : XB0, R.t, X);
+    }
     double acc[C], a[C], kk[C];
     double x2[C + 4], u2[C + 4];
     tl_sub<C>(v, X, a);
@@ -240,8 +250,8 @@ __device__ __forceinline__ void ad_sub(const double (&w)[C + 4], const double (&
     u[j] = l96_ad(x[j], x[j + 1], x[j + 3], x[j + 4], w[j + 1], w[j + 2], w[j + 3], w[j + 4]);
 }
 
-template <int C, int NT, bool STREAM>
-__global__ void __launch_bounds__(NT) k_ad(edak_problem P, const double* __restrict__ forcing,
+template <int C, int NT, bool STREAM, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* __restrict__ forcing,
                                            double* __restrict__ gout, const int32_t* __restrict__ col_traj,
                                            SweepGeom geo, int s0, int s1, const double* __restrict__ gin) {
   extern __shared__ __align__(16) double dsm_[];
@@ -283,16 +293,23 @@ __global__ void __launch_bounds__(NT) k_ad(edak_problem P, const double* __restr
     for (int j = 0; j < C; ++j) g[j + 2] = force(N, j);
   }
 
+  using SS = Stage<C, NT>;
+  double* XB0 = dsm_ + sizeof(XBuf<NT>) / sizeof(double);
+  double* XB1 = XB0 + SS::PLEN;
+  const int used = R.nact * C;
+  const int gst = wrap(R.base - 2 + (int)threadIdx.x, n);
   const size_t sstride = STREAM ? (size_t)4 * n : (size_t)n;
-  double Xn[C + 4];
-  R.load_halo(tr + (size_t)(s1 - 1) * sstride, Xn);
+  if (!STREAM) {
+    SS::stage(((s1 - 1) & 1) ? XB1 : XB0, tr + (size_t)(s1 - 1) * n, gst, n, used);
+    cp_wait_all();
+    __syncthreads();
+  }
 #pragma unroll 1
   for (int s = s1 - 1; s >= s0; --s) {
     const double* Xs = tr + (size_t)s * sstride;
     double X[C + 4], x2[C + 4], x3[C + 4], x4[C + 4];
-#pragma unroll
-    for (int k = 0; k < C + 4; ++k) X[k] = Xn[k];
-    if (s > s0) R.load_halo(Xs - sstride, Xn);
+    if (STREAM) R.load_halo(Xs, X);
+    else SS::win((s & 1) ? XB1 : XB0, R.t, X);  // staged, published by the last barrier
     if (STREAM) {
       R.load_halo(Xs + n, x2);
       R.load_halo(Xs + 2 * n, x3);
@@ -302,6 +319,8 @@ __global__ void __launch_bounds__(NT) k_ad(edak_problem P, const double* __restr
 #pragma unroll
       for (int j = 0; j < C; ++j) x2[j + 2] = axpy_rn(X[j + 2], h, l96_f(X[j + 3], X[j], X[j + 1], X[j + 2], F));
       xchg2(R, xb, buf, x2, g);
+      // X_{s-1} goes to the buffer X_{s+1} used: every thread read it last step
+      if (s > s0) SS::stage(((s - 1) & 1) ? XB1 : XB0, Xs - n, gst, n, used);
 #pragma unroll
       for (int j = 0; j < C; ++j)
         x3[j + 2] = axpy_rn(X[j + 2], h, l96_f(x2[j + 3], x2[j], x2[j + 1], x2[j + 2], F));
@@ -335,6 +354,7 @@ __global__ void __launch_bounds__(NT) k_ad(edak_problem P, const double* __restr
       vh[j] += u[j];
       a[j + 2] = fma(h, u[j], c6 * g[j + 2]);  // a1
     }
+    if (!STREAM) cp_wait_all();  // X_{s-1} landed; published by this barrier
     xchg1(R, xb, buf, a);
     ad_sub<C>(a, X, u);
 #pragma unroll
@@ -353,9 +373,9 @@ __global__ void __launch_bounds__(NT) k_ad(edak_problem P, const double* __restr
 // ------------------------------------------------------------ launchers --
 
 // opt a kernel into > 48 KB of dynamic shared memory (idempotent)
-template <int NT, typename K, typename... Args>
+template <int NT, int C = 0, typename K, typename... Args>
 static void go(K kernel, dim3 grid, cudaStream_t st, Args... args) {
-  const size_t bytes = sizeof(XBuf<NT>);
+  const size_t bytes = sizeof(XBuf<NT>) + (C ? 2 * Stage<C ? C : 1, NT>::PLEN * sizeof(double) : 0);
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   kernel<<<grid, NT, bytes, st>>>(args...);
 }
@@ -417,6 +437,11 @@ static bool plan(int n, int hl_total, int hr_total, int& C, int& NT, SweepGeom& 
   else if (C_ == 8 && NT_ == 256) { constexpr int CC = 8, TT = 256; __VA_ARGS__; } \
   else { set_error("no kernel family"); return EDAK_EUNSUPPORTED; }
 
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 // window chunking: a tile sweep of K steps needs redundant halos ~12K wide;
 // splitting the window into chunks of <= SWEEP_CHUNK steps (ring state
 // handed over through HBM between chunks: 16 B/element per boundary) keeps
@@ -475,10 +500,18 @@ v1:
     const double* vin = c == 0 ? v0 : work2 + (size_t)((c - 1) & 1) * blk;
     double* vout = c + 1 < nch ? work2 + (size_t)(c & 1) * blk : nullptr;
     dim3 grid(nt, ncols);
-    EDAK_DISPATCH(C, NT, {
-      if (stream) go<TT>(k_tl<CC, TT, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
-      else go<TT>(k_tl<CC, TT, false>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
-    });
+    // measured best on B200: 4 resident CTAs (126 regs, no spills)
+    const int mb = env_int("EDAK_TL_MINB", 4);
+    if (C == 8 && NT == 128 && !stream && mb == 3) {
+      go<128, 8>(k_tl<8, 128, false, 3>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
+    } else if (C == 8 && NT == 128 && !stream && mb == 4) {
+      go<128, 8>(k_tl<8, 128, false, 4>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
+    } else {
+      EDAK_DISPATCH(C, NT, {
+        if (stream) go<TT, CC>(k_tl<CC, TT, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
+        else go<TT, CC>(k_tl<CC, TT, false>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
+      });
+    }
     count_launch();
     int rc = check_launch("k_tl");
     if (rc) return rc;
@@ -524,10 +557,18 @@ v1:
     const double* gin = k == 0 ? nullptr : work2 + (size_t)((k - 1) & 1) * blk;
     double* gout = c == 0 ? g : work2 + (size_t)(k & 1) * blk;
     dim3 grid(nt, ncols);
-    EDAK_DISPATCH(C, NT, {
-      if (stream) go<TT>(k_ad<CC, TT, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1, gin);
-      else go<TT>(k_ad<CC, TT, false>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1, gin);
-    });
+    // measured best on B200: 3 resident CTAs (168 regs, no spills)
+    const int mb = env_int("EDAK_AD_MINB", 3);
+    if (C == 8 && NT == 128 && !stream && mb == 3) {
+      go<128, 8>(k_ad<8, 128, false, 3>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1, gin);
+    } else if (C == 8 && NT == 128 && !stream && mb == 2) {
+      go<128, 8>(k_ad<8, 128, false, 2>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1, gin);
+    } else {
+      EDAK_DISPATCH(C, NT, {
+        if (stream) go<TT, CC>(k_ad<CC, TT, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1, gin);
+        else go<TT, CC>(k_ad<CC, TT, false>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1, gin);
+      });
+    }
     count_launch();
     int rc = check_launch("k_ad");
     if (rc) return rc;

@@ -34,12 +34,6 @@ struct Tile2 {
   }
 };
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n"); }
-__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 // stage the ring window [base-2, base+R+2) of one state level into buf.
 // Thread i copies q = i - 2 + k NT: consecutive threads read consecutive ring

@@ -36,8 +36,14 @@ def timeit(fn, reps=10):
 ref = None
 modes = sys.argv[1:] or ["v1", "v2"]
 for mode in modes:
-    for k in ("EDAK_SWEEP_V2", "EDAK_SWEEP_NOCHUNK", "EDAK_SWEEP_FAMILY"):
+    for k in ("EDAK_SWEEP_V2", "EDAK_SWEEP_NOCHUNK", "EDAK_SWEEP_FAMILY", "EDAK_TL_MINB",
+              "EDAK_AD_MINB"):
         os.environ.pop(k, None)
+    for part in mode.split("+")[1:]:          # e.g. v1+tl4+ad3
+        if part.startswith("tl"):
+            os.environ["EDAK_TL_MINB"] = part[2:]
+        if part.startswith("ad"):
+            os.environ["EDAK_AD_MINB"] = part[2:]
     if mode.startswith("v2"):
         os.environ["EDAK_SWEEP_V2"] = "1"
     if "nochunk" in mode:
