@@ -20,45 +20,70 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// ----------------------------------------------------------------- TN ----
-// CTA: 256 threads (8 warps as 2 x 4), C tile 64 (a) x 64 (b); warp tile 32 x 16.
-constexpr int TN_BM = 64, TN_BN = 64, TN_BK = 32, TN_PAD = 4;
+// cp.async 8-byte copy with zero-fill (src_bytes = 0 writes zeros)
+__device__ __forceinline__ void cpa8(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// Both kernels: CTA tile 64 x 64, 8 warps as 2 x 4 (warp tile 32 x 16 = 4 x 2
+// DMMA.8x8x4 fragments), K chunks of 32 staged by a 2-deep cp.async
+// pipeline so the next chunk's loads overlap this chunk's DMMAs.
+constexpr int G_BM = 64, G_BN = 64, G_BK = 32, G_PAD = 4;
+
+// ----------------------------------------------------------------- TN ----
+// sA[stage][col a][k], sB[stage][col b][k]  (both operands K-contiguous)
 __global__ void __launch_bounds__(256) k_gemm_tn(const double* __restrict__ A, int64_t lda,
                                                  const double* __restrict__ B, int64_t ldb, int m, int nb,
                                                  int64_t K, int64_t kslice, double* __restrict__ part) {
-  __shared__ double sA[TN_BM][TN_BK + TN_PAD];
-  __shared__ double sB[TN_BN][TN_BK + TN_PAD];
+  extern __shared__ __align__(16) double gsm[];
+  double (*sA)[G_BM][G_BK + G_PAD] = reinterpret_cast<double (*)[G_BM][G_BK + G_PAD]>(gsm);
+  double (*sB)[G_BN][G_BK + G_PAD] =
+      reinterpret_cast<double (*)[G_BN][G_BK + G_PAD]>(gsm + 2 * G_BM * (G_BK + G_PAD));
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int wa = (warp >> 2) * 32, wb = (warp & 3) * 16;
-  const int a0 = blockIdx.x * TN_BM, b0 = blockIdx.y * TN_BN;
+  const int a0 = blockIdx.x * G_BM, b0 = blockIdx.y * G_BN;
   const int64_t k_begin = (int64_t)blockIdx.z * kslice;
   const int64_t k_end = min(K, k_begin + kslice);
-  double acc[4][2][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  for (int64_t k0 = k_begin; k0 < k_end; k0 += TN_BK) {
-    // 64 columns x 32 contiguous k for each operand: 2048 doubles, 8 per thread
+  const int nch = (int)((k_end - k_begin + G_BK - 1) / G_BK);
+  auto load = [&](int stg, int64_t k0) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int idx = t + q * 256;
       const int col = idx >> 5, kk = idx & 31;
       const int64_t k = k0 + kk;
       const bool kin = k < k_end;
-      sA[col][kk] = (kin && a0 + col < m) ? __ldg(A + k + (int64_t)(a0 + col) * lda) : 0.0;
-      sB[col][kk] = (kin && b0 + col < nb) ? __ldg(B + k + (int64_t)(b0 + col) * ldb) : 0.0;
+      const bool va = kin && a0 + col < m, vb = kin && b0 + col < nb;
+      cpa8(&sA[stg][col][kk], va ? A + k + (int64_t)(a0 + col) * lda : A, va);
+      cpa8(&sB[stg][col][kk], vb ? B + k + (int64_t)(b0 + col) * ldb : B, vb);
+    }
+    cpa_commit();
+  };
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (nch > 0) load(0, k_begin);
+  for (int c = 0; c < nch; ++c) {
+    if (c + 1 < nch) {
+      load((c + 1) & 1, k_begin + (int64_t)(c + 1) * G_BK);
+      cpa_wait<1>();
+    } else {
+      cpa_wait<0>();
     }
     __syncthreads();
+    const int stg = c & 1;
 #pragma unroll
-    for (int ks = 0; ks < TN_BK; ks += 4) {
+    for (int ks = 0; ks < G_BK; ks += 4) {
       double af[4], bf[2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = sA[wa + i * 8 + (lane >> 2)][ks + (lane & 3)];
+      for (int i = 0; i < 4; ++i) af[i] = sA[stg][wa + i * 8 + (lane >> 2)][ks + (lane & 3)];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) bf[j] = sB[wb + j * 8 + (lane >> 2)][ks + (lane & 3)];
+      for (int j = 0; j < 2; ++j) bf[j] = sB[stg][wb + j * 8 + (lane >> 2)][ks + (lane & 3)];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -66,7 +91,6 @@ __global__ void __launch_bounds__(256) k_gemm_tn(const double* __restrict__ A, i
     }
     __syncthreads();
   }
-  // partial tile (m x nb, column-major with ld = m) for this K slice
   double* P = part + (size_t)blockIdx.z * m * nb;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -92,13 +116,13 @@ __global__ void k_reduce_parts(const double* __restrict__ part, int nsplit, int 
 }
 
 static int tn_nsplit(int m, int nb, int64_t K, int64_t& kslice) {
-  const int tiles = ((m + TN_BM - 1) / TN_BM) * ((nb + TN_BN - 1) / TN_BN);
+  const int tiles = ((m + G_BM - 1) / G_BM) * ((nb + G_BN - 1) / G_BN);
   int64_t want = (2 * 148 + tiles - 1) / tiles;  // >= ~2 waves of CTAs
   int64_t maxs = (K + 255) / 256;                // slices of >= 256 rows
   int64_t s = want < maxs ? want : maxs;
   if (s < 1) s = 1;
   kslice = (K + s - 1) / s;
-  kslice = (kslice + TN_BK - 1) / TN_BK * TN_BK;
+  kslice = (kslice + G_BK - 1) / G_BK * G_BK;
   s = (K + kslice - 1) / kslice;
   return (int)s;
 }
@@ -108,12 +132,19 @@ int64_t gemm_tn_partials(int m, int nb, int64_t K) {
   return (int64_t)tn_nsplit(m, nb, K, ks) * m * nb;
 }
 
+static constexpr size_t G_SMEM = 2 * (size_t)(G_BM + G_BN) * (G_BK + G_PAD) * sizeof(double);
+
 int launch_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int ldc, int m, int nb,
                    int64_t K, double* part, cudaStream_t st) {
   int64_t ks;
   const int s = tn_nsplit(m, nb, K, ks);
-  dim3 grid((m + TN_BM - 1) / TN_BM, (nb + TN_BN - 1) / TN_BN, s);
-  k_gemm_tn<<<grid, 256, 0, st>>>(A, lda, B, ldb, m, nb, K, ks, part);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm_tn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G_SMEM);
+    attr = true;
+  }
+  dim3 grid((m + G_BM - 1) / G_BM, (nb + G_BN - 1) / G_BN, s);
+  k_gemm_tn<<<grid, 256, G_SMEM, st>>>(A, lda, B, ldb, m, nb, K, ks, part);
   int64_t tot = (int64_t)m * nb;
   int nblk = (int)((tot + 255) / 256);
   k_reduce_parts<<<nblk < 1024 ? nblk : 1024, 256, 0, st>>>(part, s, m, nb, C, ldc);
@@ -122,54 +153,62 @@ int launch_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, d
 }
 
 // ----------------------------------------------------------------- NN ----
-constexpr int NN_BM = 64, NN_BN = 64, NN_BK = 32, NN_PAD = 4;
-
+// sA[stage][l][i] (A is M-contiguous), sB[stage][j][l] (B is K-contiguous)
 __global__ void __launch_bounds__(256) k_gemm_nn(const double* __restrict__ A, int64_t lda,
                                                  const double* __restrict__ B, int ldb,
                                                  const double* __restrict__ bscale, const double* Cin,
                                                  int64_t ldc, double beta, double* D, int64_t ldd, int64_t M,
                                                  int N, int kk) {
-  __shared__ double sA[NN_BK][NN_BM + NN_PAD];
-  __shared__ double sB[NN_BN][NN_BK + NN_PAD];
+  extern __shared__ __align__(16) double gsm[];
+  double (*sA)[G_BK][G_BM + G_PAD] = reinterpret_cast<double (*)[G_BK][G_BM + G_PAD]>(gsm);
+  double (*sB)[G_BN][G_BK + G_PAD] =
+      reinterpret_cast<double (*)[G_BN][G_BK + G_PAD]>(gsm + 2 * G_BK * (G_BM + G_PAD));
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int wi = (warp >> 2) * 32, wj = (warp & 3) * 16;
-  const int64_t i0 = (int64_t)blockIdx.x * NN_BM;
-  const int j0 = blockIdx.y * NN_BN;
+  const int64_t i0 = (int64_t)blockIdx.x * G_BM;
+  const int j0 = blockIdx.y * G_BN;
+  const int nch = (kk + G_BK - 1) / G_BK;
+  auto load = [&](int stg, int l0) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int idx = t + q * 256;
+      {
+        const int l = idx >> 6, i = idx & 63;
+        const bool v = l0 + l < kk && i0 + i < M;
+        cpa8(&sA[stg][l][i], v ? A + (i0 + i) + (int64_t)(l0 + l) * lda : A, v);
+      }
+      {
+        const int j = idx >> 5, l = idx & 31;
+        const bool v = l0 + l < kk && j0 + j < N;
+        cpa8(&sB[stg][j][l], v ? B + (l0 + l) + (int64_t)(j0 + j) * ldb : B, v);
+      }
+    }
+    cpa_commit();
+  };
   double acc[4][2][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  for (int l0 = 0; l0 < kk; l0 += NN_BK) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int idx = t + q * 256;
-      // A chunk: 32 (l) x 64 (i), i contiguous in memory
-      {
-        const int l = idx >> 6, i = idx & 63;
-        const int64_t gi = i0 + i;
-        sA[l][i] = (l0 + l < kk && gi < M) ? __ldg(A + gi + (int64_t)(l0 + l) * lda) : 0.0;
-      }
-      // B chunk: 64 (j) x 32 (l), l contiguous in memory
-      {
-        const int j = idx >> 5, l = idx & 31;
-        double bv = 0.0;
-        if (l0 + l < kk && j0 + j < N) {
-          bv = __ldg(B + (l0 + l) + (int64_t)(j0 + j) * ldb);
-          if (bscale) bv *= __ldg(bscale + l0 + l);
-        }
-        sB[j][l] = bv;
-      }
+  load(0, 0);
+  for (int c = 0; c < nch; ++c) {
+    if (c + 1 < nch) {
+      load((c + 1) & 1, (c + 1) * G_BK);
+      cpa_wait<1>();
+    } else {
+      cpa_wait<0>();
     }
     __syncthreads();
+    const int stg = c & 1, l0 = c * G_BK;
 #pragma unroll
-    for (int ks = 0; ks < NN_BK; ks += 4) {
+    for (int ks = 0; ks < G_BK; ks += 4) {
       double af[4], bf[2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = sA[ks + (lane & 3)][wi + i * 8 + (lane >> 2)];
+      for (int i = 0; i < 4; ++i) af[i] = sA[stg][ks + (lane & 3)][wi + i * 8 + (lane >> 2)];
+      const int l = l0 + ks + (lane & 3);
+      const double sc = (bscale && l < kk) ? __ldg(bscale + l) : 1.0;
 #pragma unroll
-      for (int j = 0; j < 2; ++j) bf[j] = sB[wj + j * 8 + (lane >> 2)][ks + (lane & 3)];
+      for (int j = 0; j < 2; ++j) bf[j] = sc * sB[stg][wj + j * 8 + (lane >> 2)][ks + (lane & 3)];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -195,8 +234,13 @@ __global__ void __launch_bounds__(256) k_gemm_nn(const double* __restrict__ A, i
 
 int launch_gemm_nn(const double* A, int64_t lda, const double* B, int ldb, const double* bscale, const double* Cin,
                    int64_t ldc, double beta, double* D, int64_t ldd, int64_t M, int N, int kk, cudaStream_t st) {
-  dim3 grid((unsigned)((M + NN_BM - 1) / NN_BM), (N + NN_BN - 1) / NN_BN);
-  k_gemm_nn<<<grid, 256, 0, st>>>(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M, N, kk);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm_nn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G_SMEM);
+    attr = true;
+  }
+  dim3 grid((unsigned)((M + G_BM - 1) / G_BM), (N + G_BN - 1) / G_BN);
+  k_gemm_nn<<<grid, 256, G_SMEM, st>>>(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M, N, kk);
   count_launch();
   return check_launch("k_gemm_nn");
 }
