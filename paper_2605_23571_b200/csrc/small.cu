@@ -77,8 +77,85 @@ __global__ void __launch_bounds__(256) k_potrf_shifted(const double* __restrict_
   }
 }
 
+// Right-looking variant entirely in shared memory (l <= 128): per pivot one
+// scaled row and one parallel rank-1 update of the trailing upper triangle;
+// same breakdown test and shift schedule as k_potrf_shifted.
+constexpr int POTRF_SMEM_MAX = 128;
+
+__global__ void __launch_bounds__(1024) k_potrf_smem(const double* __restrict__ W, int l, double* __restrict__ Cm,
+                                                     int mode, double scale, double* nu_out, int32_t* info) {
+  extern __shared__ __align__(16) double psm[];
+  double* A = psm;            // l x l, column-major, upper triangle live
+  double* row = psm + l * l;  // row j of C
+  __shared__ int fail;
+  const int t = threadIdx.x, NT = blockDim.x;
+  double sc = scale;
+  if (mode == 1) {  // np.trace(w)
+    sc = 0.0;
+    for (int j = 0; j < l; ++j) sc += W[j + (size_t)j * l];
+  }
+  double nu = 0.0;
+  int attempt = 0;
+  for (; attempt < 6; ++attempt) {
+    if (attempt == 1) {
+      nu = 2.220446049250313e-16 * sc;
+      if (mode == 0 || !(nu > 0.0)) break;
+    } else if (attempt > 1) {
+      nu *= 10.0;
+    }
+    for (int e = t; e < l * l; e += NT) {
+      const int r = e % l, c = e / l;
+      A[e] = r <= c ? W[e] + (r == c ? nu : 0.0) : 0.0;
+    }
+    if (t == 0) fail = 0;
+    __syncthreads();
+    for (int j = 0; j < l; ++j) {
+      const double d = A[j + j * l];
+      if (!(d > 0.0)) {  // dpotrf: pivot <= 0 or NaN
+        if (t == 0) fail = 1;
+        break;
+      }
+      const double cjj = sqrt(d);
+      for (int c = j + t; c < l; c += NT) row[c] = c == j ? cjj : A[j + c * l] / cjj;
+      __syncthreads();
+      const int m = l - j - 1;
+      for (int e = t; e < m * m; e += NT) {
+        const int r = j + 1 + e % m, c = j + 1 + e / m;
+        if (r <= c) A[r + c * l] -= row[r] * row[c];
+      }
+      for (int c = j + t; c < l; c += NT) A[j + c * l] = row[c];  // row j of C is final
+      __syncthreads();
+    }
+    __syncthreads();
+    if (!fail) break;
+  }
+  const bool ok = attempt < 6 && !fail && !(attempt >= 1 && mode == 0);
+  if (ok)
+    for (int e = t; e < l * l; e += NT) {
+      const int r = e % l, c = e / l;
+      Cm[e] = r <= c ? A[e] : 0.0;
+    }
+  if (t == 0) {
+    info[0] = attempt;
+    info[1] = ok ? 0 : 1;
+    nu_out[0] = ok ? nu : 0.0;
+  }
+}
+
 int launch_potrf_shifted(const double* W, int l, double* C, int mode, double scale, double* nu_out, int32_t* info,
                          cudaStream_t st) {
+  if (l <= POTRF_SMEM_MAX) {
+    const size_t sm = (size_t)(l * l + l) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_potrf_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (POTRF_SMEM_MAX * POTRF_SMEM_MAX + POTRF_SMEM_MAX) * (int)sizeof(double));
+      attr = true;
+    }
+    k_potrf_smem<<<1, 1024, sm, st>>>(W, l, C, mode, scale, nu_out, info);
+    count_launch();
+    return check_launch("k_potrf_smem");
+  }
   k_potrf_shifted<<<1, 256, 0, st>>>(W, l, C, mode, scale, nu_out, info);
   count_launch();
   return check_launch("k_potrf_shifted");
@@ -98,7 +175,44 @@ __global__ void k_trinv_upper(const double* __restrict__ R, int l, double* __res
   }
 }
 
+// Shared-memory variant (l <= 128): rows of X = R^-1 from the bottom up,
+// X[i][c] = -(1/R_ii) sum_{k=i+1..c} R[i][k] X[k][c], one thread per column c.
+__global__ void __launch_bounds__(128) k_trinv_smem(const double* __restrict__ R, int l, double* __restrict__ X) {
+  extern __shared__ __align__(16) double tsm[];
+  const double* Rs = R;  // read as warp-wide broadcasts (L1)
+  double* Xs = tsm;      // column-major l x l
+  const int t = threadIdx.x;
+  for (int e = t; e < l * l; e += blockDim.x) Xs[e] = 0.0;
+  __syncthreads();
+  for (int i = l - 1; i >= 0; --i) {
+    const double rii = Rs[i + i * l];
+    for (int c = i + t; c < l; c += blockDim.x) {
+      if (c == i) {
+        Xs[i + c * l] = 1.0 / rii;
+      } else {
+        double s = 0.0;
+        for (int k = i + 1; k <= c; ++k) s += Rs[i + k * l] * Xs[k + c * l];
+        Xs[i + c * l] = -s / rii;
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = t; e < l * l; e += blockDim.x) X[e] = Xs[e];
+}
+
 int launch_trinv_upper(const double* R, int l, double* X, cudaStream_t st) {
+  if (l <= POTRF_SMEM_MAX) {
+    const size_t sm = (size_t)l * l * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_trinv_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           POTRF_SMEM_MAX * POTRF_SMEM_MAX * (int)sizeof(double));
+      attr = true;
+    }
+    k_trinv_smem<<<1, 128, sm, st>>>(R, l, X);
+    count_launch();
+    return check_launch("k_trinv_smem");
+  }
   k_trinv_upper<<<(l + 127) / 128, 128, 0, st>>>(R, l, X);
   count_launch();
   return check_launch("k_trinv_upper");

@@ -235,3 +235,26 @@ def test_pcg_members_batched_equals_single(gpu):
         om = setup.members[j]
         ref, ej, er = pcg_envelope(om.hessian_apply, om.rhs(), cfg, cost_fn=om.quadratic_cost)
         assert_trace(trs[j], ref, ej, er)
+
+
+@pytest.mark.parametrize("l", [6, 50, 128, 200])
+def test_potrf_trinv_sizes(gpu, l):
+    """Shared-memory (l <= 128) and global (l > 128) Cholesky / inverse."""
+    from paper_2605_23571_b200.linalg import potrf_shifted, trinv_upper
+    rng = np.random.default_rng(l)
+    x = rng.standard_normal((l, l))
+    w = x @ x.T + l * np.eye(l)
+    C, nu, info = potrf_shifted(torch.tensor(w.T.copy(), device="cuda"), 0)
+    assert info.cpu().tolist() == [0, 0]
+    c = C.cpu().numpy().T
+    npt.assert_allclose(c, np.linalg.cholesky(w).T, rtol=1e-12, atol=1e-12 * np.abs(c).max())
+    X = trinv_upper(C).cpu().numpy().T
+    npt.assert_allclose(X @ c, np.eye(l), atol=1e-11)
+    # rank-deficient Gram: plain fails, the eps*trace shift schedule succeeds
+    y = rng.standard_normal((l, max(1, l // 2)))
+    wd = y @ y.T
+    C, nu, info = potrf_shifted(torch.tensor(wd.T.copy(), device="cuda"), 1)
+    inf = info.cpu().tolist()
+    assert inf[1] == 0 and inf[0] >= 1 and float(nu[0]) > 0
+    c = C.cpu().numpy().T
+    npt.assert_allclose(c.T @ c, wd + float(nu[0]) * np.eye(l), atol=1e-10 * np.abs(wd).max())
