@@ -303,19 +303,21 @@ def run_ours(args):
     t_step = max_over_ranks(local_s, torch.device("cuda", local)) / args.steps
     value = applies * world / t_step
 
-    # ---- e2e: same pass through the public API with HOST (pinned) buffers
+    # ---- e2e: the same pass from HOST inputs, through the public API.  Per
+    # step the host ships each row's initial state (x_b, x_j) and its
+    # (perturbed) observations y_j (pinned -> device); the device integrates
+    # the trajectories, forms the innovations (DeviceEnsemble.refresh,
+    # eda.py:99-105) and runs the pass; the increments x come back to the host.
     e2e = None
     if not args.no_e2e:
-        lin = dens.lin
-        h_states = torch.empty_like(lin.states, device="cpu").pin_memory()
-        h_states.copy_(lin.states)
-        h_innov = torch.empty_like(dens.innovations, device="cpu").pin_memory()
-        h_innov.copy_(dens.innovations)
+        h_x0 = torch.empty_like(dens.x0, device="cpu").pin_memory()
+        h_x0.copy_(dens.x0)
+        h_y = torch.empty_like(dens.y, device="cpu").pin_memory()
+        h_y.copy_(dens.y)
         h_x = torch.empty((cfg.members, cfg.n), dtype=torch.float64).pin_memory()
 
         def e2e_step():
-            lin.states.copy_(h_states, non_blocking=True)
-            dens.innovations.copy_(h_innov, non_blocking=True)
+            dens.refresh(h_x0, h_y)
             r = eng.run()
             h_x.copy_(r.x, non_blocking=True)
             return r
@@ -329,11 +331,12 @@ def run_ours(args):
         e2.record()
         barrier()
         t2 = max_over_ranks(s2.elapsed_time(e2) * 1e-3, torch.device("cuda", local)) / args.steps
-        h2d = h_states.numel() * 8 + h_innov.numel() * 8
+        h2d = h_x0.numel() * 8 + h_y.numel() * 8
         d2h = h_x.numel() * 8 + 2 * cfg.members * (cfg.pcg_iters + 1) * 8 + 8 * cfg.members
         e2e = {"value": applies * world / t2, "unit": UNIT, "ms_per_step": t2 * 1e3,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "path": "host pinned trajectories+innovations -> EdaPass.run (C-ABI) -> host x"}
+               "path": "host pinned x0 + y per row -> DeviceEnsemble.refresh (GPU RK4 "
+                       "trajectories, innovations) -> EdaPass.run (C-ABI) -> host x"}
 
     roof = None
     if rank == 0:

@@ -87,10 +87,37 @@ class DeviceEnsemble:
     innovations: torch.Tensor  # (M+1, p)
     traj_of: np.ndarray        # row -> trajectory index
     lin: Linearization = None
+    x0: torch.Tensor = None    # (M+1, n) initial states: x_b and the member x_j
+    y: torch.Tensor = None     # (M+1, p) (perturbed) observations y, y_j
+    grid_t: torch.Tensor = None
+    times_t: torch.Tensor = None
 
     @property
     def members(self):
         return self.innovations.shape[0] - 1
+
+    def refresh(self, x0=None, y=None):
+        """New assimilation cycle from initial states / observations (host or
+        device; copied into the resident buffers): integrate every row on the
+        GPU, observe it, innovations d_j = y_j - G(x_j) (eda.py:99-105).  All
+        device buffers keep their addresses, so operators built on them stay
+        valid."""
+        if x0 is not None:
+            self.x0.copy_(x0, non_blocking=True)
+        if y is not None:
+            self.y.copy_(y, non_blocking=True)
+        cfg = self.cfg
+        n, N = cfg.n, cfg.n_steps
+        rows = self.x0.shape[0]
+        full = self.states if self.states.shape[0] == rows else self._scratch
+        _lib.call("edak_integrate", n, N, float(cfg.dt), float(cfg.forcing), self.x0.data_ptr(), rows,
+                  full.data_ptr(), (N + 1) * n, None, 0, _lib.stream())
+        _lib.call("edak_observe", full.data_ptr(), (N + 1) * n, n, self.grid_t.data_ptr(),
+                  self.net.grid.size, self.times_t.data_ptr(), self.net.times.size, rows,
+                  self._gx.data_ptr(), _lib.stream())
+        torch.sub(self.y, self._gx, out=self.innovations)
+        if full is not self.states:
+            self.states.copy_(full[: self.states.shape[0]])
 
 
 def _normal_block(seed, path_fn, rows, size):
@@ -146,6 +173,10 @@ def build_ensemble(cfg, members=None, member_offset=0, truth=None):
         traj_of = np.arange(members + 1)
     ens = DeviceEnsemble(cfg, net, ub, rn, states, innov, traj_of)
     ens.lin = Linearization(states, cfg.dt, cfg.forcing, net, ub, rn)
+    ens.x0, ens.y, ens.grid_t, ens.times_t = x0, yj.contiguous(), grid_t, times_t
+    ens._gx = gx
+    ens._scratch = (None if not cfg.shared_linearization else
+                    torch.empty((members + 1, N + 1, n), dtype=torch.float64, device=dev))
     return ens
 
 
