@@ -250,11 +250,12 @@ __global__ void __launch_bounds__(NT, 4) k_ad2(edak_problem P, const double* __r
 #pragma unroll
   for (int j = 0; j < C; ++j) gp[j] = __ldg(P.gpos + R.gidx(j));
   // w_all[level] at own elements: R^-1 d at observed points, 0 elsewhere
+  const double inv_s2 = 1.0 / s2;  // as k_ad: reciprocal, hoisted level lookup
   auto force = [&](int level, double (&f)[C]) {
     const int tp = __ldg(P.tpos + level);
 #pragma unroll
     for (int j = 0; j < C; ++j)
-      f[j] = (tp < 0 || gp[j] < 0) ? 0.0 : __ldg(fc + (size_t)tp * G + gp[j]) / s2;
+      f[j] = (tp < 0 || gp[j] < 0) ? 0.0 : __ldg(fc + (size_t)tp * G + gp[j]) * inv_s2;
   };
 
   stage_state<C, NT>((s1 - 1) & 1 ? XB1 : XB0, tr + (size_t)(s1 - 1) * n, g0, n);
