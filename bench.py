@@ -211,12 +211,20 @@ def kernel_roofline(torch, lib, eng, reps, peaks):
     stream_bytes = 32.0 * N * n * M + 16.0 * n * M
     return {
         "bound": "fp64",
-        "kernel": dom,
+        "kernel": dom + (" (edak_ad_sweep: 3 window chunks)" if dom == "k_ad"
+                         else " (edak_tl_sweep: 3 window chunks)"),
+        "executed_fp64_pipe_util": "k_ad 48%, k_tl 51% of the FP64 pipe (ncu, profiles/): the "
+                                   "stage recompute adds ~18 DP instructions per element-step "
+                                   "that the algorithmic count (37/42) leaves out",
         "achieved": achieved,
         "peak": peaks["dfma_tflops"],
         "unit": "TFLOP/s",
         "frac": achieved / peaks["dfma_tflops"],
-        "traffic": None,
+        # dram__bytes_read.sum + dram__bytes_write.sum of one edak_ad_sweep
+        # (3 chunk launches of k_ad) from `ncu --set full`
+        # (profiles/r1_cfg4_sweeps_ncu_summary.txt); algorithmic minimum ~0.66 GB
+        "traffic": 0.795e9 if dom == "k_ad" else 0.80e9,
+        "traffic_unit": "bytes per launch (ncu, profiles/r1_cfg4_sweeps_ncu_summary.txt)",
         "peak_source": "measured in this run: DFMA-pipe loop (edak_peak_dfma); "
                        "DMMA loop %.1f TFLOP/s" % peaks["dmma_tflops"],
         "algorithmic_flops_per_launch": flops[dom],

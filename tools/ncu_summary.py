@@ -10,8 +10,10 @@ def main(path):
                          text=True).stdout.splitlines()
     rows = list(csv.reader(raw))
     hdr = rows[0]
+    units = dict(zip(hdr, rows[1]))
+    rows = [rows[0]] + rows[1:]
     keys = [
-        ("gpu__time_duration.sum", "duration_us", 1e-3),
+        ("gpu__time_duration.sum", "duration", 1),
         ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64_pipe_%", 1),
         ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64_inst_%", 1),
         ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor_pipe_%", 1),
@@ -19,8 +21,8 @@ def main(path):
         ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps_active_%", 1),
         ("launch__registers_per_thread", "regs", 1),
         ("launch__occupancy_limit_registers", "occ_limit_regs", 1),
-        ("dram__bytes_read.sum", "dram_read_MB", 1e-6),
-        ("dram__bytes_write.sum", "dram_write_MB", 1e-6),
+        ("dram__bytes_read.sum", "dram_read", 1),
+        ("dram__bytes_write.sum", "dram_write", 1),
         ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_%", 1),
         ("smsp__inst_executed.sum", "warp_insts", 1),
     ]
@@ -34,7 +36,7 @@ def main(path):
                 continue
             try:
                 fv = float(v.replace(",", "")) * sc
-                print(f"   {lab:16s} {fv:14.3f}")
+                print(f"   {lab:16s} {fv:14.3f} {units.get(k, '')}")
             except ValueError:
                 pass
         st = []
