@@ -21,11 +21,19 @@ __host__ __device__ __forceinline__ int wrap(int i, int n) {
 // tendency (model.py:20-22): ((x[i+1] - x[i-2]) * x[i-1] - x[i]) + F
 __device__ __forceinline__ double l96_f(double xp1, double xm2, double xm1,
                                         double x0, double F) {
+#ifdef EDAK_EXP_FMA  // timing experiment: contracted (not bit-exact) stages
+  return fma(xp1 - xm2, xm1, -x0) + F;
+#else
   return __dadd_rn(__dsub_rn(__dmul_rn(__dsub_rn(xp1, xm2), xm1), x0), F);
+#endif
 }
 // stage update x + c*k (model.py:41,43,45): rounded product then sum
 __device__ __forceinline__ double axpy_rn(double x, double c, double k) {
+#ifdef EDAK_EXP_FMA
+  return fma(c, k, x);
+#else
   return __dadd_rn(x, __dmul_rn(c, k));
+#endif
 }
 
 // ---- tangent-linear / adjoint tendencies (FMA allowed; rel ~1e-16) ----
