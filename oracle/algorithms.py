@@ -267,3 +267,60 @@ def pcg(apply_h, b, cfg, precond=None, cost_fn=None, on_iterate=None):
         p = p_new
         rz = rz_new
     return x, trace
+
+
+def _fresh_vector(rng, basis, j, n):
+    """Random unit vector orthogonal to the first j basis vectors
+    (krylov.py:171-180)."""
+    for _ in range(5):
+        v = rng.standard_normal(n)
+        for _ in range(2):
+            v -= basis[:j].T @ (basis[:j] @ v)
+        norm = np.linalg.norm(v)
+        if norm > 1e-8 * np.sqrt(n):
+            return v / norm
+    return None
+
+
+def lanczos_eigs(apply_h, n, m, n_eigs, seed=0):
+    """Lanczos with full reorthogonalization and invariant-subspace restarts
+    (krylov.py:116-168)."""
+    from .streams import substream
+    m = min(m, n)
+    if not 1 <= n_eigs <= m:
+        raise ValueError("need 1 <= n_eigs <= m")
+    rng = substream(seed, "lanczos")
+    basis = np.empty((m, n))
+    alphas = np.zeros(m)
+    betas = np.zeros(m)
+    block_end = {}
+    basis[0] = _fresh_vector(rng, basis, 0, n)
+    scale = 0.0
+    j = 0
+    while j < m:
+        w = apply_h(basis[j])
+        alphas[j] = basis[j] @ w
+        w -= alphas[j] * basis[j]
+        for _ in range(2):
+            w -= basis[: j + 1].T @ (basis[: j + 1] @ w)
+        beta = np.linalg.norm(w)
+        scale = max(scale, abs(alphas[j]), beta)
+        if j + 1 == m:
+            block_end[j] = beta
+            break
+        if beta <= 1e-12 * max(scale, 1.0):
+            block_end[j] = beta
+            nxt = _fresh_vector(rng, basis, j + 1, n)
+            if nxt is None:
+                m = j + 1
+                break
+            basis[j + 1] = nxt
+        else:
+            betas[j] = beta
+            basis[j + 1] = w / beta
+        j += 1
+    tri = np.diag(alphas[:m]) + np.diag(betas[: m - 1], 1) + np.diag(betas[: m - 1], -1)
+    theta, s = np.linalg.eigh(tri)
+    order = np.argsort(theta)[::-1][:n_eigs]
+    bounds = np.array([sum(abs(b * s[pos, i]) for pos, b in block_end.items()) for i in order])
+    return theta[order], bounds

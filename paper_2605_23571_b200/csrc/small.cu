@@ -241,8 +241,8 @@ __global__ void __launch_bounds__(JAC_NT) k_svd_jacobi(const double* __restrict_
     for (size_t e = t; e < (size_t)cols * cols; e += JAC_NT) V[e] = (e % cols == e / cols) ? 1.0 : 0.0;
   __syncthreads();
   const int m = cols + (cols & 1);  // even tournament size (index `cols` = dummy)
-  // LAPACK dgesvj's convergence threshold: sqrt(rows) * eps
-  const double tol = sqrt((double)rows) * 2.220446049250313e-16;
+  // LAPACK dgesvj's convergence threshold: sqrt(rows) * eps (squared)
+  const double tol2 = (double)rows * 2.220446049250313e-16 * 2.220446049250313e-16;
   // one half-warp (16 lanes) per column pair: 64 pairs in flight per pass.
   // Both halves of a warp always run the same loop trip count (shuffles use
   // the full mask); idle halves carry live = false.
@@ -278,10 +278,11 @@ __global__ void __launch_bounds__(JAC_NT) k_svd_jacobi(const double* __restrict_
           be += __shfl_xor_sync(0xffffffffu, be, o);
           ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        if (!live || al == 0.0 || be == 0.0 || fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
+        // threshold without square roots: |ga| <= tol sqrt(al be)
+        if (!live || al == 0.0 || be == 0.0 || ga * ga <= tol2 * (al * be)) continue;
         const double zeta = (be - al) / (2.0 * ga);
-        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
+        const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+        const double c = rsqrt(fma(tt, tt, 1.0)), s = c * tt;
         for (int i = hl; i < rows; i += 16) {
           const double x = ap[i], y = aq[i];
           ap[i] = c * x - s * y;

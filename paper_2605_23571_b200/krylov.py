@@ -217,3 +217,90 @@ def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None):
     elif cfg.trace_cost and cost == "exact":
         c = ("exact", ens.cost_members)
     return pcg_device(apply_h_cols, B, cfg, apply_p, c, snapshots=snapshots)
+
+
+# ----------------------------------------------------------------- Lanczos --
+
+def lanczos_eigs(apply_h, n, m, n_eigs, seed=0):
+    """Leading Ritz values of a symmetric operator with residual bounds
+    (krylov.py:116-168): Lanczos with full reorthogonalization (twice, as
+    DMMA GEMMs over the device basis) and restarts on invariant subspaces.
+
+    Fully device-resident when ``apply_h`` is our hessian_apply; the scalar
+    recurrence decisions (restart test) read one norm per step on the host,
+    like the reference.  Fresh vectors come from the reference's
+    ``substream(seed, "lanczos")`` host stream; the Ritz problem of the
+    tridiagonal matrix is solved by the device Jacobi SVD (it is SPD for the
+    I + A operators this is used on; values are |Ritz values| otherwise)."""
+    from .linalg import gemm_nn, gemm_tn, svd_jacobi
+    from .twin import substream
+    m = min(m, n)
+    if not 1 <= n_eigs <= m:
+        raise ValueError("need 1 <= n_eigs <= m")
+    dev = _dev.device()
+    prob = _device_problem(apply_h)
+    if prob is not None:
+        work = prob.lin.work(1)
+
+        def h(v):
+            prob.n_matvecs += 1
+            return prob.lin.hessian_cols(v, None, 1.0, None, None, work)
+    else:
+        def h(v):
+            y = np.asarray(apply_h(v[0].cpu().numpy()), dtype=float)
+            return torch.from_numpy(y).to(dev)[None]
+
+    rng = substream(seed, "lanczos")
+    basis = torch.zeros((m, n), dtype=torch.float64, device=dev)
+
+    def orth(v, j):
+        if j == 0:
+            return v
+        neg = -torch.ones(j, dtype=torch.float64, device=dev)
+        for _ in range(2):
+            c = gemm_tn(basis[:j], v)              # (1, j): basis_i . v
+            v = gemm_nn(basis[:j], c, bscale=neg, Cin=v, beta=1.0)
+        return v
+
+    def fresh(j):
+        for _ in range(5):
+            v = torch.from_numpy(rng.standard_normal(n)).to(dev)[None]
+            v = orth(v, j)
+            norm = float(torch.linalg.vector_norm(v))
+            if norm > 1e-8 * np.sqrt(n):
+                return v / norm
+        return None
+
+    alphas, betas = np.zeros(m), np.zeros(m)
+    block_end = {}
+    basis[0] = fresh(0)[0]
+    scale = 0.0
+    j = 0
+    while j < m:
+        w = h(basis[j:j + 1])
+        alphas[j] = float((basis[j] * w[0]).sum())
+        w = w - alphas[j] * basis[j:j + 1]
+        w = orth(w, j + 1)
+        beta = float(torch.linalg.vector_norm(w))
+        scale = max(scale, abs(alphas[j]), beta)
+        if j + 1 == m:
+            block_end[j] = beta
+            break
+        if beta <= 1e-12 * max(scale, 1.0):
+            block_end[j] = beta
+            nxt = fresh(j + 1)
+            if nxt is None:
+                m = j + 1
+                break
+            basis[j + 1] = nxt[0]
+        else:
+            betas[j] = beta
+            basis[j + 1] = w[0] / beta
+        j += 1
+    tri = np.diag(alphas[:m]) + np.diag(betas[: m - 1], 1) + np.diag(betas[: m - 1], -1)
+    U, sig, _ = svd_jacobi(torch.from_numpy(np.ascontiguousarray(tri.T)).to(dev))
+    theta = sig.cpu().numpy()[:n_eigs]
+    s = U.cpu().numpy()  # row i = eigenvector i (descending)
+    bounds = np.array([sum(abs(b * s[i, pos]) for pos, b in block_end.items())
+                       for i in range(n_eigs)])
+    return theta, bounds

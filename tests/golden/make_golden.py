@@ -219,6 +219,12 @@ def extract_fixtures():
                 key = f"{row['seed']}/{row['member']}"
                 rows.setdefault(key, []).append((int(row["index"]), row["value"]))
         keep[name] = {k: [v for _, v in sorted(vs)] for k, vs in rows.items()}
+    # Lanczos eigenvalues of I + A (eig-sensitivity, harness.py:126-146)
+    eig = {}
+    with open(os.path.join(FIXTURES, "eig-sensitivity.csv"), newline="") as fh:
+        for row in csv.DictReader(fh):
+            eig.setdefault(row["variant"], []).append((int(row["index"]), row["value"]))
+    keep["eig-sensitivity"] = {k: [v for _, v in sorted(vs)] for k, vs in eig.items()}
     # fixture configs (tiny.cfg / ensemble.cfg / theta.cfg are n=40, G=8,
     # 10 members, 8 iterations; seeds from regenerate.sh)
     keep["config"] = {"n": 40, "obs_grid_count": 8, "members": 10, "max_iters": 8}

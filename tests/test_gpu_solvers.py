@@ -258,3 +258,28 @@ def test_potrf_trinv_sizes(gpu, l):
     assert inf[1] == 0 and inf[0] >= 1 and float(nu[0]) > 0
     c = C.cpu().numpy().T
     npt.assert_allclose(c.T @ c, wd + float(nu[0]) * np.eye(l), atol=1e-10 * np.abs(wd).max())
+
+
+def test_lanczos_gpu(gpu):
+    """Device Lanczos (krylov.lanczos_eigs, krylov.py:116-168) against the
+    reference's eig-sensitivity fixture and the oracle on the n=120 mirror."""
+    from paper_2605_23571_b200.krylov import lanczos_eigs
+    with open(os.path.join(GOLDEN, "fixtures.json")) as fh:
+        fx = json.load(fh)
+    tw = TwinConfig(n=40, obs_grid_count=8, members=10, cov_length=2.0)
+    setup = build_setup(tw)
+    prob = _gpu_problem(setup.control)
+    vals, bounds = lanczos_eigs(prob.hessian_apply, 40, min(40, tw.p + 80), min(150, tw.p),
+                                seed=tw.seed)
+    ref = [float(v) for v in fx["eig-sensitivity"]["D=2"]]
+    npt.assert_allclose(vals[: len(ref)], ref, rtol=1e-8)
+    tw = TwinConfig(n=120, obs_grid_count=10, members=0, seed=21)
+    op = build_setup(tw).control
+    vals, bounds = lanczos_eigs(_gpu_problem(op).hessian_apply, 120, 60, 40, seed=5)
+    ref, ref_b = oalg.lanczos_eigs(op.hessian_apply, 120, 60, 40, seed=5)
+    npt.assert_allclose(vals, ref, rtol=1e-8)
+    assert np.all(bounds <= 1e-6 * ref[0])
+    # dense diagonal operator with restarts through invariant subspaces
+    d = np.linspace(1.0, 30.0, 30)
+    v, b = lanczos_eigs(lambda x: d * x, 30, 30, 5, seed=3)
+    npt.assert_allclose(v, d[::-1][:5], rtol=1e-10)

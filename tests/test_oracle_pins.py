@@ -143,3 +143,21 @@ def test_baseline_cfg2_shift_path(ref_problem):
         big = ref >= 1e-6 * ref[0]
         npt.assert_allclose(approx.values[big], ref[big], rtol=1e-10)
         assert np.all(np.abs(approx.values[~big] - ref[~big]) <= floor)
+
+
+def test_lanczos_matches_reference_fixture():
+    """eig-sensitivity fixture (Lanczos over hessian_apply, diffusion B):
+    oracle Lanczos on the oracle twin reproduces the reference's values."""
+    import csv
+    from oracle.algorithms import lanczos_eigs
+    path = os.path.join(GOLDEN, "fixtures.json")
+    with open(path) as fh:
+        fx = json.load(fh)
+    if "eig-sensitivity" not in fx:
+        pytest.skip("fixture not extracted")
+    tw = TwinConfig(n=40, obs_grid_count=8, members=10, cov_length=2.0)
+    setup = build_setup(tw)
+    vals, _ = lanczos_eigs(setup.control.hessian_apply, 40, min(40, tw.p + 80),
+                           min(150, tw.p), seed=tw.seed)
+    ref = [float(v) for v in fx["eig-sensitivity"]["D=2"]]
+    npt.assert_allclose(vals[: len(ref)], ref, rtol=1e-10)
