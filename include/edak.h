@@ -46,7 +46,9 @@ typedef struct edak_problem {
   const double* states;
   const double* stages;
   int64_t traj_stride;   /* doubles between consecutive trajectories        */
-  int32_t stage_mode;    /* 0 = recompute stages from states, 1 = stream    */
+  int32_t stage_mode;    /* 0 = recompute stages from states, 1 = stream all
+                          * four stored stages, 2 = hybrid: stream x1..x3
+                          * and recompute x4 (stages buffer required)       */
   int32_t pad0;
   /* observation network (ObsNetwork, obs.py:23-41) as position maps */
   const int32_t* gpos;   /* [n]: position of grid point i in net.grid, or -1 */

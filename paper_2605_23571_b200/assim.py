@@ -23,7 +23,8 @@ from . import _dev, _lib
 from .covariance import device_factor
 from .obs import DeviceNetwork
 
-STAGE_MODES = ("auto", "recompute", "stream")
+STAGE_MODES = ("auto", "recompute", "stream", "hybrid")
+_MODE_CODE = {"recompute": 0, "stream": 1, "hybrid": 2}
 
 
 def _prob_struct(n, n_steps, dt, forcing, states, stages, traj_stride, stage_mode,
@@ -33,7 +34,7 @@ def _prob_struct(n, n_steps, dt, forcing, states, stages, traj_stride, stage_mod
     P.states = states.data_ptr() if states is not None else None
     P.stages = stages.data_ptr() if stages is not None else None
     P.traj_stride = traj_stride
-    P.stage_mode = 1 if stage_mode == "stream" else 0
+    P.stage_mode = _MODE_CODE[stage_mode]
     P.gpos, P.tpos = dnet.gpos.data_ptr(), dnet.tpos.data_ptr()
     P.G, P.T = dnet.G, dnet.T
     P.sigma2 = float(sigma2)
@@ -84,18 +85,18 @@ class Linearization:
             else:
                 stage_mode = ("recompute" if stages_recomputable(states, stages, dt, forcing)
                               else "stream")
-        if stage_mode == "stream" and stages is None:
-            raise ValueError("stage_mode='stream' needs the stored stages")
+        if stage_mode in ("stream", "hybrid") and stages is None:
+            raise ValueError(f"stage_mode={stage_mode!r} needs the stored stages")
         self.stage_mode = stage_mode
         self.states = states
-        self.stages = stages if stage_mode == "stream" else None
+        self.stages = stages if stage_mode in ("stream", "hybrid") else None
         self.dt, self.forcing = float(dt), float(forcing)
         self.net, self.ub, self.rn = net, ub, rn
         self.dnet = DeviceNetwork(net, self.n, self.n_steps)
         self.dfac = device_factor(ub)
         self.p = self.dnet.p
         self.sigma2 = float(rn.sigma) ** 2
-        stride = (self.stages[0].numel() if stage_mode == "stream"
+        stride = (self.stages[0].numel() if self.stages is not None
                   else states[0].numel())
         self._P = _prob_struct(self.n, self.n_steps, dt, forcing, states, self.stages,
                                stride, stage_mode, self.dnet, self.dfac, self.sigma2)

@@ -58,7 +58,7 @@ static bool bad_problem(const edak_problem* P) {
     set_error("invalid edak_problem");
     return true;
   }
-  if ((P->stage_mode == 0 && !P->states) || (P->stage_mode == 1 && !P->stages)) {
+  if ((P->stage_mode == 0 && !P->states) || (P->stage_mode != 0 && !P->stages)) {
     set_error("edak_problem: trajectory buffer missing for stage_mode");
     return true;
   }

@@ -464,6 +464,10 @@ static int plan_chunks(int N, bool periodic, const double* work2) {
 }
 
 int sweep2_mode(const edak_problem* P, int K);
+int sweep3_mode(const edak_problem* P, int K);
+int launch_tl3(const edak_problem*, const double*, double*, int, const int32_t*, int, int, double*, cudaStream_t);
+int launch_ad3(const edak_problem*, const double*, double*, int, const int32_t*, int, int, const double*,
+               cudaStream_t);
 int launch_tl2(const edak_problem*, const double*, double*, int, const int32_t*, int, int, double*, cudaStream_t);
 int launch_ad2(const edak_problem*, const double*, double*, int, const int32_t*, int, int, const double*,
                cudaStream_t);
@@ -473,6 +477,20 @@ int launch_tl(const edak_problem* P, const double* v0, double* obs, int ncols, c
   int C, NT, nt;
   SweepGeom geo;
   const int N = P->n_steps;
+  if (const int m3 = sweep3_mode(P, SWEEP_CHUNK)) {  // hybrid storage: stream x1..x3
+    const int nch = (m3 == 1 || !work2 || N <= SWEEP_CHUNK) ? 1 : (N + SWEEP_CHUNK - 1) / SWEEP_CHUNK;
+    if (!(m3 == 2 && nch == 1 && N > SWEEP_CHUNK && sweep3_mode(P, N) == 0)) {
+      const size_t blk = (size_t)ncols * P->n;
+      for (int c = 0; c < nch; ++c) {
+        const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch);
+        const double* vin = c == 0 ? v0 : work2 + (size_t)((c - 1) & 1) * blk;
+        double* vout = c + 1 < nch ? work2 + (size_t)(c & 1) * blk : nullptr;
+        int rc = launch_tl3(P, vin, obs, ncols, col_traj, s0, s1, vout, st);
+        if (rc) return rc;
+      }
+      return EDAK_OK;
+    }
+  }
   if (const int m2 = sweep2_mode(P, SWEEP_CHUNK)) {  // shared-memory-staged kernels
     const int nch = (m2 == 1 || !work2 || N <= SWEEP_CHUNK || getenv("EDAK_SWEEP_NOCHUNK"))
                         ? 1 : (N + SWEEP_CHUNK - 1) / SWEEP_CHUNK;
@@ -496,7 +514,7 @@ v1:
     return EDAK_EUNSUPPORTED;
   }
   const int nch = plan_chunks(N, geo.periodic && nt == 1, work2);
-  const bool stream = P->stage_mode == 1;
+  const bool stream = P->stage_mode != 0;  // 1 stream, 2 hybrid (small rings)
   const size_t blk = (size_t)ncols * P->n;
   for (int c = 0; c < nch; ++c) {
     const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch), K = s1 - s0;
@@ -533,6 +551,20 @@ int launch_ad(const edak_problem* P, const double* forcing, double* g, int ncols
   int C, NT, nt;
   SweepGeom geo;
   const int N = P->n_steps;
+  if (const int m3 = sweep3_mode(P, SWEEP_CHUNK)) {  // hybrid storage: stream x1..x3
+    const int nch = (m3 == 1 || !work2 || N <= SWEEP_CHUNK) ? 1 : (N + SWEEP_CHUNK - 1) / SWEEP_CHUNK;
+    if (!(m3 == 2 && nch == 1 && N > SWEEP_CHUNK && sweep3_mode(P, N) == 0)) {
+      const size_t blk = (size_t)ncols * P->n;
+      for (int c = nch - 1, k = 0; c >= 0; --c, ++k) {
+        const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch);
+        const double* gin = k == 0 ? nullptr : work2 + (size_t)((k - 1) & 1) * blk;
+        double* gout = c == 0 ? g : work2 + (size_t)(k & 1) * blk;
+        int rc = launch_ad3(P, forcing, gout, ncols, col_traj, s0, s1, gin, st);
+        if (rc) return rc;
+      }
+      return EDAK_OK;
+    }
+  }
   if (const int m2 = sweep2_mode(P, SWEEP_CHUNK)) {
     const int nch = (m2 == 1 || !work2 || N <= SWEEP_CHUNK || getenv("EDAK_SWEEP_NOCHUNK"))
                         ? 1 : (N + SWEEP_CHUNK - 1) / SWEEP_CHUNK;
@@ -555,7 +587,7 @@ v1:
     return EDAK_EUNSUPPORTED;
   }
   const int nch = plan_chunks(N, geo.periodic && nt == 1, work2);
-  const bool stream = P->stage_mode == 1;
+  const bool stream = P->stage_mode != 0;  // 1 stream, 2 hybrid (small rings)
   const size_t blk = (size_t)ncols * P->n;
   for (int c = nch - 1, k = 0; c >= 0; --c, ++k) {
     const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch), K = s1 - s0;

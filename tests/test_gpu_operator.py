@@ -191,3 +191,22 @@ def test_ensemble_per_member_trajectories(gpu):
     AZ = ens.a_apply_members(Z).cpu().numpy()
     for j, o in enumerate(ops):
         assert rel(AZ[j], o.a_apply(Z[j].cpu().numpy())) < 1e-12
+
+
+def test_hybrid_equals_recompute(gpu):
+    """stage_mode "hybrid" (stream x1..x3, recompute x4; sweep3.cu) gives the
+    same bits as recomputing every stage, in tile mode (n=16384, chunked
+    window) and periodic mode (n=1024)."""
+    from paper_2605_23571_b200.assim import Linearization
+    from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
+    for n, N, L in [(16384, 24, 16.0), (1024, 16, 8.0)]:
+        op = _oracle_problem(n, N, 4, 3, L, 9)
+        ub = CirculantFactor(n, op.ub.symbol)
+        a = Linearization(op.traj.states[None], 0.025, 8.0, op.net, ub, DiagonalNoise(1.0),
+                          op.traj.stages[None], "recompute")
+        b = Linearization(op.traj.states[None], 0.025, 8.0, op.net, ub, DiagonalNoise(1.0),
+                          op.traj.stages[None], "hybrid")
+        z = torch.randn(3, n, dtype=torch.float64, device="cuda")
+        assert torch.equal(a.hessian_cols(z), b.hessian_cols(z))
+        d = torch.randn(3, op.net.p, dtype=torch.float64, device="cuda")
+        assert torch.equal(a.rhs_cols(d), b.rhs_cols(d))

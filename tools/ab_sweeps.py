@@ -58,3 +58,25 @@ for mode in modes:
     t_h = timeit(lambda: ens.a_apply_members(V, ident=1.0))
     print(f"cfg{cfg.name[-1]} {mode}: TL {t_tl:.3f} ms  AD {t_ad:.3f} ms  hessian {t_h:.3f} ms  "
           f"identical={same}", flush=True)
+
+# hybrid storage (stream x1..x3, recompute x4) vs state-only recompute
+if os.environ.get("HYBRID_AB", "1") == "1":
+    from paper_2605_23571_b200.assim import Linearization
+    from paper_2605_23571_b200.model import integrate_device
+    for k in ("EDAK_SWEEP_V2", "EDAK_SWEEP_NOCHUNK", "EDAK_SWEEP_FAMILY"):
+        os.environ.pop(k, None)
+    st, sg = integrate_device(dens.x0, cfg.dt, cfg.n_steps, cfg.forcing, want_stages=True)
+    hyb = Linearization(st, cfg.dt, cfg.forcing, dens.net, dens.ub, dens.rn, sg, "hybrid")
+    rec = Linearization(st, cfg.dt, cfg.forcing, dens.net, dens.ub, dens.rn, None, "recompute")
+    ct = torch.arange(1, ens.M + 1, dtype=torch.int32, device="cuda") % st.shape[0]
+    for name, L in (("recompute", rec), ("hybrid", hyb)):
+        o = L.tl_cols(V, ct)
+        gg = L.ad_cols(W, ct)
+        if name == "recompute":
+            ro, rg = o, gg
+        same = bool(torch.equal(o, ro)) and bool(torch.equal(gg, rg))
+        t_tl = timeit(lambda: L.tl_cols(V, ct))
+        t_ad = timeit(lambda: L.ad_cols(W, ct))
+        t_h = timeit(lambda: L.hessian_cols(V, ct, 1.0))
+        print(f"cfg{cfg.name[-1]} {name}: TL {t_tl:.3f} ms  AD {t_ad:.3f} ms  hessian {t_h:.3f} ms  "
+              f"identical={same}", flush=True)
