@@ -111,7 +111,12 @@ int64_t edak_work_doubles(const edak_problem* P, int ncols);
  * NULL, receives the raw TL observations G U_B z (ncols x p). */
 int edak_hessian_block(const edak_problem* P, const double* z, double* az,
                        int ncols, const int32_t* col_traj, double ident,
-                       double* work, double* obs_out, void* stream);
+                       double* work, double* obs_out, double* dot_part,
+                       void* stream);
+/* when ident != 0 and dot_part != NULL the final U_B pass also writes tile
+ * partials of z[c] . az[c] (PCG p . Hp): dot_part[c * tiles + t],
+ * tiles = edak_hessian_dot_tiles(n) */
+int64_t edak_hessian_dot_tiles(int n);
 /* b[c] = U_B^T G^T R^-1 d[c]  (MemberProblem.rhs, assim.py:74-77) */
 int edak_rhs(const edak_problem* P, const double* innov, double* b, int ncols,
              const int32_t* col_traj, double* work, void* stream);
@@ -178,7 +183,16 @@ int edak_pcg_cost0(int p_obs, int ncols, const double* d, double sigma2,
  * krylov.py:79-89,108-113) */
 int edak_pcg_alpha(int n, int ncols, const double* p, const double* hp,
                    double* x, double* r, double* work, int32_t* status,
-                   int32_t* iters, int it, const double* b, void* stream);
+                   int32_t* iters, int it, const double* b,
+                   const double* php_part, int php_tiles, void* stream);
+/* Fused single-pass-LMP step: W = S^T r; rz_new = |r|^2 + W^T diag(coef) W
+ * (= r.Pr exactly); record / stop test / beta; p = r + beta p + S(coef o W)
+ * (= Pr + beta p, krylov.py:86-96) in the GEMM epilogue.  lmpwork >=
+ * edak_lmp_work_doubles(n, k, ncols). */
+int edak_pcg_lmp_beta(int n, int k, int ncols, const double* S, const double* coef,
+                      const double* r, double* p, double* work, double* lmpwork,
+                      double rtol, double* hist_rz, double* hist_J, int hist_ld,
+                      int32_t* status, int32_t* iters, int it, void* stream);
 /* rz_new = r.z, hist_rz[., it] (+ hist_J[., it] when not NULL), stop test
  * (rtol < 0 = None), p = z + beta p (krylov.py:86-96) */
 int edak_pcg_beta(int n, int ncols, const double* z, const double* r, double* p,

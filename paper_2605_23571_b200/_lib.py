@@ -39,7 +39,8 @@ _PROTOS = {
     "edak_tl_sweep": (C.c_int, [C.POINTER(Problem), vp, vp, C.c_int, vp, vp, vp]),
     "edak_ad_sweep": (C.c_int, [C.POINTER(Problem), vp, vp, C.c_int, vp, vp, vp]),
     "edak_work_doubles": (i64, [C.POINTER(Problem), C.c_int]),
-    "edak_hessian_block": (C.c_int, [C.POINTER(Problem), vp, vp, C.c_int, vp, f64, vp, vp, vp]),
+    "edak_hessian_block": (C.c_int, [C.POINTER(Problem), vp, vp, C.c_int, vp, f64, vp, vp, vp, vp]),
+    "edak_hessian_dot_tiles": (i64, [C.c_int]),
     "edak_rhs": (C.c_int, [C.POINTER(Problem), vp, vp, C.c_int, vp, vp, vp]),
     "edak_cost": (C.c_int, [C.POINTER(Problem), vp, vp, vp, C.c_int, vp, vp, vp]),
     "edak_gemm_tn_partials": (i64, [C.c_int, C.c_int, i64]),
@@ -53,7 +54,10 @@ _PROTOS = {
     "edak_pcg_work_doubles": (i64, [C.c_int, C.c_int]),
     "edak_pcg_init": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, vp, C.c_int, vp, vp, vp]),
     "edak_pcg_cost0": (C.c_int, [C.c_int, C.c_int, vp, f64, vp, C.c_int, vp]),
-    "edak_pcg_alpha": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]),
+    "edak_pcg_alpha": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, vp, C.c_int, vp, vp, C.c_int,
+                                 vp]),
+    "edak_pcg_lmp_beta": (C.c_int, [C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, f64, vp, vp,
+                                    C.c_int, vp, vp, C.c_int, vp]),
     "edak_pcg_beta": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, vp, f64, vp, vp, C.c_int, vp, vp,
                                 C.c_int, vp]),
     "edak_lmp_work_doubles": (i64, [C.c_int, C.c_int, C.c_int]),

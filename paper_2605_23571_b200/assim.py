@@ -119,8 +119,15 @@ class Linearization:
         k = int(_lib.lib().edak_sweep_work_doubles(_lib.C.byref(self._P), ncols))
         return torch.empty(k, dtype=torch.float64, device=self.states.device)
 
-    def hessian_cols(self, Z, col_traj=None, ident=0.0, obs_out=None, out=None, work=None):
-        """out = ident * Z + A Z for a (ncols, n) device block."""
+    def dot_tiles(self):
+        """Tile count of the p.Hp partials the fused U_B pass can emit."""
+        return int(_lib.lib().edak_hessian_dot_tiles(self.n))
+
+    def hessian_cols(self, Z, col_traj=None, ident=0.0, obs_out=None, out=None, work=None,
+                     dot_part=None):
+        """out = ident * Z + A Z for a (ncols, n) device block; with ident != 0
+        and ``dot_part`` (ncols, dot_tiles()) also the tile partials of
+        Z[c].out[c] (PCG p.Hp) from the last U_B pass's epilogue."""
         Z = Z.contiguous()
         ncols = Z.shape[0]
         ct = self._map(col_traj, ncols)
@@ -128,7 +135,7 @@ class Linearization:
         work = self.work(ncols) if work is None else work
         _lib.call("edak_hessian_block", _lib.C.byref(self._P), Z.data_ptr(), out.data_ptr(),
                   ncols, _lib.ptr(ct), float(ident), work.data_ptr(), _lib.ptr(obs_out),
-                  _lib.stream())
+                  _lib.ptr(dot_part), _lib.stream())
         return out
 
     def rhs_cols(self, D, col_traj=None):
@@ -315,10 +322,10 @@ class Ensemble:
         """All members' right-hand sides, (M, n) device block (one launch)."""
         return self.lin.rhs_cols(self.D, self.traj_of)
 
-    def a_apply_members(self, Z, ident=0.0, obs_out=None, out=None, work=None):
+    def a_apply_members(self, Z, ident=0.0, obs_out=None, out=None, work=None, dot_part=None):
         """Column j of Z through member j's Hessian term: (M, n) -> (M, n)."""
         self.n_matvecs += 1
-        return self.lin.hessian_cols(Z, self.traj_of, ident, obs_out, out, work)
+        return self.lin.hessian_cols(Z, self.traj_of, ident, obs_out, out, work, dot_part)
 
     def cost_members(self, Z):
         return self.lin.cost_cols(Z, self.D, self.traj_of)

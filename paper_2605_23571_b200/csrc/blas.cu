@@ -158,7 +158,8 @@ __global__ void __launch_bounds__(256) k_gemm_nn(const double* __restrict__ A, i
                                                  const double* __restrict__ B, int ldb,
                                                  const double* __restrict__ bscale, const double* Cin,
                                                  int64_t ldc, double beta, double* D, int64_t ldd, int64_t M,
-                                                 int N, int kk) {
+                                                 int N, int kk, const double* __restrict__ colscale,
+                                                 const double* C2) {
   extern __shared__ __align__(16) double gsm[];
   double (*sA)[G_BK][G_BM + G_PAD] = reinterpret_cast<double (*)[G_BK][G_BM + G_PAD]>(gsm);
   double (*sB)[G_BN][G_BK + G_PAD] =
@@ -227,20 +228,22 @@ __global__ void __launch_bounds__(256) k_gemm_nn(const double* __restrict__ A, i
         if (gi < M && gj < N) {
           double v = acc[i][j][h];
           if (Cin) v += beta * Cin[gi + gj * ldc];
+          if (C2) v += colscale[gj] * C2[gi + gj * ldd];  // C2 may alias D
           D[gi + gj * ldd] = v;
         }
       }
 }
 
 int launch_gemm_nn(const double* A, int64_t lda, const double* B, int ldb, const double* bscale, const double* Cin,
-                   int64_t ldc, double beta, double* D, int64_t ldd, int64_t M, int N, int kk, cudaStream_t st) {
+                   int64_t ldc, double beta, double* D, int64_t ldd, int64_t M, int N, int kk, cudaStream_t st,
+                   const double* colscale, const double* C2) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_gemm_nn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G_SMEM);
     attr = true;
   }
   dim3 grid((unsigned)((M + G_BM - 1) / G_BM), (N + G_BN - 1) / G_BN);
-  k_gemm_nn<<<grid, 256, G_SMEM, st>>>(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M, N, kk);
+  k_gemm_nn<<<grid, 256, G_SMEM, st>>>(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M, N, kk, colscale, C2);
   count_launch();
   return check_launch("k_gemm_nn");
 }

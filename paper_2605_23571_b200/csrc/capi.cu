@@ -31,12 +31,15 @@ int launch_integrate(int, int, double, double, const double*, int, double*, int6
                      cudaStream_t);
 int launch_observe(const double*, int64_t, int, const int32_t*, int, const int32_t*, int, int, double*,
                    cudaStream_t);
-int launch_circ(const edak_problem*, const double*, double*, int, double, const double*, cudaStream_t);
+int launch_circ(const edak_problem*, const double*, double*, int, double, const double*, cudaStream_t,
+                double* dotp = nullptr);
+int circ_tiles(int n);
 int64_t gemm_tn_partials(int, int, int64_t);
 int launch_gemm_tn(const double*, int64_t, const double*, int64_t, double*, int, int, int, int64_t, double*,
                    cudaStream_t);
 int launch_gemm_nn(const double*, int64_t, const double*, int, const double*, const double*, int64_t, double,
-                   double*, int64_t, int64_t, int, int, cudaStream_t);
+                   double*, int64_t, int64_t, int, int, cudaStream_t, const double* colscale = nullptr,
+                   const double* C2 = nullptr);
 int launch_col_dots(int, int, const double*, const double*, double*, cudaStream_t);
 int launch_potrf_shifted(const double*, int, double*, int, double, double*, int32_t*, cudaStream_t);
 int launch_trinv_upper(const double*, int, double*, cudaStream_t);
@@ -46,7 +49,10 @@ int64_t pcg_work_doubles(int, int);
 int launch_pcg_init(int, int, const double*, const double*, double*, double*, double*, double*, double*, int,
                     int32_t*, int32_t*, cudaStream_t);
 int launch_pcg_alpha(int, int, const double*, const double*, double*, double*, double*, int32_t*, int32_t*, int,
-                     const double*, cudaStream_t);
+                     const double*, const double*, int, cudaStream_t);
+int launch_pcg_rz(int, int, int, const double*, const double*, double*, double, double*, double*, int, int32_t*,
+                  int32_t*, int, cudaStream_t);
+double* pcg_beta_ptr(int, int, double*);
 int launch_pcg_beta(int, int, const double*, const double*, double*, double*, double, double*, double*, int,
                     int32_t*, int32_t*, int, cudaStream_t);
 int launch_pcg_cost0(int, int, const double*, double, double*, int, cudaStream_t);
@@ -124,9 +130,15 @@ int64_t edak_work_doubles(const edak_problem* P, int ncols) {
   return (int64_t)ncols * (4 * (int64_t)P->n + (int64_t)P->G * P->T);
 }
 
+int64_t edak_hessian_dot_tiles(int n) { return circ_tiles(n); }
+
 int edak_hessian_block(const edak_problem* P, const double* z, double* az, int ncols, const int32_t* col_traj,
-                       double ident, double* work, double* obs_out, void* stream) {
+                       double ident, double* work, double* obs_out, double* dot_part, void* stream) {
   if (bad_problem(P) || !z || !az || !work) return EDAK_EINVAL;
+  if (dot_part && ident == 0.0) {
+    set_error("edak_hessian_block: dot_part needs ident != 0 (p.Hp of the I + A apply)");
+    return EDAK_EINVAL;
+  }
   if (ncols == 0) return EDAK_OK;
   cudaStream_t st = as_stream(stream);
   const int64_t n = P->n, p = (int64_t)P->G * P->T;
@@ -139,7 +151,7 @@ int edak_hessian_block(const edak_problem* P, const double* z, double* az, int n
   if ((rc = launch_circ(P, z, v0, ncols, 0.0, nullptr, st))) return rc;
   if ((rc = launch_tl(P, v0, obs, ncols, col_traj, st, w2))) return rc;
   if ((rc = launch_ad(P, obs, g, ncols, col_traj, st, w2))) return rc;
-  return launch_circ(P, g, az, ncols, ident, ident != 0.0 ? z : nullptr, st);
+  return launch_circ(P, g, az, ncols, ident, ident != 0.0 ? z : nullptr, st, dot_part);
 }
 
 int edak_rhs(const edak_problem* P, const double* innov, double* b, int ncols, const int32_t* col_traj, double* work,
@@ -217,9 +229,11 @@ int edak_pcg_cost0(int p_obs, int ncols, const double* d, double sigma2, double*
 }
 
 int edak_pcg_alpha(int n, int ncols, const double* p, const double* hp, double* x, double* r, double* work,
-                   int32_t* status, int32_t* iters, int it, const double* b, void* stream) {
+                   int32_t* status, int32_t* iters, int it, const double* b, const double* php_part, int php_tiles,
+                   void* stream) {
   if (ncols == 0) return EDAK_OK;
-  return launch_pcg_alpha(n, ncols, p, hp, x, r, work, status, iters, it, b, as_stream(stream));
+  return launch_pcg_alpha(n, ncols, p, hp, x, r, work, status, iters, it, b, php_part, php_tiles,
+                          as_stream(stream));
 }
 
 int edak_pcg_beta(int n, int ncols, const double* z, const double* r, double* p, double* work, double rtol,
@@ -228,6 +242,23 @@ int edak_pcg_beta(int n, int ncols, const double* z, const double* r, double* p,
   if (ncols == 0) return EDAK_OK;
   return launch_pcg_beta(n, ncols, z, r, p, work, rtol, hist_rz, hist_J, hist_ld, status, iters, it,
                          as_stream(stream));
+}
+
+int edak_pcg_lmp_beta(int n, int k, int ncols, const double* S, const double* coef, const double* r, double* p,
+                      double* work, double* lmpwork, double rtol, double* hist_rz, double* hist_J, int hist_ld,
+                      int32_t* status, int32_t* iters, int it, void* stream) {
+  if (ncols == 0) return EDAK_OK;
+  if (!S || !coef || !r || !p || !work || !lmpwork || !hist_rz || !status || !iters) return EDAK_EINVAL;
+  cudaStream_t st = as_stream(stream);
+  double* W = lmpwork;
+  double* part = lmpwork + (int64_t)k * ncols;
+  int rc;
+  // W = S^T r (lmp.py:63); rz_new = |r|^2 + W^T diag(coef) W; beta
+  if ((rc = launch_gemm_tn(S, n, r, n, W, k, k, ncols, n, part, st))) return rc;
+  if ((rc = launch_pcg_rz(n, ncols, k, W, coef, work, rtol, hist_rz, hist_J, hist_ld, status, iters, it, st)))
+    return rc;
+  // p = r + beta p + S (coef o W)  (= z + beta p, krylov.py:95 with z = P r)
+  return launch_gemm_nn(S, n, W, k, coef, r, n, 1.0, p, n, n, ncols, k, st, pcg_beta_ptr(n, ncols, work), p);
 }
 
 int64_t edak_lmp_work_doubles(int n, int k, int ncols) {

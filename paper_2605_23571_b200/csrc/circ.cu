@@ -23,7 +23,8 @@ __device__ __forceinline__ int padi(int q) { return q + q / CIRC_R; }
 template <int R, int NT>
 __global__ void __launch_bounds__(NT) k_circ(int n, const double* __restrict__ taps, int K, int Kp, int w,
                                              const double* __restrict__ in, double* __restrict__ out,
-                                             double ident, const double* __restrict__ zadd) {
+                                             double ident, const double* __restrict__ zadd,
+                                             double* __restrict__ dotp) {
   extern __shared__ double sm[];
   double* st = sm;                      // reversed taps, Kp (zero padded)
   double* sg = sm + Kp;                 // segment, padded
@@ -62,16 +63,38 @@ __global__ void __launch_bounds__(NT) k_circ(int n, const double* __restrict__ t
     for (int r = 0; r < R; ++r) cur[r] = nxt[r];
   }
   double* dst = out + (size_t)col * n;
+  double dp = 0.0;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int i = i0 + t * R + r;
-    if (i < n) dst[i] = zadd ? acc[r] + ident * zadd[(size_t)col * n + i] : acc[r];
+    if (i < n) {
+      double o = acc[r];
+      if (zadd) {
+        const double zi = zadd[(size_t)col * n + i];
+        o += ident * zi;
+        dp += zi * o;  // tile partial of zadd . out (PCG p . Hp, krylov.py:81)
+      }
+      dst[i] = o;
+    }
+  }
+  if (dotp) {  // fixed-order CTA reduction -> dotp[col][tile]
+    __syncthreads();
+    dp = warp_sum(dp);
+    if ((t & 31) == 0) sm[t >> 5] = dp;
+    __syncthreads();
+    if (t == 0) {
+      double s = 0.0;
+      for (int w = 0; w < NT / 32; ++w) s += sm[w];
+      dotp[(size_t)col * gridDim.x + blockIdx.x] = s;
+    }
   }
 }
 
 // out = U_B in (+ ident * zadd when zadd != NULL: the I + A of assim.py:70-72)
+int circ_tiles(int n) { return (n + CIRC_NT * CIRC_R - 1) / (CIRC_NT * CIRC_R); }
+
 int launch_circ(const edak_problem* P, const double* in, double* out, int ncols, double ident,
-                const double* zadd, cudaStream_t st) {
+                const double* zadd, cudaStream_t st, double* dotp) {
   const int n = P->n, K = P->ntaps;
   if (K < 1 || K > CIRC_MAXTAPS) {
     set_error("circulant factor: tap count outside [1, 4096]");
@@ -87,7 +110,7 @@ int launch_circ(const edak_problem* P, const double* in, double* out, int ncols,
     cudaFuncSetAttribute(k_circ<CIRC_R, CIRC_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_circ<CIRC_R, CIRC_NT><<<grid, CIRC_NT, smem, st>>>(n, P->taps, K, Kp, P->tap_w, in, out, ident, zadd);
+  k_circ<CIRC_R, CIRC_NT><<<grid, CIRC_NT, smem, st>>>(n, P->taps, K, Kp, P->tap_w, in, out, ident, zadd, dotp);
   count_launch();
   return check_launch("k_circ");
 }

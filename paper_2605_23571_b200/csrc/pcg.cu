@@ -74,14 +74,15 @@ __global__ void __launch_bounds__(PCG_NT) k_pcg_upd_x(int n, int T, int M, const
                                                       const double* __restrict__ hp, double* __restrict__ x,
                                                       double* __restrict__ r, const double* __restrict__ rzb,
                                                       int32_t* __restrict__ status, int32_t* __restrict__ iters,
-                                                      int it, const double* __restrict__ part_a,
-                                                      double* __restrict__ part_x, const double* __restrict__ b) {
+                                                      int it, const double* __restrict__ part_a, int Ta,
+                                                      double* __restrict__ part_x, const double* __restrict__ b,
+                                                      double* __restrict__ part_rr) {
   __shared__ double sh[32];
   __shared__ double s_php;
   const int c = blockIdx.y, t = blockIdx.x;
   if (status[c] != 0) return;
   if (threadIdx.x < 32) {
-    const double v = sum_parts(part_a + (size_t)c * T, T);
+    const double v = sum_parts(part_a + (size_t)c * Ta, Ta);
     if (threadIdx.x == 0) s_php = v;
   }
   __syncthreads();
@@ -96,17 +97,62 @@ __global__ void __launch_bounds__(PCG_NT) k_pcg_upd_x(int n, int T, int M, const
   const double alpha = rzb[(size_t)((it - 1) & 1) * M + c] / php;
   const size_t o = (size_t)c * n;
   const int i0 = t * PCG_TILE, i1 = min(n, i0 + PCG_TILE);
-  double xbr = 0.0;
+  double xbr = 0.0, rr = 0.0;
   for (int i = i0 + threadIdx.x; i < i1; i += PCG_NT) {
     const double xi = x[o + i] + alpha * p[o + i];
     const double ri = r[o + i] - alpha * hp[o + i];
     x[o + i] = xi;
     r[o + i] = ri;
     if (b) xbr += xi * (b[o + i] + ri);
+    rr += ri * ri;
   }
   if (b) {
     xbr = block_sum<PCG_NT>(xbr, sh);
     if (threadIdx.x == 0) part_x[(size_t)c * T + t] = xbr;
+  }
+  if (part_rr) {
+    rr = block_sum<PCG_NT>(rr, sh);
+    if (threadIdx.x == 0) part_rr[(size_t)c * T + t] = rr;
+  }
+}
+
+// Fused LMP/beta step (single-pass P = I + S diag(coef) S^T): with W = S^T r,
+//   rz_new = r.(r + S(coef o W)) = |r|^2 + sum_i coef_i W_i^2  (exact identity),
+// recorded and tested here; beta = rz_new / rz_old goes to the p update that
+// the LMP GEMM epilogue performs (p = r + beta p + S (coef o W)).
+__global__ void __launch_bounds__(128) k_pcg_rz(int T, int M, int k, const double* __restrict__ W,
+                                                const double* __restrict__ coef, const double* __restrict__ part_rr,
+                                                const double* __restrict__ part_x, double* __restrict__ rzb,
+                                                double* __restrict__ beta, double rtol, double* __restrict__ hist_rz,
+                                                double* __restrict__ hist_J, int hist_ld,
+                                                int32_t* __restrict__ status, int32_t* __restrict__ iters, int it) {
+  __shared__ double sh[32];
+  const int c = blockIdx.x;
+  double q = 0.0;
+  for (int i = threadIdx.x; i < k; i += 128) {
+    const double w = W[i + (size_t)c * k];
+    q += coef[i] * (w * w);
+  }
+  q = block_sum<128>(q, sh);
+  if (threadIdx.x < 32) {
+    const double rr = sum_parts(part_rr + (size_t)c * T, T);
+    const double xbr = hist_J ? sum_parts(part_x + (size_t)c * T, T) : 0.0;
+    if (threadIdx.x == 0) {
+      if (status[c] != 0) {
+        beta[c] = 0.0;
+        return;
+      }
+      const double rz_new = rr + q;
+      const double rz_old = rzb[(size_t)((it - 1) & 1) * M + c];
+      const bool stop = rz_new <= 0.0 ||
+                        (rtol >= 0.0 && sqrt(rz_new) <= rtol * sqrt(hist_rz[(size_t)c * hist_ld]));
+      hist_rz[(size_t)c * hist_ld + it] = rz_new;
+      if (hist_J) hist_J[(size_t)c * hist_ld + it] = hist_J[(size_t)c * hist_ld] - 0.5 * xbr;
+      iters[c] = it;
+      rzb[(size_t)(it & 1) * M + c] = rz_new;
+      if (stop) status[c] = 1;
+      beta[c] = stop ? 0.0 : rz_new / rz_old;
+    }
   }
 }
 
@@ -167,8 +213,8 @@ __global__ void __launch_bounds__(PCG_NT) k_pcg_cost0(int np_obs, const double* 
   if (threadIdx.x == 0) hist_J[(size_t)c * hist_ld] = 0.5 * mm;
 }
 
-// work layout: part_a | part_x | part_m | part_r (M*T each) | rzb (2*M)
-int64_t pcg_work_doubles(int n, int M) { return 4LL * M * pcg_tiles(n) + 2LL * M; }
+// work layout: part_a | part_x | part_rr | part_r (M*T each) | rzb (2*M) | beta (M)
+int64_t pcg_work_doubles(int n, int M) { return 4LL * M * pcg_tiles(n) + 3LL * M; }
 
 int launch_pcg_init(int n, int M, const double* b, const double* z, double* x, double* r, double* p, double* work,
                     double* hist_rz, int hist_ld, int32_t* status, int32_t* iters, cudaStream_t st) {
@@ -179,17 +225,41 @@ int launch_pcg_init(int n, int M, const double* b, const double* z, double* x, d
 }
 
 int launch_pcg_alpha(int n, int M, const double* p, const double* hp, double* x, double* r, double* work,
-                     int32_t* status, int32_t* iters, int it, const double* b, cudaStream_t st) {
+                     int32_t* status, int32_t* iters, int it, const double* b, const double* php_part,
+                     int php_tiles, cudaStream_t st) {
   const int T = pcg_tiles(n);
   double* part_a = work;
   double* part_x = work + (size_t)M * T;
+  double* part_rr = work + 2 * (size_t)M * T;
   double* rzb = work + 4 * (size_t)M * T;
   dim3 grid(T, M);
-  k_dot_partial<<<grid, PCG_NT, 0, st>>>(n, T, p, hp, part_a);
-  k_pcg_upd_x<<<grid, PCG_NT, 0, st>>>(n, T, M, p, hp, x, r, rzb, status, iters, it, part_a, part_x, b);
-  count_launch(2);
+  if (!php_part) {
+    k_dot_partial<<<grid, PCG_NT, 0, st>>>(n, T, p, hp, part_a);
+    count_launch();
+    php_part = part_a;
+    php_tiles = T;
+  }
+  k_pcg_upd_x<<<grid, PCG_NT, 0, st>>>(n, T, M, p, hp, x, r, rzb, status, iters, it, php_part, php_tiles, part_x, b,
+                                       part_rr);
+  count_launch();
   return check_launch("k_pcg_upd_x");
 }
+
+int launch_pcg_rz(int n, int M, int k, const double* W, const double* coef, double* work, double rtol,
+                  double* hist_rz, double* hist_J, int hist_ld, int32_t* status, int32_t* iters, int it,
+                  cudaStream_t st) {
+  const int T = pcg_tiles(n);
+  double* part_x = work + (size_t)M * T;
+  double* part_rr = work + 2 * (size_t)M * T;
+  double* rzb = work + 4 * (size_t)M * T;
+  double* beta = rzb + 2 * (size_t)M;
+  k_pcg_rz<<<M, 128, 0, st>>>(T, M, k, W, coef, part_rr, part_x, rzb, beta, rtol, hist_rz, hist_J, hist_ld, status,
+                              iters, it);
+  count_launch();
+  return check_launch("k_pcg_rz");
+}
+
+double* pcg_beta_ptr(int n, int M, double* work) { return work + 4 * (size_t)M * pcg_tiles(n) + 2 * (size_t)M; }
 
 int launch_pcg_beta(int n, int M, const double* z, const double* r, double* p, double* work, double rtol,
                     double* hist_rz, double* hist_J, int hist_ld, int32_t* status, int32_t* iters, int it,

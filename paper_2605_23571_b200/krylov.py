@@ -9,10 +9,16 @@ count, the same stop rules and the same RuntimeError messages.
 PCG recurrence (no coupling, krylov.py:49-97 per member) but each step is
 one launch over all members:
 
-    Hp      edak_hessian_block   (member j's own trajectory, I + A fused)
-    alpha   edak_pcg_alpha       (p.Hp, breakdown flag, x/r update, cost)
-    z = Pr  edak_lmp_apply       (DMMA GEMMs over the whole residual block)
-    beta    edak_pcg_beta        (r.z, stop test, p update)
+    Hp      edak_hessian_block   (member j's own trajectory, I + A fused,
+                                  p.Hp tile partials in the last U_B pass)
+    alpha   edak_pcg_alpha       (breakdown flag, x/r update, cost, |r|^2)
+    beta    edak_pcg_lmp_beta    (W = S^T r; r.Pr = |r|^2 + W^T diag(c) W;
+                                  stop test; p = r + beta p + S(c o W) in
+                                  the DMMA GEMM epilogue -- z = P r is
+                                  never materialised)
+
+With a two-pass (non-orthonormal S) or user preconditioner the beta step is
+z = P r (edak_lmp_apply / callable) then edak_pcg_beta (r.z, stop, p).
 
 All reductions are fixed-order (deterministic).  The cost trace uses the J
 identity J(x) = 1/2 x.(I+A)x - b.x + 1/2 d.R^-1 d (test_assim.py:52-63) with
@@ -85,11 +91,14 @@ def _traces(status, iters, hist_rz, hist_J, trace_cost):
     return out
 
 
-def pcg_device(apply_h, B, cfg, apply_p=None, cost=None, check_every=8, snapshots=None):
+def pcg_device(apply_h, B, cfg, apply_p=None, cost=None, check_every=8, snapshots=None,
+               dot_tiles=0, lmp=None):
     """Batched PCG on a (M, n) device block of right-hand sides.
 
-    apply_h(P, out, gp) writes (I + A) P into ``out`` (``gp`` is unused and
-    passed as None).
+    apply_h(P, out, dotp) writes (I + A) P into ``out``; when ``dot_tiles``
+    > 0 it also writes the (M, dot_tiles) tile partials of P.out into
+    ``dotp`` (else dotp is None).  ``lmp`` = (S, coef) of a single-pass LMP
+    selects the fused beta step (then ``apply_p`` is only used for z0).
     apply_p(R) -> P R (None = identity).  cost: None, ("recurrence", D,
     sigma2) with innovations D (M, p), or ("exact", fn) with fn(X) -> (M,)
     J values.  ``snapshots`` (a list) receives device copies of
@@ -112,7 +121,6 @@ def pcg_device(apply_h, B, cfg, apply_p=None, cost=None, check_every=8, snapshot
     _lib.call("edak_pcg_init", n, M, B.data_ptr(), Z0.data_ptr(), X.data_ptr(), Rr.data_ptr(),
               P.data_ptr(), work.data_ptr(), hist_rz.data_ptr(), L, status.data_ptr(),
               iters.data_ptr(), s)
-    rzb = work[-2 * M:]
     trace_cost = bool(cfg.trace_cost and cost is not None)
     rec = trace_cost and cost[0] == "recurrence"
     if rec:
@@ -121,22 +129,35 @@ def pcg_device(apply_h, B, cfg, apply_p=None, cost=None, check_every=8, snapshot
     elif trace_cost:
         hist_J[:, 0] = cost[1](X)
     rtol = -1.0 if cfg.residual_rtol is None else float(cfg.residual_rtol)
+    rzb = work[-3 * M:-M]
+    dotp = (torch.empty((M, dot_tiles), dtype=torch.float64, device=dev) if dot_tiles > 0
+            else None)
+    if lmp is not None:
+        S, coef = lmp
+        lmpwork = torch.empty(int(_lib.lib().edak_lmp_work_doubles(n, S.shape[0], M)),
+                              dtype=torch.float64, device=dev)
     if snapshots is not None:
         snapshots.append((0, X.clone(), Rr.clone(), P.clone(), rzb[:M].clone()))
     for it in range(1, cfg.max_iters + 1):
-        apply_h(P, HP, None)
+        apply_h(P, HP, dotp)
         _lib.call("edak_pcg_alpha", n, M, P.data_ptr(), HP.data_ptr(), X.data_ptr(),
                   Rr.data_ptr(), work.data_ptr(), status.data_ptr(), iters.data_ptr(), it,
-                  B.data_ptr() if rec else None, s)
+                  B.data_ptr() if rec else None, _lib.ptr(dotp), dot_tiles, s)
         if not rec:
             if trace_cost:
                 run = status == 0
                 hist_J[:, it] = torch.where(run, cost[1](X), hist_J[:, it])
-        Zr = apply_p(Rr) if apply_p is not None else Rr
-        _lib.call("edak_pcg_beta", n, M, Zr.data_ptr(), Rr.data_ptr(), P.data_ptr(),
-                  work.data_ptr(), rtol, hist_rz.data_ptr(),
-                  hist_J.data_ptr() if rec else None, L, status.data_ptr(), iters.data_ptr(),
-                  it, s)
+        if lmp is not None:
+            _lib.call("edak_pcg_lmp_beta", n, S.shape[0], M, S.data_ptr(), coef.data_ptr(),
+                      Rr.data_ptr(), P.data_ptr(), work.data_ptr(), lmpwork.data_ptr(), rtol,
+                      hist_rz.data_ptr(), hist_J.data_ptr() if rec else None, L,
+                      status.data_ptr(), iters.data_ptr(), it, s)
+        else:
+            Zr = apply_p(Rr) if apply_p is not None else Rr
+            _lib.call("edak_pcg_beta", n, M, Zr.data_ptr(), Rr.data_ptr(), P.data_ptr(),
+                      work.data_ptr(), rtol, hist_rz.data_ptr(),
+                      hist_J.data_ptr() if rec else None, L, status.data_ptr(),
+                      iters.data_ptr(), it, s)
         if snapshots is not None:
             snapshots.append((it, X.clone(), Rr.clone(), P.clone(),
                               rzb[(it & 1) * M:(it & 1) * M + M].clone()))
@@ -170,9 +191,9 @@ def pcg(apply_h, b, cfg, precond=None, cost_fn=None):
     if prob is not None:
         work = prob.lin.work(1)
 
-        def apply_h_cols(P, out, gp):
+        def apply_h_cols(P, out, dotp):
             prob.n_matvecs += 1
-            prob.lin.hessian_cols(P, None, 1.0, gp, out, work)
+            prob.lin.hessian_cols(P, None, 1.0, None, out, work, dotp)
     else:
         def apply_h_cols(P, out, gp):
             y = np.asarray(apply_h(P[0].cpu().numpy()), dtype=float)
@@ -196,27 +217,31 @@ def pcg(apply_h, b, cfg, precond=None, cost_fn=None):
         else:
             cost = ("exact", lambda X: torch.tensor([float(cost_fn(X[0].cpu().numpy()))],
                                                     dtype=torch.float64, device=X.device))
-    X, traces = pcg_device(apply_h_cols, Bc, cfg, apply_p, cost)
+    X, traces = pcg_device(apply_h_cols, Bc, cfg, apply_p, cost,
+                           dot_tiles=prob.lin.dot_tiles() if prob is not None else 0)
     x = X[0].cpu().numpy() if b_np else X[0]
     return x, traces[0]
 
 
-def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None):
+def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fused=True):
     """Batched PCG over all members of an ``Ensemble``: B (M, n) device
     right-hand sides (e.g. ens.rhs_all()).  cost: "recurrence", "exact" or
-    None.  Returns (X (M, n), [SolveTrace] * M)."""
+    None.  ``fused`` folds p.Hp into the Hessian's last pass and a
+    single-pass LMP into the beta step.  Returns (X (M, n), [SolveTrace] * M)."""
     work = ens.lin.work(ens.M)
 
-    def apply_h_cols(P, out, gp):
-        ens.a_apply_members(P, ident=1.0, obs_out=gp, out=out, work=work)
+    def apply_h_cols(P, out, dotp):
+        ens.a_apply_members(P, ident=1.0, out=out, work=work, dot_part=dotp)
 
     apply_p = precond.apply_cols if precond is not None else None
+    lmp = precond.single_pass() if (fused and precond is not None) else None
     c = None
     if cfg.trace_cost and cost == "recurrence":
         c = ("recurrence", ens.D, ens.lin.sigma2)
     elif cfg.trace_cost and cost == "exact":
         c = ("exact", ens.cost_members)
-    return pcg_device(apply_h_cols, B, cfg, apply_p, c, snapshots=snapshots)
+    return pcg_device(apply_h_cols, B, cfg, apply_p, c, snapshots=snapshots,
+                      dot_tiles=ens.lin.dot_tiles() if fused else 0, lmp=lmp)
 
 
 # ----------------------------------------------------------------- Lanczos --

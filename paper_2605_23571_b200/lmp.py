@@ -81,12 +81,26 @@ class SpectralLmp:
             self.fused = bool((g - eye).abs().max() <= ORTHO_TOL)
         self._ready = True
 
+    def single_pass(self):
+        """(S (k, n), c = theta/(lam+1) - 1) when P is applied in one pass
+        (S orthonormal), else None.  Batched PCG then folds P into its beta
+        step (edak_pcg_lmp_beta) instead of materialising z = P r."""
+        self._prepare()
+        return (self._S, self._c_full) if self.fused else None
+
+    def work_cols(self, ncols, device):
+        key = (ncols, str(device))
+        if getattr(self, "_work_key", None) != key:
+            self._work = torch.empty(int(_lib.lib().edak_lmp_work_doubles(self.n, self.k, ncols)),
+                                     dtype=torch.float64, device=device)
+            self._work_key = key
+        return self._work
+
     def _project_cols(self, coef, R, out=None):
         n, ncols = R.shape[1], R.shape[0]
         R = R.contiguous()
         out = torch.empty_like(R) if out is None else out
-        work = torch.empty(int(_lib.lib().edak_lmp_work_doubles(n, self.k, ncols)),
-                           dtype=torch.float64, device=R.device)
+        work = self.work_cols(ncols, R.device)
         _lib.call("edak_lmp_apply", n, self.k, ncols, self._S.data_ptr(), coef.data_ptr(),
                   R.data_ptr(), out.data_ptr(), work.data_ptr(), _lib.stream())
         return out

@@ -283,3 +283,32 @@ def test_lanczos_gpu(gpu):
     d = np.linspace(1.0, 30.0, 30)
     v, b = lanczos_eigs(lambda x: d * x, 30, 30, 5, seed=3)
     npt.assert_allclose(v, d[::-1][:5], rtol=1e-10)
+
+
+def test_pcg_fused_lmp_beta_matches_two_step(gpu, ref_problem):
+    """Fused beta step (r.Pr = |r|^2 + W^T diag(c) W, p = r + beta p +
+    S(c o W) in the GEMM epilogue, p.Hp from the Hessian's last pass) vs
+    the unfused z = P r / r.z / p-update path and the cfg1 golden traces."""
+    from paper_2605_23571_b200.assim import Ensemble
+    from paper_2605_23571_b200.krylov import SolverConfig, pcg_members
+    from paper_2605_23571_b200.lmp import make_lmp
+    from paper_2605_23571_b200.nystrom import NystromConfig, nystrom_evd
+    from oracle.twin import BASELINE_CONFIGS, baseline_setup
+    g = ref_problem
+    st = baseline_setup(BASELINE_CONFIGS[1])
+    ctl = _gpu_problem(st.control)
+    approx = nystrom_evd(ctl.a_apply, g["cfg1_gamma"], NystromConfig(10, 10, shift_mode="trace"))
+    lmp = make_lmp(approx, "halfsum")
+    assert lmp.single_pass() is not None
+    mems = [_gpu_problem(m) for m in st.members]
+    ens = Ensemble.from_members(mems)
+    cfg = SolverConfig(max_iters=30)
+    Xf, trf = pcg_members(ens, ens.rhs_all(), cfg, precond=lmp, fused=True)
+    Xu, tru = pcg_members(ens, ens.rhs_all(), cfg, precond=lmp, fused=False)
+    npt.assert_allclose(Xf.cpu().numpy(), Xu.cpu().numpy(), rtol=0, atol=1e-10 * float(Xu.abs().max()))
+    for j in range(len(mems)):
+        npt.assert_allclose(trf[j].cost, tru[j].cost, rtol=1e-11)
+        r0 = tru[j].resnorm[0]  # same bar as the cfg1 golden resnorm check
+        assert np.max(np.abs(np.array(trf[j].resnorm) - tru[j].resnorm)) <= 1e-10 * r0
+    for j in (0, 4, 9):
+        npt.assert_allclose(trf[j].cost, g[f"cfg1_m{j}_cost"], rtol=1e-10)
