@@ -14,6 +14,7 @@
 #include <cstdlib>
 
 #include "sweep.cuh"
+#include <type_traits>
 
 namespace edak {
 
@@ -108,7 +109,7 @@ __device__ __forceinline__ void tl_sub(const double (&u)[C + 4], const double (&
     a[j] = l96_tl(u[j + 3], u[j], u[j + 1], u[j + 2], x[j + 3], x[j], x[j + 1]);
 }
 
-template <int C, int NT, bool STREAM, int MINB = 1>
+template <int C, int NT, bool STREAM, int MINB = 1, bool PAIR = false>
 __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* __restrict__ vin,
                                            double* __restrict__ obs, const int32_t* __restrict__ col_traj,
                                            SweepGeom geo, int s0, int s1, double* __restrict__ vout) {
@@ -152,11 +153,11 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
   // software pipeline: the state of step s+1 is staged (cp.async, coalesced)
   // into the other shared buffer while step s runs; STREAM reads stored
   // stages straight from memory
-  using SS = Stage<C, NT>;
+  using SS = std::conditional_t<PAIR, Stage2<C, NT>, Stage<C, NT>>;
   double* XB0 = dsm_ + sizeof(XBuf<NT>) / sizeof(double);
   double* XB1 = XB0 + SS::PLEN;
   const int used = R.nact * C;
-  const int gst = wrap(R.base - 2 + (int)threadIdx.x, n);
+  const int gst = PAIR ? R.base - 2 : wrap(R.base - 2 + (int)threadIdx.x, n);
   const size_t sstride = STREAM ? (size_t)4 * n : (size_t)n;
   if (!STREAM) SS::stage((s0 & 1) ? XB1 : XB0, tr + (size_t)s0 * n, gst, n, used);
 #pragma unroll 1
@@ -250,7 +251,7 @@ __device__ __forceinline__ void ad_sub(const double (&w)[C + 4], const double (&
     u[j] = l96_ad(x[j], x[j + 1], x[j + 3], x[j + 4], w[j + 1], w[j + 2], w[j + 3], w[j + 4]);
 }
 
-template <int C, int NT, bool STREAM, int MINB = 1>
+template <int C, int NT, bool STREAM, int MINB = 1, bool PAIR = false>
 __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* __restrict__ forcing,
                                            double* __restrict__ gout, const int32_t* __restrict__ col_traj,
                                            SweepGeom geo, int s0, int s1, const double* __restrict__ gin) {
@@ -301,11 +302,11 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
     add_force(N, g);
   }
 
-  using SS = Stage<C, NT>;
+  using SS = std::conditional_t<PAIR, Stage2<C, NT>, Stage<C, NT>>;
   double* XB0 = dsm_ + sizeof(XBuf<NT>) / sizeof(double);
   double* XB1 = XB0 + SS::PLEN;
   const int used = R.nact * C;
-  const int gst = wrap(R.base - 2 + (int)threadIdx.x, n);
+  const int gst = PAIR ? R.base - 2 : wrap(R.base - 2 + (int)threadIdx.x, n);
   const size_t sstride = STREAM ? (size_t)4 * n : (size_t)n;
   if (!STREAM) {
     SS::stage(((s1 - 1) & 1) ? XB1 : XB0, tr + (size_t)(s1 - 1) * n, gst, n, used);
@@ -384,7 +385,8 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
 // opt a kernel into > 48 KB of dynamic shared memory (idempotent)
 template <int NT, int C = 0, typename K, typename... Args>
 static void go(K kernel, dim3 grid, cudaStream_t st, Args... args) {
-  const size_t bytes = sizeof(XBuf<NT>) + (C ? 2 * Stage<C ? C : 1, NT>::PLEN * sizeof(double) : 0);
+  const size_t bytes =
+      sizeof(XBuf<NT>) + (C ? 2 * (size_t)Stage2<C ? (C + 1) / 2 * 2 : 2, NT>::PLEN * sizeof(double) : 0);
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   kernel<<<grid, NT, bytes, st>>>(args...);
 }
@@ -426,7 +428,8 @@ static bool plan(int n, int hl_total, int hr_total, int& C, int& NT, SweepGeom& 
   const int W = range - hl_total - hr_total;
   if (W < 64) return false;
   ntiles = (n + W - 1) / W;
-  geo.W = (n + ntiles - 1) / ntiles;  // balanced tiles
+  geo.W = ((n + ntiles - 1) / ntiles + 1) & ~1;  // balanced tiles, even width (W budget is even)
+  if (geo.W > W) geo.W = W;
   geo.HL = hl_total;
   geo.periodic = 0;
   geo.nact = NT;
@@ -461,6 +464,13 @@ static int plan_chunks(int N, bool periodic, const double* work2) {
   if (periodic || !work2 || N <= SWEEP_CHUNK) return 1;
   if (const char* e = getenv("EDAK_SWEEP_NOCHUNK")) return 1;
   return (N + SWEEP_CHUNK - 1) / SWEEP_CHUNK;
+}
+
+// 16-byte pair staging: every row start and tile base even, rows 16-B aligned
+static bool pair_ok(const edak_problem* P, const SweepGeom& geo) {
+  if (getenv("EDAK_NO_PAIR")) return false;
+  return P->n % 2 == 0 && P->traj_stride % 2 == 0 && ((uintptr_t)P->states & 15) == 0 &&
+         (geo.periodic || (geo.W % 2 == 0 && geo.HL % 2 == 0));
 }
 
 int sweep2_mode(const edak_problem* P, int K);
@@ -529,7 +539,9 @@ v1:
     dim3 grid(nt, ncols);
     // measured best on B200: 4 resident CTAs (126 regs, no spills)
     const int mb = env_int("EDAK_TL_MINB", 4);
-    if (C == 8 && NT == 128 && !stream && mb == 3) {
+    if (C == 8 && NT == 128 && !stream && mb == 4 && pair_ok(P, geo)) {
+      go<128, 8>(k_tl<8, 128, false, 4, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
+    } else if (C == 8 && NT == 128 && !stream && mb == 3) {
       go<128, 8>(k_tl<8, 128, false, 3>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
     } else if (C == 8 && NT == 128 && !stream && mb == 4) {
       go<128, 8>(k_tl<8, 128, false, 4>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
@@ -600,7 +612,9 @@ v1:
     dim3 grid(nt, ncols);
     // measured best on B200: 3 resident CTAs (168 regs, no spills)
     const int mb = env_int("EDAK_AD_MINB", 3);
-    if (C == 8 && NT == 128 && !stream && mb == 3) {
+    if (C == 8 && NT == 128 && !stream && mb == 3 && pair_ok(P, geo)) {
+      go<128, 8>(k_ad<8, 128, false, 3, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1, gin);
+    } else if (C == 8 && NT == 128 && !stream && mb == 3) {
       go<128, 8>(k_ad<8, 128, false, 3>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1, gin);
     } else if (C == 8 && NT == 128 && !stream && mb == 2) {
       go<128, 8>(k_ad<8, 128, false, 2>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1, gin);

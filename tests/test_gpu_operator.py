@@ -210,3 +210,22 @@ def test_hybrid_equals_recompute(gpu):
         assert torch.equal(a.hessian_cols(z), b.hessian_cols(z))
         d = torch.randn(3, op.net.p, dtype=torch.float64, device="cuda")
         assert torch.equal(a.rhs_cols(d), b.rhs_cols(d))
+
+
+def test_pair_staging_equals_generic(gpu, monkeypatch):
+    """16-byte pair staging (even n, sweep.cuh Stage2) and the generic 8-byte
+    staging give the same bits: tile mode with wrapping edge tiles
+    (n=16384, 2 chunks) and periodic mode (n=1024)."""
+    from paper_2605_23571_b200.assim import Linearization
+    from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
+    for n, N, L in [(16384, 16, 16.0), (1024, 12, 8.0), (6002, 9, 8.0)]:
+        op = _oracle_problem(n, N, 4, 3, L, 11)
+        ub = CirculantFactor(n, op.ub.symbol)
+        a = Linearization(op.traj.states[None], 0.025, 8.0, op.net, ub, DiagonalNoise(1.0))
+        z = torch.randn(3, n, dtype=torch.float64, device="cuda")
+        d = torch.randn(3, op.net.p, dtype=torch.float64, device="cuda")
+        hz, rd = a.hessian_cols(z), a.rhs_cols(d)
+        monkeypatch.setenv("EDAK_NO_PAIR", "1")
+        assert torch.equal(hz, a.hessian_cols(z))
+        assert torch.equal(rd, a.rhs_cols(d))
+        monkeypatch.delenv("EDAK_NO_PAIR")
