@@ -290,6 +290,26 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
     for (int j = 0; j < C; ++j)
       if (gp[j] >= 0) gg[j + 2] += __ldg(f + gp[j]) * inv_s2;
   };
+  // PAIR path: the forcing of level s is fetched by cp.async into per-thread
+  // smem slots at the start of step s (with the next state tile) and added at
+  // its end, so its global latency hides behind the step instead of stalling
+  // every warp of the CTA at once (long_scoreboard in the ncu profile)
+  double* FS = dsm_ + sizeof(XBuf<NT>) / sizeof(double) + 2 * Stage2<C, NT>::PLEN;
+  auto fetch_force = [&](int tp, int sbuf) {
+    if (tp < 0) return;
+    const double* f = fc + (size_t)tp * G;
+    double* d = FS + (size_t)sbuf * C * NT + threadIdx.x;
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+      if (gp[j] >= 0) cp_async8(d + j * NT, f + gp[j]);
+  };
+  auto add_fetched = [&](int tp, int sbuf, double (&gg)[C + 4]) {
+    if (tp < 0) return;
+    const double* d = FS + (size_t)sbuf * C * NT + threadIdx.x;
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+      if (gp[j] >= 0) gg[j + 2] += d[j * NT] * inv_s2;
+  };
 
   // window chunk [s0, s1), swept backward: g enters at level s1 (w_all[N]
   // when s1 == N, model.py:154) and leaves at level s0
@@ -308,7 +328,9 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
   const int used = R.nact * C;
   const int gst = PAIR ? R.base - 2 : wrap(R.base - 2 + (int)threadIdx.x, n);
   const size_t sstride = STREAM ? (size_t)4 * n : (size_t)n;
+  int tp_cur = PAIR ? __ldg(P.tpos + s1 - 1) : -1;
   if (!STREAM) {
+    if (PAIR) fetch_force(tp_cur, (s1 - 1) & 1);
     SS::stage(((s1 - 1) & 1) ? XB1 : XB0, tr + (size_t)(s1 - 1) * n, gst, n, used);
     cp_wait_all();
     __syncthreads();
@@ -316,6 +338,7 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
 #pragma unroll 1
   for (int s = s1 - 1; s >= s0; --s) {
     const double* Xs = tr + (size_t)s * sstride;
+    const int tp_next = (PAIR && s > s0) ? __ldg(P.tpos + s - 1) : -1;
     double X[C + 4], x2[C + 4], x3[C + 4], x4[C + 4];
     if (STREAM) R.load_halo(Xs, X);
     else SS::win((s & 1) ? XB1 : XB0, R.t, X);  // staged, published by the last barrier
@@ -329,7 +352,10 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
       for (int j = 0; j < C; ++j) x2[j + 2] = axpy_rn(X[j + 2], h, l96_f(X[j + 3], X[j], X[j + 1], X[j + 2], F));
       xchg2(R, xb, buf, x2, g);
       // X_{s-1} goes to the buffer X_{s+1} used: every thread read it last step
-      if (s > s0) SS::stage(((s - 1) & 1) ? XB1 : XB0, Xs - n, gst, n, used);
+      if (s > s0) {
+        if (PAIR) fetch_force(tp_next, (s - 1) & 1);  // same commit group as X_{s-1}
+        SS::stage(((s - 1) & 1) ? XB1 : XB0, Xs - n, gst, n, used);
+      }
 #pragma unroll
       for (int j = 0; j < C; ++j)
         x3[j + 2] = axpy_rn(X[j + 2], h, l96_f(x2[j + 3], x2[j], x2[j + 1], x2[j + 2], F));
@@ -368,7 +394,12 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
     ad_sub<C>(a, X, u);
 #pragma unroll
     for (int j = 0; j < C; ++j) g[j + 2] = vh[j] + u[j];
-    add_force(s, g);
+    if (PAIR) {
+      add_fetched(tp_cur, s & 1, g);
+      tp_cur = tp_next;
+    } else {
+      add_force(s, g);
+    }
   }
   if (R.t < R.nact) {
     double* go = gout + (size_t)col * n;
@@ -383,10 +414,11 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
 // ------------------------------------------------------------ launchers --
 
 // opt a kernel into > 48 KB of dynamic shared memory (idempotent)
-template <int NT, int C = 0, typename K, typename... Args>
+template <int NT, int C = 0, int EXTRA = 0, typename K, typename... Args>
 static void go(K kernel, dim3 grid, cudaStream_t st, Args... args) {
-  const size_t bytes =
-      sizeof(XBuf<NT>) + (C ? 2 * (size_t)Stage2<C ? (C + 1) / 2 * 2 : 2, NT>::PLEN * sizeof(double) : 0);
+  const size_t bytes = sizeof(XBuf<NT>) +
+                       (C ? 2 * (size_t)Stage2<C ? (C + 1) / 2 * 2 : 2, NT>::PLEN * sizeof(double) : 0) +
+                       (size_t)EXTRA * sizeof(double);
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   kernel<<<grid, NT, bytes, st>>>(args...);
 }
@@ -613,7 +645,8 @@ v1:
     // measured best on B200: 3 resident CTAs (168 regs, no spills)
     const int mb = env_int("EDAK_AD_MINB", 3);
     if (C == 8 && NT == 128 && !stream && mb == 3 && pair_ok(P, geo)) {
-      go<128, 8>(k_ad<8, 128, false, 3, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1, gin);
+      go<128, 8, 2 * 8 * 128>(k_ad<8, 128, false, 3, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1,
+                              gin);
     } else if (C == 8 && NT == 128 && !stream && mb == 3) {
       go<128, 8>(k_ad<8, 128, false, 3>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1, gin);
     } else if (C == 8 && NT == 128 && !stream && mb == 2) {
