@@ -27,6 +27,42 @@ def gaussian_sketch(n, ell, rng):
     return SketchMatrix(rng.standard_normal((n, ell)), "gaussian", 0)
 
 
+def power_sketch(prob, ell, rng):
+    """sketch.py:48-51: A times a Gaussian test matrix (one build matvec)."""
+    return SketchMatrix(prob.a_apply(rng.standard_normal((prob.n, ell))), "power", 1)
+
+
+def bcov_sketch(ub, ell, rng):
+    """sketch.py:54-57."""
+    return SketchMatrix(ub.apply(ub.apply_t(rng.standard_normal((ub.n, ell)))), "bcov", 0)
+
+
+def bfactor_sketch(ub, ell, rng):
+    """sketch.py:60-63."""
+    return SketchMatrix(ub.apply_t(rng.standard_normal((ub.n, ell))), "bfactor", 0)
+
+
+KINDS = ("gaussian", "power", "bcov", "bfactor", "rhsdiff")
+
+
+def make_sketch(kind, setup, ell, rng):
+    """sketch.py:77-97."""
+    if kind == "gaussian":
+        return gaussian_sketch(setup.cfg.n, ell, rng)
+    if kind == "power":
+        return power_sketch(setup.control, ell, rng)
+    if kind == "bcov":
+        return bcov_sketch(setup.ub, ell, rng)
+    if kind == "bfactor":
+        return bfactor_sketch(setup.ub, ell, rng)
+    if kind == "rhsdiff":
+        if ell != len(setup.members):
+            raise ValueError(f"rhsdiff sketch width is the ensemble size "
+                             f"({len(setup.members)}), got ell={ell}")
+        return rhs_diff_sketch(setup.control, setup.members)
+    raise ValueError(f"unknown sketch kind {kind!r}; expected one of {KINDS}")
+
+
 def rhs_diff_sketch(control, members):
     """Gamma_j = b_j - b_0, free in matvecs (sketch.py:66-74)."""
     b0 = control.rhs()

@@ -200,7 +200,35 @@ class MemberProblem:
         self.lin = Linearization(np.asarray(traj.states)[None], traj.dt, traj.forcing, net,
                                  ub, rn, None if stages is None else np.asarray(stages)[None],
                                  stage_mode)
+        self._index = None
         self._d = _dev.f64(self.innovation)[None]
+
+    @classmethod
+    def view(cls, lin, index, innovation, traj=None):
+        """A member on trajectory ``index`` of a shared device Linearization
+        (no host trajectory upload; eda.build_setup).  ``innovation`` may be
+        a device row; ``traj`` is the reference-style Trajectory (lazy)."""
+        self = cls.__new__(cls)
+        self.lin = lin
+        self.net, self.ub, self.rn = lin.net, lin.ub, lin.rn
+        self.traj = traj
+        self._index = int(index)
+        self._d = torch.as_tensor(innovation, dtype=torch.float64).to(lin.states.device)
+        self._d = self._d.reshape(1, -1).contiguous()
+        self._innov = None
+        self.n_matvecs = 0
+        return self
+
+    def __getattr__(self, name):  # lazy host copy for device views
+        if name == "innovation":
+            self.innovation = self._d[0].cpu().numpy()
+            return self.innovation
+        raise AttributeError(name)
+
+    def _ct(self, ncols):
+        if self._index is None:
+            return None
+        return torch.full((ncols,), self._index, dtype=torch.int32, device=self.lin.states.device)
 
     @property
     def n(self):
@@ -213,28 +241,34 @@ class MemberProblem:
     def a_apply_cols(self, Z):
         """A on a (ncols, n) device block (no host copies); counts one matvec."""
         self.n_matvecs += 1
-        return self.lin.hessian_cols(Z)
+        return self.lin.hessian_cols(Z, self._ct(Z.shape[0]))
 
     def a_apply(self, z):
         """A z for (n,) or (n, l); one call = one matvec (assim.py:55-64)."""
         self.n_matvecs += 1
         cols, vec, as_np = _dev.to_cols(z, self.n)
-        return _dev.from_cols(self.lin.hessian_cols(cols), vec, as_np)
+        return _dev.from_cols(self.lin.hessian_cols(cols, self._ct(cols.shape[0])), vec, as_np)
 
     def hessian_apply(self, z):
         """(I + A) z (assim.py:70-72), the identity fused into the last U_B."""
         self.n_matvecs += 1
         cols, vec, as_np = _dev.to_cols(z, self.n)
-        return _dev.from_cols(self.lin.hessian_cols(cols, ident=1.0), vec, as_np)
+        return _dev.from_cols(self.lin.hessian_cols(cols, self._ct(cols.shape[0]), ident=1.0),
+                              vec, as_np)
+
+    def hessian_cols(self, Z, ident=1.0, out=None, work=None, dot_part=None):
+        """(ident I + A) on a (ncols, n) device block (PCG drop-in path)."""
+        return self.lin.hessian_cols(Z, self._ct(Z.shape[0]), ident, None, out, work, dot_part)
 
     def rhs(self):
         """b = U_B^T G^T R^-1 d (assim.py:74-77)."""
-        return self.lin.rhs_cols(self._d)[0].cpu().numpy()
+        return self.lin.rhs_cols(self._d, self._ct(1))[0].cpu().numpy()
 
     def quadratic_cost(self, z):
         """J(z), a TL sweep, not counted as a matvec (assim.py:79-82)."""
         cols, _, _ = _dev.to_cols(z, self.n)
-        return float(self.lin.cost_cols(cols, self._d)[0])
+        D = self._d.expand(cols.shape[0], -1)
+        return float(self.lin.cost_cols(cols, D, self._ct(cols.shape[0]))[0])
 
     def reset_matvecs(self):
         self.n_matvecs = 0
@@ -276,6 +310,9 @@ class TrajectoryOperator:
         return _dev.from_cols(self.lin.hessian_cols(cols, self._ct(cols.shape[0]), 1.0),
                               vec, as_np)
 
+    def hessian_cols(self, Z, ident=1.0, out=None, work=None, dot_part=None):
+        return self.lin.hessian_cols(Z, self._ct(Z.shape[0]), ident, None, out, work, dot_part)
+
 
 class Ensemble:
     """A batch of members sharing (n, N, dt, F, net, U_B, R).
@@ -301,8 +338,15 @@ class Ensemble:
 
     @classmethod
     def from_members(cls, members, stage_mode="auto"):
-        """Stack reference-style MemberProblems (identical net/ub/rn/dt)."""
+        """Stack reference-style MemberProblems (identical net/ub/rn/dt).
+        Views of one device Linearization (eda.build_setup) are batched
+        without touching the host."""
         m0 = members[0]
+        lin0 = getattr(m0, "lin", None)
+        if lin0 is not None and all(getattr(m, "lin", None) is lin0 and
+                                    getattr(m, "_index", None) is not None for m in members):
+            D = torch.cat([m._d for m in members], 0)
+            return cls(lin0, D, [m._index for m in members])
         trajs, index, traj_of = [], {}, []
         for m in members:
             key = id(m.traj)

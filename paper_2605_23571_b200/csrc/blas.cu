@@ -109,7 +109,15 @@ __global__ void k_reduce_parts(const double* __restrict__ part, int nsplit, int 
   const int64_t tot = (int64_t)m * nb;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int z = 0; z < nsplit; ++z) s += part[(size_t)z * tot + e];  // fixed order
+    int z = 0;
+    for (; z + 8 <= nsplit; z += 8) {  // 8 loads in flight, same summation order
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = part[(size_t)(z + q) * tot + e];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += v[q];
+    }
+    for (; z < nsplit; ++z) s += part[(size_t)z * tot + e];  // fixed order
     const int a = (int)(e % m), b = (int)(e / m);
     C[a + (size_t)b * ldc] = s;
   }
@@ -132,7 +140,7 @@ int64_t gemm_tn_partials(int m, int nb, int64_t K) {
   return (int64_t)tn_nsplit(m, nb, K, ks) * m * nb;
 }
 
-static constexpr size_t G_SMEM = 2 * (size_t)(G_BM + G_BN) * (G_BK + G_PAD) * sizeof(double);
+static constexpr size_t G_SMEM = (2 * (size_t)(G_BM + G_BN) * (G_BK + G_PAD) + 2 * G_BK) * sizeof(double);
 
 int launch_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int ldc, int m, int nb,
                    int64_t K, double* part, cudaStream_t st) {
@@ -154,7 +162,7 @@ int launch_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, d
 
 // ----------------------------------------------------------------- NN ----
 // sA[stage][l][i] (A is M-contiguous), sB[stage][j][l] (B is K-contiguous)
-__global__ void __launch_bounds__(256) k_gemm_nn(const double* __restrict__ A, int64_t lda,
+__global__ void __launch_bounds__(256, 3) k_gemm_nn(const double* __restrict__ A, int64_t lda,
                                                  const double* __restrict__ B, int ldb,
                                                  const double* __restrict__ bscale, const double* Cin,
                                                  int64_t ldc, double beta, double* D, int64_t ldd, int64_t M,
@@ -164,6 +172,8 @@ __global__ void __launch_bounds__(256) k_gemm_nn(const double* __restrict__ A, i
   double (*sA)[G_BK][G_BM + G_PAD] = reinterpret_cast<double (*)[G_BK][G_BM + G_PAD]>(gsm);
   double (*sB)[G_BN][G_BK + G_PAD] =
       reinterpret_cast<double (*)[G_BN][G_BK + G_PAD]>(gsm + 2 * G_BK * (G_BM + G_PAD));
+  double (*sS)[G_BK] = reinterpret_cast<double (*)[G_BK]>(gsm + 2 * G_BK * (G_BM + G_PAD) +
+                                                          2 * G_BN * (G_BK + G_PAD));
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int wi = (warp >> 2) * 32, wj = (warp & 3) * 16;
   const int64_t i0 = (int64_t)blockIdx.x * G_BM;
@@ -184,6 +194,10 @@ __global__ void __launch_bounds__(256) k_gemm_nn(const double* __restrict__ A, i
         cpa8(&sB[stg][j][l], v ? B + (l0 + l) + (int64_t)(j0 + j) * ldb : B, v);
       }
     }
+    if (bscale && t < G_BK) {
+      const bool v = l0 + t < kk;
+      cpa8(&sS[stg][t], v ? bscale + l0 + t : bscale, v);
+    }
     cpa_commit();
   };
   double acc[4][2][2];
@@ -200,14 +214,13 @@ __global__ void __launch_bounds__(256) k_gemm_nn(const double* __restrict__ A, i
       cpa_wait<0>();
     }
     __syncthreads();
-    const int stg = c & 1, l0 = c * G_BK;
+    const int stg = c & 1;
 #pragma unroll
     for (int ks = 0; ks < G_BK; ks += 4) {
       double af[4], bf[2];
 #pragma unroll
       for (int i = 0; i < 4; ++i) af[i] = sA[stg][ks + (lane & 3)][wi + i * 8 + (lane >> 2)];
-      const int l = l0 + ks + (lane & 3);
-      const double sc = (bscale && l < kk) ? __ldg(bscale + l) : 1.0;
+      const double sc = bscale ? sS[stg][ks + (lane & 3)] : 1.0;
 #pragma unroll
       for (int j = 0; j < 2; ++j) bf[j] = sc * sB[stg][wj + j * 8 + (lane >> 2)][ks + (lane & 3)];
 #pragma unroll

@@ -141,6 +141,12 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
     const int e = R.t * C + j;
     gw[j] = (R.t < R.nact && e >= wlo && e < whi) ? __ldg(P.gpos + R.gidx(j)) : -1;
   }
+  auto capture_tp = [&](int tp) {
+    if (tp < 0) return;
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+      if (gw[j] >= 0) ob[(size_t)tp * G + gw[j]] = v[j + 2];
+  };
   auto capture = [&](int level) {
     const int tp = __ldg(P.tpos + level);
     if (tp < 0) return;
@@ -163,6 +169,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
 #pragma unroll 1
   for (int s = s0; s < s1; ++s) {
     const double* Xs = tr + (size_t)s * sstride;
+    const int tp_next = __ldg(P.tpos + s + 1);  // consumed at the end of the step
     double X[C + 4];
     if (!STREAM) cp_wait_all();
     xchg1(R, xb, buf, v);  // barrier: staged X_s visible, X_{s-1}'s buffer free
@@ -230,7 +237,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
     tl_sub<C>(u4, x4, a);
 #pragma unroll
     for (int j = 0; j < C; ++j) v[j + 2] = fma(c6, acc[j] + a[j], v[j + 2]);
-    capture(s + 1);
+    capture_tp(tp_next);
   }
   if (vout && R.t < R.nact) {
     double* vo = vout + (size_t)col * n;

@@ -193,7 +193,7 @@ def pcg(apply_h, b, cfg, precond=None, cost_fn=None):
 
         def apply_h_cols(P, out, dotp):
             prob.n_matvecs += 1
-            prob.lin.hessian_cols(P, None, 1.0, None, out, work, dotp)
+            prob.hessian_cols(P, 1.0, out, work, dotp)
     else:
         def apply_h_cols(P, out, gp):
             y = np.asarray(apply_h(P[0].cpu().numpy()), dtype=float)
@@ -269,7 +269,7 @@ def lanczos_eigs(apply_h, n, m, n_eigs, seed=0):
 
         def h(v):
             prob.n_matvecs += 1
-            return prob.lin.hessian_cols(v, None, 1.0, None, None, work)
+            return prob.hessian_cols(v, 1.0, None, work)
     else:
         def h(v):
             y = np.asarray(apply_h(v[0].cpu().numpy()), dtype=float)

@@ -232,9 +232,59 @@ def extract_fixtures():
         json.dump(keep, fh, indent=1, sort_keys=True)
 
 
+def extract_harness_rows():
+    """Every row of the reference's fixture CSVs (regenerate.sh: tiny.cfg,
+    theta.cfg, ensemble.cfg at n=40), as written by the reference harness,
+    for the GPU harness CSV-contract test."""
+    out = {}
+    for name in ("eig-sensitivity", "eig-error", "control-lmp", "theta-sensitivity",
+                 "ensemble-lmp"):
+        with open(os.path.join(FIXTURES, name + ".csv"), newline="") as fh:
+            rd = csv.reader(fh)
+            header = next(rd)
+            out[name] = [row for row in rd]
+    out["header"] = header
+    with open(os.path.join(HERE, "harness_fixtures.json"), "w") as fh:
+        json.dump(out, fh, separators=(",", ":"))
+
+
+def regen_harness_rows():
+    """The same five fixture runs regenerated HERE by the unmodified
+    reference harness (its own run_experiment): pins the oracle restatement
+    bit for bit on this numpy/LAPACK, and |regen - fixture| measures the
+    machine-to-machine spread of the LAPACK-stage rows (the GPU tolerance)."""
+    from dataclasses import replace as dc_replace
+    from edasketch import harness
+    specs = {
+        "eig-sensitivity": dict(k_list=[8], kinds=["gaussian", "power", "rhsdiff"],
+                                length_grid=[2.0, 6.0], passes_grid=[4, 10], seeds=[0]),
+        "eig-error": dict(k_list=[8], kinds=["gaussian", "power", "rhsdiff"],
+                          length_grid=[2.0, 6.0], passes_grid=[4, 10], seeds=[0, 1, 2]),
+        "control-lmp": dict(k_list=[8], kinds=["gaussian", "power", "rhsdiff"],
+                            length_grid=[2.0, 6.0], passes_grid=[4, 10], seeds=[0, 1, 2]),
+        "theta-sensitivity": dict(k_list=[8, 6], seeds=[0, 1]),
+        "ensemble-lmp": dict(k_list=[8, 6], seeds=[0]),
+    }
+    out = {}
+    for name, kw in specs.items():
+        spec = harness.default_spec(name)
+        spec = dc_replace(spec, ell=10, max_iters=8, **kw)
+        spec.twin = dc_replace(spec.twin, n=40, obs_grid_count=8, members=10)
+        table = harness.run_experiment(spec)
+        out[name] = [[harness._format_value(v) for v in row] for row in table.rows]
+    with open(os.path.join(HERE, "harness_regen.json"), "w") as fh:
+        json.dump(out, fh, separators=(",", ":"))
+
+
 if __name__ == "__main__":
+    if "--harness-only" in sys.argv:
+        extract_harness_rows()
+        regen_harness_rows()
+        sys.exit(0)
     make_model_cases()
     make_problem_cases()
     extract_fixtures()
+    extract_harness_rows()
+    regen_harness_rows()
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))
