@@ -229,3 +229,43 @@ def test_pair_staging_equals_generic(gpu, monkeypatch):
         assert torch.equal(hz, a.hessian_cols(z))
         assert torch.equal(rd, a.rhs_cols(d))
         monkeypatch.delenv("EDAK_NO_PAIR")
+
+
+def test_model_obs_dropins_and_device_setup(gpu):
+    """model.tlm / adjoint / spinup, ObsNetwork.observe* and eda.build_setup
+    (device twin) against the oracle restatements of model.py / obs.py /
+    eda.py."""
+    from oracle.twin import TwinConfig as OTwin, build_setup as obuild
+    from paper_2605_23571_b200 import model as gm
+    from paper_2605_23571_b200.eda import TwinConfig, build_setup
+    from paper_2605_23571_b200.obs import ObsNetwork as GObs
+    tw = dict(n=40, obs_grid_count=8, members=4)
+    o = obuild(OTwin(**tw), trial_seed=3)
+    g = build_setup(TwinConfig(**tw), trial_seed=3)
+    # spin-up and truth are bit-exact (RK4 producer); U_B perturbations are
+    # the circulant kernel vs numpy's FFT (rounding-level differences)
+    np.testing.assert_array_equal(g.truth.states, o.truth.states)
+    np.testing.assert_allclose(g.control.traj.states, o.control.traj.states, rtol=1e-13, atol=1e-13)
+    for gm_, om_ in zip([g.control] + g.members, [o.control] + o.members):
+        np.testing.assert_allclose(gm_.innovation, om_.innovation, rtol=0, atol=1e-12)
+    traj = o.control.traj
+    rng = np.random.default_rng(5)
+    v = rng.standard_normal(40)
+    ref = ol96.tlm(traj, v)
+    got = gm.tlm(traj, v)
+    assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
+    w_all = rng.standard_normal(ref.shape)
+    ref_g = ol96.adjoint(traj, w_all)
+    assert np.linalg.norm(gm.adjoint(traj, w_all) - ref_g) <= 1e-13 * np.linalg.norm(ref_g)
+    onet = o.net
+    gnet = GObs(onet.grid, onet.times)
+    np.testing.assert_array_equal(gnet.observe(traj), onet.observe(traj))
+    np.testing.assert_array_equal(gnet.observe(g.control.traj), g.net.observe(g.control.traj))
+    r1 = onet.observe_tl(traj, v)
+    assert np.linalg.norm(gnet.observe_tlm(traj, v) - r1) <= 1e-13 * np.linalg.norm(r1)
+    w = rng.standard_normal(onet.p)
+    r2 = onet.observe_ad(traj, w)
+    assert np.linalg.norm(gnet.observe_adj(traj, w) - r2) <= 1e-13 * np.linalg.norm(r2)
+    from oracle.streams import substream as osub
+    np.testing.assert_array_equal(gm.spinup(40, 0.025, 8.0, 100, osub(1, "spinup")),
+                                  ol96.spinup(40, 0.025, 8.0, 100, osub(1, "spinup")))
