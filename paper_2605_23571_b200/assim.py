@@ -362,6 +362,10 @@ class Ensemble:
         innov = np.stack([np.asarray(m.innovation, dtype=float) for m in members])
         return cls(lin, innov, traj_of)
 
+    def subset(self, lo, hi):
+        """Members lo..hi-1 as an Ensemble on the same Linearization."""
+        return Ensemble(self.lin, self.D[lo:hi], self.traj_of[lo:hi].cpu().numpy())
+
     def rhs_all(self):
         """All members' right-hand sides, (M, n) device block (one launch)."""
         return self.lin.rhs_cols(self.D, self.traj_of)

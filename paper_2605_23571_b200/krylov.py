@@ -91,6 +91,88 @@ def _traces(status, iters, hist_rz, hist_J, trace_cost):
     return out
 
 
+class _PcgRun:
+    """State and per-iteration launches of one batched PCG (pcg_device).
+    Split out so that several independent member groups can be stepped in
+    lockstep on their own CUDA streams (pcg_members ``groups``)."""
+
+    def __init__(self, apply_h, B, cfg, apply_p=None, cost=None, dot_tiles=0, lmp=None,
+                 Z0=None):
+        self.apply_h, self.apply_p, self.cfg = apply_h, apply_p, cfg
+        B = B.contiguous()
+        self.B = B
+        M, n = B.shape
+        self.M, self.n = M, n
+        dev = B.device
+        self.L = L = cfg.max_iters + 1
+        self.X, self.R, self.P = torch.empty_like(B), torch.empty_like(B), torch.empty_like(B)
+        self.HP = torch.empty_like(B)
+        self.work = torch.empty(int(_lib.lib().edak_pcg_work_doubles(n, M)),
+                                dtype=torch.float64, device=dev)
+        self.hist_rz = torch.zeros((M, L), dtype=torch.float64, device=dev)
+        self.hist_J = torch.full((M, L), float("nan"), dtype=torch.float64, device=dev)
+        self.status = torch.zeros(M, dtype=torch.int32, device=dev)
+        self.iters = torch.zeros(M, dtype=torch.int32, device=dev)
+        s = _lib.stream()
+        if Z0 is None:
+            Z0 = apply_p(B) if apply_p is not None else B
+        _lib.call("edak_pcg_init", n, M, B.data_ptr(), Z0.data_ptr(), self.X.data_ptr(),
+                  self.R.data_ptr(), self.P.data_ptr(), self.work.data_ptr(),
+                  self.hist_rz.data_ptr(), L, self.status.data_ptr(), self.iters.data_ptr(), s)
+        self.trace_cost = bool(cfg.trace_cost and cost is not None)
+        self.rec = self.trace_cost and cost[0] == "recurrence"
+        self.cost = cost
+        if self.rec:
+            D, sigma2 = cost[1].contiguous(), float(cost[2])
+            _lib.call("edak_pcg_cost0", D.shape[1], M, D.data_ptr(), sigma2,
+                      self.hist_J.data_ptr(), L, s)
+        elif self.trace_cost:
+            self.hist_J[:, 0] = cost[1](self.X)
+        self.rtol = -1.0 if cfg.residual_rtol is None else float(cfg.residual_rtol)
+        self.rzb = self.work[-3 * M:-M]
+        self.dot_tiles = dot_tiles
+        self.dotp = (torch.empty((M, dot_tiles), dtype=torch.float64, device=dev)
+                     if dot_tiles > 0 else None)
+        self.lmp = lmp
+        if lmp is not None:
+            S = lmp[0]
+            self.lmpwork = torch.empty(int(_lib.lib().edak_lmp_work_doubles(n, S.shape[0], M)),
+                                       dtype=torch.float64, device=dev)
+
+    def step(self, it):
+        n, M, L, s = self.n, self.M, self.L, _lib.stream()
+        X, R, P, HP, work = self.X, self.R, self.P, self.HP, self.work
+        self.apply_h(P, HP, self.dotp)
+        _lib.call("edak_pcg_alpha", n, M, P.data_ptr(), HP.data_ptr(), X.data_ptr(),
+                  R.data_ptr(), work.data_ptr(), self.status.data_ptr(), self.iters.data_ptr(),
+                  it, self.B.data_ptr() if self.rec else None, _lib.ptr(self.dotp),
+                  self.dot_tiles, s)
+        if self.trace_cost and not self.rec:
+            run = self.status == 0
+            self.hist_J[:, it] = torch.where(run, self.cost[1](X), self.hist_J[:, it])
+        hJ = self.hist_J.data_ptr() if self.rec else None
+        if self.lmp is not None:
+            S, coef = self.lmp
+            _lib.call("edak_pcg_lmp_beta", n, S.shape[0], M, S.data_ptr(), coef.data_ptr(),
+                      R.data_ptr(), P.data_ptr(), work.data_ptr(), self.lmpwork.data_ptr(),
+                      self.rtol, self.hist_rz.data_ptr(), hJ, L, self.status.data_ptr(),
+                      self.iters.data_ptr(), it, s)
+        else:
+            Zr = self.apply_p(R) if self.apply_p is not None else R
+            _lib.call("edak_pcg_beta", n, M, Zr.data_ptr(), R.data_ptr(), P.data_ptr(),
+                      work.data_ptr(), self.rtol, self.hist_rz.data_ptr(), hJ, L,
+                      self.status.data_ptr(), self.iters.data_ptr(), it, s)
+
+    def snapshot(self, it):
+        M = self.M
+        rz = self.rzb[(it & 1) * M:(it & 1) * M + M] if it else self.rzb[:M]
+        return (it, self.X.clone(), self.R.clone(), self.P.clone(), rz.clone())
+
+    def traces(self):
+        return _traces(self.status.cpu().numpy(), self.iters.cpu().numpy(),
+                       self.hist_rz.cpu().numpy(), self.hist_J.cpu().numpy(), self.trace_cost)
+
+
 def pcg_device(apply_h, B, cfg, apply_p=None, cost=None, check_every=8, snapshots=None,
                dot_tiles=0, lmp=None):
     """Batched PCG on a (M, n) device block of right-hand sides.
@@ -104,68 +186,16 @@ def pcg_device(apply_h, B, cfg, apply_p=None, cost=None, check_every=8, snapshot
     J values.  ``snapshots`` (a list) receives device copies of
     (it, X, R, P, rz) after every iteration (parity tests: teacher forcing).
     Returns X (M, n) and a list of SolveTrace."""
-    B = B.contiguous()
-    M, n = B.shape
-    dev = B.device
-    L = cfg.max_iters + 1
-    X, Rr, P = torch.empty_like(B), torch.empty_like(B), torch.empty_like(B)
-    HP = torch.empty_like(B)
-    work = torch.empty(int(_lib.lib().edak_pcg_work_doubles(n, M)), dtype=torch.float64,
-                       device=dev)
-    hist_rz = torch.zeros((M, L), dtype=torch.float64, device=dev)
-    hist_J = torch.full((M, L), float("nan"), dtype=torch.float64, device=dev)
-    status = torch.zeros(M, dtype=torch.int32, device=dev)
-    iters = torch.zeros(M, dtype=torch.int32, device=dev)
-    s = _lib.stream()
-    Z0 = apply_p(B) if apply_p is not None else B
-    _lib.call("edak_pcg_init", n, M, B.data_ptr(), Z0.data_ptr(), X.data_ptr(), Rr.data_ptr(),
-              P.data_ptr(), work.data_ptr(), hist_rz.data_ptr(), L, status.data_ptr(),
-              iters.data_ptr(), s)
-    trace_cost = bool(cfg.trace_cost and cost is not None)
-    rec = trace_cost and cost[0] == "recurrence"
-    if rec:
-        D, sigma2 = cost[1].contiguous(), float(cost[2])
-        _lib.call("edak_pcg_cost0", D.shape[1], M, D.data_ptr(), sigma2, hist_J.data_ptr(), L, s)
-    elif trace_cost:
-        hist_J[:, 0] = cost[1](X)
-    rtol = -1.0 if cfg.residual_rtol is None else float(cfg.residual_rtol)
-    rzb = work[-3 * M:-M]
-    dotp = (torch.empty((M, dot_tiles), dtype=torch.float64, device=dev) if dot_tiles > 0
-            else None)
-    if lmp is not None:
-        S, coef = lmp
-        lmpwork = torch.empty(int(_lib.lib().edak_lmp_work_doubles(n, S.shape[0], M)),
-                              dtype=torch.float64, device=dev)
+    run = _PcgRun(apply_h, B, cfg, apply_p, cost, dot_tiles, lmp)
     if snapshots is not None:
-        snapshots.append((0, X.clone(), Rr.clone(), P.clone(), rzb[:M].clone()))
+        snapshots.append(run.snapshot(0))
     for it in range(1, cfg.max_iters + 1):
-        apply_h(P, HP, dotp)
-        _lib.call("edak_pcg_alpha", n, M, P.data_ptr(), HP.data_ptr(), X.data_ptr(),
-                  Rr.data_ptr(), work.data_ptr(), status.data_ptr(), iters.data_ptr(), it,
-                  B.data_ptr() if rec else None, _lib.ptr(dotp), dot_tiles, s)
-        if not rec:
-            if trace_cost:
-                run = status == 0
-                hist_J[:, it] = torch.where(run, cost[1](X), hist_J[:, it])
-        if lmp is not None:
-            _lib.call("edak_pcg_lmp_beta", n, S.shape[0], M, S.data_ptr(), coef.data_ptr(),
-                      Rr.data_ptr(), P.data_ptr(), work.data_ptr(), lmpwork.data_ptr(), rtol,
-                      hist_rz.data_ptr(), hist_J.data_ptr() if rec else None, L,
-                      status.data_ptr(), iters.data_ptr(), it, s)
-        else:
-            Zr = apply_p(Rr) if apply_p is not None else Rr
-            _lib.call("edak_pcg_beta", n, M, Zr.data_ptr(), Rr.data_ptr(), P.data_ptr(),
-                      work.data_ptr(), rtol, hist_rz.data_ptr(),
-                      hist_J.data_ptr() if rec else None, L, status.data_ptr(),
-                      iters.data_ptr(), it, s)
+        run.step(it)
         if snapshots is not None:
-            snapshots.append((it, X.clone(), Rr.clone(), P.clone(),
-                              rzb[(it & 1) * M:(it & 1) * M + M].clone()))
-        if rtol >= 0.0 and it % check_every == 0 and bool((status != 0).all()):
+            snapshots.append(run.snapshot(it))
+        if run.rtol >= 0.0 and it % check_every == 0 and bool((run.status != 0).all()):
             break
-    traces = _traces(status.cpu().numpy(), iters.cpu().numpy(), hist_rz.cpu().numpy(),
-                     hist_J.cpu().numpy(), trace_cost)
-    return X, traces
+    return run.X, run.traces()
 
 
 def _device_problem(apply_h):
@@ -223,25 +253,95 @@ def pcg(apply_h, b, cfg, precond=None, cost_fn=None):
     return x, traces[0]
 
 
-def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fused=True):
+_SIDE_STREAMS = {}
+
+
+def _side_streams(count):
+    """Persistent side streams (per device): the caching allocator keeps its
+    blocks per stream, so fresh streams every pass would re-allocate the PCG
+    state each time."""
+    dev = torch.cuda.current_device()
+    lst = _SIDE_STREAMS.setdefault(dev, [])
+    while len(lst) < count:
+        lst.append(torch.cuda.Stream())
+    return lst[:count]
+
+
+def _default_groups(M):
+    import os
+    g = os.environ.get("EDAK_PCG_GROUPS")
+    if g is not None:
+        return max(1, int(g))
+    return 2 if M >= 64 else 1
+
+
+def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fused=True,
+                groups=None, check_every=8):
     """Batched PCG over all members of an ``Ensemble``: B (M, n) device
     right-hand sides (e.g. ens.rhs_all()).  cost: "recurrence", "exact" or
     None.  ``fused`` folds p.Hp into the Hessian's last pass and a
-    single-pass LMP into the beta step.  Returns (X (M, n), [SolveTrace] * M)."""
-    work = ens.lin.work(ens.M)
+    single-pass LMP into the beta step.
 
-    def apply_h_cols(P, out, dotp):
-        ens.a_apply_members(P, ident=1.0, out=out, work=work, dot_part=dotp)
-
+    ``groups`` > 1 splits the members into that many independent batches,
+    each stepped on its own CUDA stream in lockstep: members never interact,
+    so the streams only share the GPU, and one group's sweeps fill the SMs
+    the other leaves idle (the last partial wave of every sweep launch, the
+    HBM-bound vector updates and the DMMA GEMMs).  Default: 2 for >= 64
+    members (EDAK_PCG_GROUPS overrides).  Returns (X (M, n), [SolveTrace] * M)."""
+    M = ens.M
+    G = _default_groups(M) if groups is None else groups
+    if snapshots is not None or M < 2:
+        G = 1
+    G = max(1, min(G, M))
     apply_p = precond.apply_cols if precond is not None else None
     lmp = precond.single_pass() if (fused and precond is not None) else None
-    c = None
-    if cfg.trace_cost and cost == "recurrence":
-        c = ("recurrence", ens.D, ens.lin.sigma2)
-    elif cfg.trace_cost and cost == "exact":
-        c = ("exact", ens.cost_members)
-    return pcg_device(apply_h_cols, B, cfg, apply_p, c, snapshots=snapshots,
-                      dot_tiles=ens.lin.dot_tiles() if fused else 0, lmp=lmp)
+    B = B.contiguous()
+    Z0 = apply_p(B) if apply_p is not None else B
+    bounds = [M * g // G for g in range(G + 1)]
+    main = torch.cuda.current_stream()
+    streams = [main] + _side_streams(G - 1)
+    runs = []
+    for g in range(G):
+        lo, hi = bounds[g], bounds[g + 1]
+        sub = ens if G == 1 else ens.subset(lo, hi)
+        if g:
+            streams[g].wait_stream(main)
+        with torch.cuda.stream(streams[g]):
+            work = sub.lin.work(sub.M)
+
+            def apply_h_cols(P, out, dotp, sub=sub, work=work):
+                sub.a_apply_members(P, ident=1.0, out=out, work=work, dot_part=dotp)
+
+            c = None
+            if cfg.trace_cost and cost == "recurrence":
+                c = ("recurrence", sub.D, sub.lin.sigma2)
+            elif cfg.trace_cost and cost == "exact":
+                c = ("exact", sub.cost_members)
+            runs.append(_PcgRun(apply_h_cols, B[lo:hi], cfg, apply_p, c,
+                                sub.lin.dot_tiles() if fused else 0, lmp, Z0[lo:hi]))
+    if snapshots is not None:
+        snapshots.append(runs[0].snapshot(0))
+    rtol = runs[0].rtol
+    for it in range(1, cfg.max_iters + 1):
+        for g, run in enumerate(runs):
+            with torch.cuda.stream(streams[g]):
+                run.step(it)
+        if G > 1:
+            ens.n_matvecs += 1  # one batched member apply per iteration
+        if snapshots is not None:
+            snapshots.append(runs[0].snapshot(it))
+        if rtol >= 0.0 and it % check_every == 0:
+            for g in range(1, G):
+                main.wait_stream(streams[g])
+            if all(bool((r.status != 0).all()) for r in runs):
+                break
+    for g in range(1, G):
+        main.wait_stream(streams[g])
+    if G == 1:
+        return runs[0].X, runs[0].traces()
+    X = torch.cat([r.X for r in runs], 0)
+    traces = [t for r in runs for t in r.traces()]
+    return X, traces
 
 
 # ----------------------------------------------------------------- Lanczos --
