@@ -497,12 +497,19 @@ static int env_int(const char* name, int dflt) {
 // splitting the window into chunks of <= SWEEP_CHUNK steps (ring state
 // handed over through HBM between chunks: 16 B/element per boundary) keeps
 // the halo small.  work2 = 2 * ncols * n doubles (NULL: one chunk).
-constexpr int SWEEP_CHUNK = 8;
+constexpr int SWEEP_CHUNK = 12;  // measured best at cfg4/cfg5 (tools/ab_tiles.py)
+
+static int sweep_chunk() {
+  const char* e = getenv("EDAK_SWEEP_CHUNK");  // A/B knob
+  const int v = e ? atoi(e) : SWEEP_CHUNK;
+  return v >= 1 ? v : SWEEP_CHUNK;
+}
 
 static int plan_chunks(int N, bool periodic, const double* work2) {
-  if (periodic || !work2 || N <= SWEEP_CHUNK) return 1;
+  const int K = sweep_chunk();
+  if (periodic || !work2 || N <= K) return 1;
   if (const char* e = getenv("EDAK_SWEEP_NOCHUNK")) return 1;
-  return (N + SWEEP_CHUNK - 1) / SWEEP_CHUNK;
+  return (N + K - 1) / K;
 }
 
 // 16-byte pair staging: every row start and tile base even, rows 16-B aligned
@@ -580,6 +587,8 @@ v1:
     const int mb = env_int("EDAK_TL_MINB", 4);
     if (C == 8 && NT == 128 && !stream && mb == 4 && pair_ok(P, geo)) {
       go<128, 8>(k_tl<8, 128, false, 4, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
+    } else if (C == 8 && NT == 256 && !stream && pair_ok(P, geo)) {
+      go<256, 8>(k_tl<8, 256, false, 2, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
     } else if (C == 8 && NT == 128 && !stream && mb == 3) {
       go<128, 8>(k_tl<8, 128, false, 3>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
     } else if (C == 8 && NT == 128 && !stream && mb == 4) {
@@ -653,6 +662,9 @@ v1:
     const int mb = env_int("EDAK_AD_MINB", 3);
     if (C == 8 && NT == 128 && !stream && mb == 3 && pair_ok(P, geo)) {
       go<128, 8, 2 * 8 * 128>(k_ad<8, 128, false, 3, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1,
+                              gin);
+    } else if (C == 8 && NT == 256 && !stream && pair_ok(P, geo)) {
+      go<256, 8, 2 * 8 * 256>(k_ad<8, 256, false, 1, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1,
                               gin);
     } else if (C == 8 && NT == 128 && !stream && mb == 3) {
       go<128, 8>(k_ad<8, 128, false, 3>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1, gin);

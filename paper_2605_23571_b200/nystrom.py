@@ -30,7 +30,8 @@ from .linalg import col_dots, gemm_nn, gemm_tn, potrf_shifted, svd_jacobi, trinv
 
 SHIFT_MODES = (None, "trace", "ynorm")
 _MODE_CODE = {None: 0, "trace": 1, "ynorm": 2}
-JACOBI_DIRECT_MAX_N = 4096
+QR_MIN_ASPECT = 4
+QR_MIN_N = 256
 
 
 class NystromBreakdownError(RuntimeError):
@@ -111,25 +112,49 @@ def _check_rank(Y):
         raise NystromBreakdownError(f"sketch column {dead[0]} was annihilated by the operator")
 
 
+def _cholqr_pass(Y, shift=0.0):
+    """One CholeskyQR pass: R = chol(Y^T Y + shift I), Q = Y R^-1 (DMMA
+    Grams / products); info[1] != 0 when the Gram was not numerically SPD."""
+    G = gemm_tn(Y, Y)
+    if shift:
+        G.diagonal().add_(shift)
+    R, _, info = potrf_shifted(G, 0)
+    return gemm_nn(Y, trinv_upper(R)), R, info
+
+
 def _cholqr2(Y):
-    """Q (l, n) block and upper R (l, l) block with Y = Q R, or None when a
-    Gram matrix is not numerically positive definite."""
-    G1 = gemm_tn(Y, Y)
-    R1, _, info1 = potrf_shifted(G1, 0)
-    Q1 = gemm_nn(Y, trinv_upper(R1))
-    G2 = gemm_tn(Q1, Q1)
-    R2, _, info2 = potrf_shifted(G2, 0)
-    if int(info1[1]) or int(info2[1]):
+    """Q (l, n) block and upper R (l, l) block with Y = Q R by shifted
+    CholeskyQR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa, SIAM J.
+    Sci. Comput. 2020): a first pass on Y^T Y + s I, s = 11 (m l + l (l+1))
+    u ||Y||_F^2 -- SPD for any cond(Y) < u^-1 -- then CholeskyQR2 of its Q.
+    Orthogonality and residual end at the u level, like the reference's
+    Householder QR (nystrom.py:118); every pass is two DMMA GEMMs plus an
+    (l x l) Cholesky / triangular inverse.  None only if a Gram broke down."""
+    l, m = Y.shape
+    tr = float(col_dots(Y, Y).sum())
+    s = 11.0 * (m * l + l * (l + 1)) * np.finfo(float).eps * tr
+    Q, R, info = _cholqr_pass(Y, s)
+    if int(info[1]):
         return None
-    Q = gemm_nn(Q1, trinv_upper(R2))
-    R = gemm_nn(R2, R1)  # R2 R1 (upper)
+    for _ in range(2):
+        Q, R2, info = _cholqr_pass(Q)
+        if int(info[1]):
+            return None
+        R = gemm_nn(R2, R)  # upper R_k ... R_1
     return Q, R
+
+
+def _use_qr(n, ell):
+    """Tall sketches go through CholeskyQR + an (l x l) Jacobi SVD; short or
+    wide ones (n < 4 l, e.g. cfg2's l = 50 > n = 40) through a Jacobi SVD
+    of the whole F, which also covers exact rank deficiency."""
+    return n >= QR_MIN_ASPECT * ell and n >= QR_MIN_N
 
 
 def _orthobasis(Y):
     """Orthonormal basis of range(Y) for the q > 1 passes."""
     n = Y.shape[1]
-    if n >= Y.shape[0] and n > JACOBI_DIRECT_MAX_N:
+    if _use_qr(n, Y.shape[0]):
         qr = _cholqr2(Y)
         if qr is not None:
             return qr[0]
@@ -174,7 +199,7 @@ def nystrom_evd(a_apply, sketch, cfg):
     shift = float(nu[0])
     Cinv = trinv_upper(Cm)
     k_eff = min(cfg.k, ell, n)
-    qr = _cholqr2(Y) if (n >= ell and n > JACOBI_DIRECT_MAX_N) else None
+    qr = _cholqr2(Y) if _use_qr(n, ell) else None
     if qr is not None:
         Q, R = qr
         T = gemm_nn(R, Cinv)                 # R_Y C^-1 (l x l)
