@@ -154,6 +154,14 @@ int edak_potrf_shifted(const double* W, int l, double* C, int mode,
                        void* stream);
 /* Rinv = R^-1 for upper-triangular R (l x l) */
 int edak_trinv_upper(const double* R, int l, double* Rinv, void* stream);
+/* Fused blocked Cholesky (same shift schedule / breakdown test / info as
+ * edak_potrf_shifted) and inverse: C upper with W = C^T C and, if Cinv !=
+ * NULL, Cinv = C^-1 (nystrom.py:67-93,129).  work: NULL for l <= 128, else
+ * edak_chol_inv_work_doubles(l) doubles. */
+int64_t edak_chol_inv_work_doubles(int l);
+int edak_chol_inv(const double* W, int l, double* C, double* Cinv, int mode,
+                  double scale, double* nu_out, int32_t* info, double* work,
+                  void* stream);
 /* one-sided (Hestenes) Jacobi SVD of M (rows x cols, rows >= cols,
  * column-major): M V = U diag(sig), sig descending (np.linalg.svd,
  * nystrom.py:130).  U (rows x cols), sig (cols), V (cols x cols) or NULL.

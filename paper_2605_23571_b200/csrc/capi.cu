@@ -43,6 +43,8 @@ int launch_gemm_nn(const double*, int64_t, const double*, int, const double*, co
 int launch_col_dots(int, int, const double*, const double*, double*, cudaStream_t);
 int launch_potrf_shifted(const double*, int, double*, int, double, double*, int32_t*, cudaStream_t);
 int launch_trinv_upper(const double*, int, double*, cudaStream_t);
+int launch_chol_inv(const double*, int, double*, double*, int, double, double*, int32_t*, double*, cudaStream_t);
+int64_t chol_inv_work_doubles(int l);
 int64_t svd_work_doubles(int, int);
 int launch_svd_jacobi(const double*, int, int, double*, double*, double*, double*, cudaStream_t);
 int64_t pcg_work_doubles(int, int);
@@ -198,6 +200,14 @@ int edak_potrf_shifted(const double* W, int l, double* C, int mode, double scale
                        void* stream) {
   if (!W || !C || !nu_out || !info || l < 1) return EDAK_EINVAL;
   return launch_potrf_shifted(W, l, C, mode, scale, nu_out, info, as_stream(stream));
+}
+
+int64_t edak_chol_inv_work_doubles(int l) { return chol_inv_work_doubles(l); }
+
+int edak_chol_inv(const double* W, int l, double* C, double* Cinv, int mode, double scale, double* nu_out,
+                  int32_t* info, double* work, void* stream) {
+  if (!W || !C || !nu_out || !info || l < 1) return EDAK_EINVAL;
+  return launch_chol_inv(W, l, C, Cinv, mode, scale, nu_out, info, work, as_stream(stream));
 }
 
 int edak_trinv_upper(const double* R, int l, double* Rinv, void* stream) {

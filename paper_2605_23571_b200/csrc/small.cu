@@ -224,6 +224,16 @@ int launch_trinv_upper(const double* R, int l, double* X, cudaStream_t st) {
 // V (cols x cols) if Vout != NULL.
 constexpr int JAC_NT = 1024;
 
+// 1/x to full double precision: hardware reciprocal seed + two Newton steps
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 // smem_mode: 0 = everything in the global workspace (L2); 1 = A in shared
 // memory; 2 = A and V in shared memory (l <= 128 fits: 128 KB)
 __global__ void __launch_bounds__(JAC_NT) k_svd_jacobi(const double* __restrict__ M, int rows, int cols,
@@ -247,7 +257,20 @@ __global__ void __launch_bounds__(JAC_NT) k_svd_jacobi(const double* __restrict_
   // Both halves of a warp always run the same loop trip count (shuffles use
   // the full mask); idle halves carry live = false.
   const int hl = t & 15, half = (t >> 4) & 1;
-  for (int sweep = 0; sweep < 40; ++sweep) {
+  // squared column norms, recomputed at every sweep start and tracked
+  // through the rotations in between (al' = al - t ga, be' = be + t ga), so a
+  // pair costs one dot instead of three; the rotation parameters are
+  // evaluated once per pair (lane 0 of the half-warp) and broadcast
+  double* n2 = nrm;  // cols entries (the final norms reuse it afterwards)
+  int sweep = 0;
+  for (; sweep < 40; ++sweep) {
+    for (int j = warp; j < cols; j += nw) {
+      double s2 = 0.0;
+      const double* a = A + (size_t)j * rows;
+      for (int i = lane; i < rows; i += 32) s2 = fma(a[i], a[i], s2);
+      s2 = warp_sum(s2);
+      if (lane == 0) n2[j] = s2;
+    }
     if (t == 0) rotated = 0;
     __syncthreads();
     for (int rd = 0; rd < m - 1; ++rd) {
@@ -256,54 +279,77 @@ __global__ void __launch_bounds__(JAC_NT) k_svd_jacobi(const double* __restrict_
         int p = 0, q = 0;
         bool live = k < m / 2;
         if (live) {
-          p = k == 0 ? 0 : ((k - 1 + rd) % (m - 1)) + 1;
-          q = ((m - 1 - k - 1 + rd) % (m - 1)) + 1;
+          if (k != 0) {
+            p = k - 1 + rd;
+            p = (p >= m - 1 ? p - (m - 1) : p) + 1;
+          }
+          q = m - 2 - k + rd;
+          q = (q >= m - 1 ? q - (m - 1) : q) + 1;
           if (p > q) { int tmp = p; p = q; q = tmp; }
           live = q < cols && p != q;
         }
         double* ap = A + (size_t)p * rows;
         double* aq = A + (size_t)q * rows;
-        double al = 0.0, be = 0.0, ga = 0.0;
+        double ga = 0.0;
         if (live) {
-          for (int i = hl; i < rows; i += 16) {
-            const double x = ap[i], y = aq[i];
-            al = fma(x, x, al);
-            be = fma(y, y, be);
-            ga = fma(x, y, ga);
+          double g2 = 0.0;
+          int i = hl;
+          for (; i + 16 < rows; i += 32) {  // two chains
+            ga = fma(ap[i], aq[i], ga);
+            g2 = fma(ap[i + 16], aq[i + 16], g2);
           }
+          if (i < rows) ga = fma(ap[i], aq[i], ga);
+          ga += g2;
         }
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) {
-          al += __shfl_xor_sync(0xffffffffu, al, o);
-          be += __shfl_xor_sync(0xffffffffu, be, o);
-          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        for (int o = 8; o > 0; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        double c = 1.0, sn = 0.0, tt = 0.0;
+        bool rot = false;
+        if (live && hl == 0) {
+          const double al = n2[p], be = n2[q];
+          // threshold without square roots: |ga| <= tol sqrt(al be)
+          rot = al > 0.0 && be > 0.0 && ga * ga > tol2 * (al * be);
+          if (rot) {
+            // rotation from reciprocals refined by Newton steps instead of
+            // IEEE division / sqrt (the angle only has to be accurate to a
+            // few ulps; this is the serial part of every Jacobi round)
+            const double zeta = (be - al) * fast_rcp(2.0 * ga);
+            const double z2 = fma(zeta, zeta, 1.0);
+            const double sq = z2 * rsqrt(z2);  // sqrt(1 + zeta^2)
+            tt = copysign(fast_rcp(fabs(zeta) + sq), zeta);
+            c = rsqrt(fma(tt, tt, 1.0));
+            sn = c * tt;
+            n2[p] = fma(-tt, ga, al);
+            n2[q] = fma(tt, ga, be);
+            rotated = 1;
+          }
         }
-        // threshold without square roots: |ga| <= tol sqrt(al be)
-        if (!live || al == 0.0 || be == 0.0 || ga * ga <= tol2 * (al * be)) continue;
-        const double zeta = (be - al) / (2.0 * ga);
-        const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-        const double c = rsqrt(fma(tt, tt, 1.0)), s = c * tt;
+        const int src = half * 16;
+        rot = __shfl_sync(0xffffffffu, rot, src);
+        c = __shfl_sync(0xffffffffu, c, src);
+        sn = __shfl_sync(0xffffffffu, sn, src);
+        if (!rot) continue;
         for (int i = hl; i < rows; i += 16) {
           const double x = ap[i], y = aq[i];
-          ap[i] = c * x - s * y;
-          aq[i] = s * x + c * y;
+          ap[i] = c * x - sn * y;
+          aq[i] = sn * x + c * y;
         }
         if (Vout) {
           double* vp = V + (size_t)p * cols;
           double* vq = V + (size_t)q * cols;
           for (int i = hl; i < cols; i += 16) {
             const double x = vp[i], y = vq[i];
-            vp[i] = c * x - s * y;
-            vq[i] = s * x + c * y;
+            vp[i] = c * x - sn * y;
+            vq[i] = sn * x + c * y;
           }
         }
-        if (hl == 0) rotated = 1;
       }
       __syncthreads();
     }
     if (!rotated) break;
     __syncthreads();
   }
+  if (t == 0) nrm[cols] = (double)(sweep + 1);  // sweeps run (diagnostics)
   // column norms
   for (int j = warp; j < cols; j += nw) {
     double s = 0.0;
@@ -335,7 +381,7 @@ __global__ void __launch_bounds__(JAC_NT) k_svd_jacobi(const double* __restrict_
   }
 }
 
-int64_t svd_work_doubles(int rows, int cols) { return (int64_t)rows * cols + (int64_t)cols * cols + cols; }
+int64_t svd_work_doubles(int rows, int cols) { return (int64_t)rows * cols + (int64_t)cols * cols + cols + 1; }
 
 int launch_svd_jacobi(const double* M, int rows, int cols, double* U, double* sig, double* V, double* work,
                       cudaStream_t st) {

@@ -59,6 +59,23 @@ def potrf_shifted(W, mode, scale=0.0):
     return Cm, nu, info
 
 
+def chol_inv(W, mode, scale=0.0, want_inv=True):
+    """Fused blocked Cholesky + inverse (edak_chol_inv): (C, C^-1 or None,
+    nu tensor[1], info int32[2]) with potrf_shifted's schedule -- no host
+    sync."""
+    W = W.contiguous()
+    l = W.shape[0]
+    Cm = torch.empty_like(W)
+    Ci = torch.empty_like(W) if want_inv else None
+    nu = _empty(1, like=W)
+    info = torch.zeros(2, dtype=torch.int32, device=W.device)
+    nw = int(_lib.lib().edak_chol_inv_work_doubles(l))
+    work = _empty(nw, like=W) if nw else None
+    _lib.call("edak_chol_inv", W.data_ptr(), l, Cm.data_ptr(), _lib.ptr(Ci), int(mode),
+              float(scale), nu.data_ptr(), info.data_ptr(), _lib.ptr(work), _lib.stream())
+    return Cm, Ci, nu, info
+
+
 def trinv_upper(R):
     R = R.contiguous()
     X = torch.empty_like(R)

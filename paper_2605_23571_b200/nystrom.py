@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _dev
-from .linalg import col_dots, gemm_nn, gemm_tn, potrf_shifted, svd_jacobi, trinv_upper
+from .linalg import chol_inv, col_dots, gemm_nn, gemm_tn, svd_jacobi
 
 SHIFT_MODES = (None, "trace", "ynorm")
 _MODE_CODE = {None: 0, "trace": 1, "ynorm": 2}
@@ -118,8 +118,8 @@ def _cholqr_pass(Y, shift=0.0):
     G = gemm_tn(Y, Y)
     if shift:
         G.diagonal().add_(shift)
-    R, _, info = potrf_shifted(G, 0)
-    return gemm_nn(Y, trinv_upper(R)), R, info
+    R, Rinv, _, info = chol_inv(G, 0)
+    return gemm_nn(Y, Rinv), R, info
 
 
 def _cholqr2(Y):
@@ -188,7 +188,7 @@ def nystrom_evd(a_apply, sketch, cfg):
     scale = 0.0
     if cfg.shift_mode == "ynorm":
         scale = float(torch.sqrt(col_dots(Y, Y).sum()))
-    Cm, nu, info = potrf_shifted(W, mode, scale)
+    Cm, Cinv, nu, info = chol_inv(W, mode, scale)
     info = info.cpu().numpy()
     if info[1]:
         if info[0] <= 1:
@@ -197,7 +197,6 @@ def nystrom_evd(a_apply, sketch, cfg):
                 "usable shift is available")
         raise NystromBreakdownError("sketched Gram matrix stayed indefinite after shifting")
     shift = float(nu[0])
-    Cinv = trinv_upper(Cm)
     k_eff = min(cfg.k, ell, n)
     qr = _cholqr2(Y) if _use_qr(n, ell) else None
     if qr is not None:

@@ -312,3 +312,40 @@ def test_pcg_fused_lmp_beta_matches_two_step(gpu, ref_problem):
         assert np.max(np.abs(np.array(trf[j].resnorm) - tru[j].resnorm)) <= 1e-10 * r0
     for j in (0, 4, 9):
         npt.assert_allclose(trf[j].cost, g[f"cfg1_m{j}_cost"], rtol=1e-10)
+
+
+@pytest.mark.parametrize("l", [1, 6, 31, 33, 50, 64, 128, 129, 200, 256])
+def test_chol_inv_matches_potrf_and_inverse(gpu, l):
+    """Fused blocked Cholesky + inverse (cholinv.cu): same factor, shift
+    schedule, nu and info as potrf_shifted; C^-1 C = I; zero/indefinite
+    cases fail the same way."""
+    from paper_2605_23571_b200.linalg import chol_inv, potrf_shifted
+    rng = np.random.default_rng(l + 100)
+    x = rng.standard_normal((l, l))
+    w = x @ x.T + l * np.eye(l)
+    W = torch.tensor(w.T.copy(), device="cuda")
+    C, Ci, nu, info = chol_inv(W, 0)
+    assert info.cpu().tolist() == [0, 0] and float(nu[0]) == 0.0
+    c = C.cpu().numpy().T
+    npt.assert_allclose(c, np.linalg.cholesky(w).T, rtol=1e-12, atol=1e-12 * np.abs(c).max())
+    C2, _, _ = potrf_shifted(W, 0)
+    npt.assert_allclose(c, C2.cpu().numpy().T, rtol=1e-13, atol=1e-13 * np.abs(c).max())
+    X = Ci.cpu().numpy().T
+    assert np.allclose(X, np.triu(X)) and np.allclose(c, np.triu(c))
+    npt.assert_allclose(X @ c, np.eye(l), atol=1e-12)
+    for mode, scale in ((1, 0.0), (2, 7.0)):
+        y = rng.standard_normal((l, max(1, l // 2)))
+        wd = y @ y.T
+        Wd = torch.tensor(wd.T.copy(), device="cuda")
+        C, Ci, nu, info = chol_inv(Wd, mode, scale)
+        Cr, nur, infor = potrf_shifted(Wd, mode, scale)
+        assert info.cpu().tolist() == infor.cpu().tolist()
+        assert float(nu[0]) == float(nur[0])
+        if info.cpu().tolist()[1] == 0:
+            c = C.cpu().numpy().T
+            npt.assert_allclose(c.T @ c, wd + float(nu[0]) * np.eye(l),
+                                atol=1e-10 * max(np.abs(wd).max(), 1e-300))
+            npt.assert_allclose(Ci.cpu().numpy().T @ c, np.eye(l), atol=1e-6)
+    Z = torch.zeros(l, l, dtype=torch.float64, device="cuda")
+    assert chol_inv(Z, 0)[3].cpu().tolist()[1] == 1
+    assert chol_inv(Z, 2, 0.0)[3].cpu().tolist()[1] == 1

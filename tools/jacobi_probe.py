@@ -1,0 +1,42 @@
+"""Sweeps and time of the device Jacobi SVD on random / Nystrom-like T."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2605_23571_b200 import _lib, build  # noqa: E402
+
+build.build()
+lib = _lib.lib()
+
+
+def run(Mnp):
+    M = torch.from_numpy(np.ascontiguousarray(Mnp)).cuda()
+    cols, rows = M.shape
+    U = torch.empty_like(M)
+    sig = torch.empty(cols, dtype=torch.float64, device="cuda")
+    work = torch.empty(int(lib.edak_svd_work_doubles(rows, cols)), dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        _lib.call("edak_svd_jacobi", M.data_ptr(), rows, cols, U.data_ptr(), sig.data_ptr(), None,
+                  work.data_ptr(), _lib.stream())
+        e.record()
+        torch.cuda.synchronize()
+    ref = np.linalg.svd(Mnp.T, compute_uv=False)
+    err = np.max(np.abs(sig.cpu().numpy() - ref) / ref[0])
+    return s.elapsed_time(e), int(work[-1].item()), err
+
+
+rng = np.random.default_rng(0)
+for l in (64, 128, 256):
+    A = rng.standard_normal((l, l))
+    t, sw, err = run(A)
+    print(f"random {l}: {t:.3f} ms, {sw} sweeps, err {err:.1e}")
+    Q, _ = np.linalg.qr(rng.standard_normal((l, l)))
+    d = np.logspace(0, -8, l)
+    A = (Q * d) @ np.linalg.qr(rng.standard_normal((l, l)))[0]
+    t, sw, err = run(np.triu(A))
+    print(f"graded-triu {l}: {t:.3f} ms, {sw} sweeps, err {err:.1e}")

@@ -36,3 +36,6 @@ tp, _ = t(lambda: pcg_members(eng.members, B[1:].contiguous(), eng.scfg, lmp, en
 tall, _ = t(lambda: eng.run())
 print(f"{cfg.name}: rhs {tr:.2f} ms  sketch+nystrom+lmp {tl:.2f} ms  pcg {tp:.2f} ms "
       f"({tp / eng.iters:.3f} ms/it)  pass {tall:.2f} ms")
+for i in range(4):
+    ti, _ = t(lambda: eng.run(), reps=1)
+    print(f"  run {i}: {ti:.2f} ms")
