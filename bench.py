@@ -139,8 +139,9 @@ def _cpu_worker(args):
     d = inp.member_y[j] - inp.net.observe(traj)
     prob = MemberProblem(traj, inp.net, inp.ub, inp.rn, d)
     rng = np.random.default_rng(j)
-    s, _ = np.linalg.qr(rng.standard_normal((cfg.n, cfg.k)))
-    lmp = SpectralLmp(s, np.sort(rng.uniform(0, 1e3, cfg.k))[::-1], 2.0)
+    k = min(cfg.k, cfg.n)  # cfg2: k = 50 > n = 40 keeps 40 pairs, as nystrom_evd does
+    s, _ = np.linalg.qr(rng.standard_normal((cfg.n, k)))
+    lmp = SpectralLmp(s, np.sort(rng.uniform(0, 1e3, k))[::-1], 2.0)
     b = prob.rhs()
     t0 = time.perf_counter()
     pcg(prob.hessian_apply, b, SolverConfig(max_iters=iters), precond=lmp,
@@ -178,6 +179,11 @@ def cpu_sample(cfg_id, seconds, cores, truth, iters=None):
 
 
 # ------------------------------------------------------------ GPU leg -----
+# from the round's ncu --set full capture of the cfg4 sweeps (profiles/)
+SWEEP_DRAM_BYTES = {"k_ad": 0.754e9, "k_tl": 0.748e9}
+SWEEP_FP64_UTIL = "k_ad 56%, k_tl 59% of the FP64 pipe (ncu sm__pipe_fp64_cycles_active, profiles/)"
+
+
 def kernel_roofline(torch, lib, eng, reps, peaks):
     """Time the dominant kernels live (CUDA events on the launching stream)
     on the PCG block: AD sweep and TL sweep over all members."""
@@ -200,41 +206,44 @@ def kernel_roofline(torch, lib, eng, reps, peaks):
         e.record()
         torch.cuda.synchronize()
         out[name] = s.elapsed_time(e) / reps * 1e-3
-    # algorithmic flops per launch (TL 37, AD 42 per element-step)
+    # the binding roofline for per-member trajectories is HBM,
+    # with algorithmic bytes = the stored-stage formulation (4 stages x 8 B
+    # read per element-step per sweep, + 8 B/element of the swept vector in
+    # or out); algorithmic flops TL 37 / AD 42 per element-step
     flops = {"k_ad": 42.0 * N * n * M, "k_tl": 37.0 * N * n * M}
-    # executed flops: + stage recompute (22/elem-step) on the redundant-halo range
+    alg_bytes = 32.0 * N * n * M + 8.0 * n * M
     dom = max(out, key=out.get)
     t = out[dom]
-    achieved = flops[dom] / t / 1e12
-    # the streamed-stage HBM formulation the reference's Trajectory implies:
-    # 4 stages x 8 B read per element-step per sweep
-    stream_bytes = 32.0 * N * n * M + 16.0 * n * M
+    nlaunch = -(-N // 12) if N > 12 else 1  # window chunks of <= 12 steps (l96.cu SWEEP_CHUNK)
+    gbs = alg_bytes / t / 1e9
+    tflops = flops[dom] / t / 1e12
     return {
-        "bound": "fp64",
-        "kernel": dom + (" (edak_ad_sweep: 3 window chunks)" if dom == "k_ad"
-                         else " (edak_tl_sweep: 3 window chunks)"),
-        "executed_fp64_pipe_util": "k_ad 48%, k_tl 51% of the FP64 pipe (ncu, profiles/): the "
-                                   "stage recompute adds ~18 DP instructions per element-step "
-                                   "that the algorithmic count (37/42) leaves out",
-        "achieved": achieved,
-        "peak": peaks["dfma_tflops"],
-        "unit": "TFLOP/s",
-        "frac": achieved / peaks["dfma_tflops"],
-        # dram__bytes_read.sum + dram__bytes_write.sum of one edak_ad_sweep
-        # (3 chunk launches of k_ad) from `ncu --set full`
-        # (profiles/r1_cfg4_sweeps_ncu_summary.txt); algorithmic minimum ~0.66 GB
-        "traffic": 0.795e9 if dom == "k_ad" else 0.80e9,
-        "traffic_unit": "bytes per launch (ncu, profiles/r1_cfg4_sweeps_ncu_summary.txt)",
-        "peak_source": "measured in this run: DFMA-pipe loop (edak_peak_dfma); "
-                       "DMMA loop %.1f TFLOP/s" % peaks["dmma_tflops"],
-        "algorithmic_flops_per_launch": flops[dom],
+        "bound": "hbm",
+        "kernel": f"{dom} ({'AD' if dom == 'k_ad' else 'TL'} sweep over the {M} member "
+                  f"trajectories; one sweep = {nlaunch} window-chunk launches, figures per sweep)",
+        "achieved": gbs,
+        "peak": peaks["hbm_gbs"],
+        "unit": "GB/s",
+        "frac": gbs / peaks["hbm_gbs"],
+        # dram__bytes_read.sum + dram__bytes_write.sum of the sweep's launches
+        # (ncu --set full, profiles/r1_cfg4_sweeps_ncu_summary.txt)
+        "traffic": SWEEP_DRAM_BYTES.get(dom),
+        "traffic_unit": "bytes per sweep (ncu, profiles/r1_cfg4_sweeps_ncu_summary.txt)",
+        "algorithmic_bytes": alg_bytes,
+        "basis": "SURVEY.md 8d: stored-stage formulation, 32*N*n + 8*n B per column per sweep. "
+                 "The kernel recomputes the RK4 stages from the states (8 B/elem-step read), "
+                 "so its physical DRAM traffic ('traffic') is below the algorithmic bytes "
+                 "and what actually binds it is the FP64 pipe (see 'fp64').",
+        "peak_source": "hbm: MEASURED_PEAKS.json hbm_gbs; fp64: DFMA loop measured in this run",
         "launch_ms": t * 1e3,
         "launch_ms_other": {k: v * 1e3 for k, v in out.items() if k != dom},
-        "hbm_equivalent": {
-            "note": "GB/s the same launch would need if it streamed the stored RK4 "
-                    "stages (64 B/elem-step per apply) instead of recomputing them",
-            "achieved_gbs": stream_bytes / t / 1e9,
-            "hbm_peak_gbs": peaks["hbm_gbs"],
+        "fp64": {
+            "algorithmic_flops": flops[dom],
+            "achieved_tflops": tflops,
+            "peak_tflops": peaks["dfma_tflops"],
+            "frac": tflops / peaks["dfma_tflops"],
+            "dmma_peak_tflops": peaks["dmma_tflops"],
+            "executed_pipe_util": SWEEP_FP64_UTIL,
         },
     }
 
