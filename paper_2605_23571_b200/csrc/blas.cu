@@ -11,6 +11,7 @@
 //                 (lmp.py:65).  DMMA 64x64 tiles.
 //  * column dots, fixed order (PCG r.z, p.Hp; krylov.py:72,81,87).
 #include "common.cuh"
+#include <cstdlib>
 
 namespace edak {
 
@@ -125,7 +126,11 @@ __global__ void k_reduce_parts(const double* __restrict__ part, int nsplit, int 
 
 static int tn_nsplit(int m, int nb, int64_t K, int64_t& kslice) {
   const int tiles = ((m + G_BM - 1) / G_BM) * ((nb + G_BN - 1) / G_BN);
-  int64_t want = (2 * 148 + tiles - 1) / tiles;  // >= ~2 waves of CTAs
+  static const int waves = [] {  // A/B knob: CTAs per SM targeted by the split
+    const char* e = getenv("EDAK_TN_WAVES");
+    return e ? atoi(e) : 2;
+  }();
+  int64_t want = (waves * 148 + tiles - 1) / tiles;
   int64_t maxs = (K + 255) / 256;                // slices of >= 256 rows
   int64_t s = want < maxs ? want : maxs;
   if (s < 1) s = 1;

@@ -10,7 +10,7 @@ import torch  # noqa: E402
 from paper_2605_23571_b200 import _lib, build  # noqa: E402
 
 build.build()
-n, k, M = 16384, 128, 200
+n, k, M = 16384, 128, int(os.environ.get("COLS", "100"))
 dev = "cuda"
 S = torch.randn(k, n, dtype=torch.float64, device=dev)
 R = torch.randn(M, n, dtype=torch.float64, device=dev)
