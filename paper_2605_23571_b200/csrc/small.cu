@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(JAC_NT) k_svd_jacobi(const double* __restrict_
     if (!rotated) break;
     __syncthreads();
   }
-  if (t == 0) nrm[cols] = (double)(sweep + 1);  // sweeps run (diagnostics)
+  if (t == 0) work[(size_t)rows * cols + (size_t)cols * cols + cols] = (double)(sweep + 1);  // diagnostics
   // column norms
   for (int j = warp; j < cols; j += nw) {
     double s = 0.0;
