@@ -124,5 +124,11 @@ def stream(s=None):
     return s.cuda_stream
 
 
+# kernels launched by CUDA-graph replays (the C counter sees a graph's
+# launches once, at capture): krylov adds each replay's node count here
+_GRAPH_LAUNCHES = [0]
+
+
 def launch_count():
-    return int(lib().edak_launch_count())
+    """Our kernels launched so far: direct launches + graph-replayed ones."""
+    return int(lib().edak_launch_count()) + _GRAPH_LAUNCHES[0]

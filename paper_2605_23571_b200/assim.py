@@ -327,8 +327,11 @@ class Ensemble:
         self.M = self.D.shape[0]
         if traj_of is None:
             traj_of = np.arange(self.M)
-        self.traj_of = torch.as_tensor(np.asarray(traj_of), dtype=torch.int32,
-                                       device=self.D.device)
+        if isinstance(traj_of, torch.Tensor) and traj_of.device == self.D.device:
+            self.traj_of = traj_of.to(torch.int32).contiguous()  # no host round trip
+        else:
+            self.traj_of = torch.as_tensor(np.asarray(traj_of), dtype=torch.int32,
+                                           device=self.D.device)
         self.control = control  # optional (traj index, innovation row) of the control
         self.n_matvecs = 0
 
@@ -363,8 +366,9 @@ class Ensemble:
         return cls(lin, innov, traj_of)
 
     def subset(self, lo, hi):
-        """Members lo..hi-1 as an Ensemble on the same Linearization."""
-        return Ensemble(self.lin, self.D[lo:hi], self.traj_of[lo:hi].cpu().numpy())
+        """Members lo..hi-1 as an Ensemble on the same Linearization (device
+        views only: safe inside CUDA-graph capture)."""
+        return Ensemble(self.lin, self.D[lo:hi], self.traj_of[lo:hi])
 
     def rhs_all(self):
         """All members' right-hand sides, (M, n) device block (one launch)."""

@@ -254,6 +254,7 @@ def pcg(apply_h, b, cfg, precond=None, cost_fn=None):
 
 
 _SIDE_STREAMS = {}
+GRAPH_MAX_ELEMS = 1 << 20  # members x n up to which pcg_members replays a CUDA graph
 
 
 def _side_streams(count):
@@ -276,7 +277,7 @@ def _default_groups(M):
 
 
 def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fused=True,
-                groups=None, check_every=8):
+                groups=None, check_every=8, graph=None):
     """Batched PCG over all members of an ``Ensemble``: B (M, n) device
     right-hand sides (e.g. ens.rhs_all()).  cost: "recurrence", "exact" or
     None.  ``fused`` folds p.Hp into the Hessian's last pass and a
@@ -287,7 +288,16 @@ def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fu
     so the streams only share the GPU, and one group's sweeps fill the SMs
     the other leaves idle (the last partial wave of every sweep launch, the
     HBM-bound vector updates and the DMMA GEMMs).  Default: 2 for >= 64
-    members (EDAK_PCG_GROUPS overrides).  Returns (X (M, n), [SolveTrace] * M)."""
+    members (EDAK_PCG_GROUPS overrides).
+
+    ``graph`` (default: for members x n <= 2^20, when the iteration count is
+    fixed -- no residual_rtol -- and the LMP is single-pass or absent) records the whole
+    solve (init + every iteration on every group stream) as ONE CUDA graph
+    the first time an ensemble sees this shape, and replays it afterwards
+    with the new right-hand sides and LMP copied into its resident buffers:
+    no per-kernel launch cost and no inter-kernel gaps.
+    Returns (X (M, n), [SolveTrace] * M)."""
+    import os
     M = ens.M
     G = _default_groups(M) if groups is None else groups
     if snapshots is not None or M < 2:
@@ -296,7 +306,44 @@ def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fu
     apply_p = precond.apply_cols if precond is not None else None
     lmp = precond.single_pass() if (fused and precond is not None) else None
     B = B.contiguous()
+    if graph is None:
+        env = os.environ.get("EDAK_PCG_GRAPH")
+        # measured: graphs pay off where launches dominate (cfg1-3: -10..-25%
+        # per pass) and cost ~2% at cfg4 scale (two streams of long kernels)
+        graph = (env != "0") if env is not None else (B.numel() <= GRAPH_MAX_ELEMS)
+    graph = (graph and snapshots is None and cfg.residual_rtol is None and fused
+             and (precond is None or lmp is not None) and cost in ("recurrence", None))
     Z0 = apply_p(B) if apply_p is not None else B
+    if graph:
+        return _pcg_members_graph(ens, B, Z0, cfg, lmp, cost, G)
+    runs, streams = _group_runs(ens, B, Z0, cfg, apply_p, lmp, cost, G, fused)
+    main = streams[0]
+    if snapshots is not None:
+        snapshots.append(runs[0].snapshot(0))
+    rtol = runs[0].rtol
+    for it in range(1, cfg.max_iters + 1):
+        for g, run in enumerate(runs):
+            with torch.cuda.stream(streams[g]):
+                run.step(it)
+        if G > 1:
+            ens.n_matvecs += 1  # one batched member apply per iteration
+        if snapshots is not None:
+            snapshots.append(runs[0].snapshot(it))
+        if rtol >= 0.0 and it % check_every == 0:
+            for g in range(1, G):
+                main.wait_stream(streams[g])
+            if all(bool((r.status != 0).all()) for r in runs):
+                break
+    for g in range(1, G):
+        main.wait_stream(streams[g])
+    if G == 1:
+        return runs[0].X, runs[0].traces()
+    return torch.cat([r.X for r in runs], 0), [t for r in runs for t in r.traces()]
+
+
+def _group_runs(ens, B, Z0, cfg, apply_p, lmp, cost, G, fused):
+    """One _PcgRun per member group, each initialised on its own stream."""
+    M = ens.M
     bounds = [M * g // G for g in range(G + 1)]
     main = torch.cuda.current_stream()
     streams = [main] + _side_streams(G - 1)
@@ -319,29 +366,75 @@ def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fu
                 c = ("exact", sub.cost_members)
             runs.append(_PcgRun(apply_h_cols, B[lo:hi], cfg, apply_p, c,
                                 sub.lin.dot_tiles() if fused else 0, lmp, Z0[lo:hi]))
-    if snapshots is not None:
-        snapshots.append(runs[0].snapshot(0))
-    rtol = runs[0].rtol
-    for it in range(1, cfg.max_iters + 1):
-        for g, run in enumerate(runs):
-            with torch.cuda.stream(streams[g]):
-                run.step(it)
-        if G > 1:
-            ens.n_matvecs += 1  # one batched member apply per iteration
-        if snapshots is not None:
-            snapshots.append(runs[0].snapshot(it))
-        if rtol >= 0.0 and it % check_every == 0:
-            for g in range(1, G):
-                main.wait_stream(streams[g])
-            if all(bool((r.status != 0).all()) for r in runs):
-                break
-    for g in range(1, G):
-        main.wait_stream(streams[g])
-    if G == 1:
-        return runs[0].X, runs[0].traces()
-    X = torch.cat([r.X for r in runs], 0)
-    traces = [t for r in runs for t in r.traces()]
-    return X, traces
+    return runs, streams
+
+
+class _PcgGraph:
+    """A captured batched solve with its resident input buffers."""
+
+    def __init__(self, ens, B, Z0, cfg, lmp, cost, G):
+        self.B = torch.empty_like(B)
+        self.Z0 = torch.empty_like(B)
+        self.lmp = None
+        if lmp is not None:
+            self.lmp = (torch.empty_like(lmp[0]), torch.empty_like(lmp[1]))
+        self.load(B, Z0, lmp)
+        main = torch.cuda.current_stream()
+        self.cap = torch.cuda.Stream()
+        self.cap.wait_stream(main)
+        self.graph = torch.cuda.CUDAGraph()
+        n0 = int(_lib.lib().edak_launch_count())
+        # an eager warm-up on the capture stream sets every kernel's
+        # attributes (cudaFuncSetAttribute is not capturable) and allocates
+        # the group streams' pools; the capture then reuses the same buffers
+        with torch.cuda.stream(self.cap):
+            self._record(ens, cfg, cost, G)
+        self.cap.synchronize()
+        with torch.cuda.graph(self.graph, stream=self.cap):
+            self.runs = self._record(ens, cfg, cost, G)
+        self.nodes = int(_lib.lib().edak_launch_count()) - n0
+        self.nodes //= 2  # warm-up + capture
+        main.wait_stream(self.cap)
+        self.G = G
+        self.iters = cfg.max_iters
+
+    def load(self, B, Z0, lmp):
+        self.B.copy_(B)
+        self.Z0.copy_(Z0)
+        if lmp is not None:
+            self.lmp[0].copy_(lmp[0])
+            self.lmp[1].copy_(lmp[1])
+
+    def _record(self, ens, cfg, cost, G):
+        runs, streams = _group_runs(ens, self.B, self.Z0, cfg, None, self.lmp, cost, G, True)
+        for it in range(1, cfg.max_iters + 1):
+            for g, run in enumerate(runs):
+                with torch.cuda.stream(streams[g]):
+                    run.step(it)
+        cur = torch.cuda.current_stream()
+        for g in range(1, G):
+            cur.wait_stream(streams[g])
+        return runs
+
+
+def _pcg_members_graph(ens, B, Z0, cfg, lmp, cost, G):
+    key = (tuple(B.shape), cfg.max_iters, cfg.trace_cost, cost, G,
+           None if lmp is None else tuple(lmp[0].shape))
+    cache = ens.__dict__.setdefault("_pcg_graphs", {})
+    entry = cache.get(key)
+    if entry is None:
+        entry = _PcgGraph(ens, B, Z0, cfg, lmp, cost, G)
+        cache[key] = entry
+    else:
+        entry.load(B, Z0, lmp)
+    main = torch.cuda.current_stream()
+    entry.graph.replay()
+    _lib._GRAPH_LAUNCHES[0] += entry.nodes
+    ens.n_matvecs += entry.iters
+    runs = entry.runs
+    if entry.G == 1:
+        return runs[0].X.clone(), runs[0].traces()
+    return torch.cat([r.X for r in runs], 0), [t for r in runs for t in r.traces()]
 
 
 # ----------------------------------------------------------------- Lanczos --

@@ -349,3 +349,36 @@ def test_chol_inv_matches_potrf_and_inverse(gpu, l):
     Z = torch.zeros(l, l, dtype=torch.float64, device="cuda")
     assert chol_inv(Z, 0)[3].cpu().tolist()[1] == 1
     assert chol_inv(Z, 2, 0.0)[3].cpu().tolist()[1] == 1
+
+
+def test_pcg_members_graph_replay_equals_eager(gpu):
+    """The captured CUDA-graph solve (first call captures, later calls replay
+    with new right-hand sides / LMP) gives the same bits as eager launches,
+    for one and for two member groups."""
+    from paper_2605_23571_b200.assim import Ensemble
+    from paper_2605_23571_b200.krylov import SolverConfig, pcg_members
+    from paper_2605_23571_b200.lmp import make_lmp
+    from paper_2605_23571_b200.nystrom import NystromConfig, nystrom_evd
+    tw = TwinConfig(n=40, obs_grid_count=8, members=6)
+    setup = build_setup(tw, trial_seed=0)
+    mems = [_gpu_problem(m) for m in setup.members]
+    ens = Ensemble.from_members(mems)
+    ctl = _gpu_problem(setup.control)
+    B = ens.rhs_all()
+    cfg = SolverConfig(max_iters=9)
+    lmps = []
+    for k in (4, 6):
+        approx = nystrom_evd(ctl.a_apply, (B - B.mean(0)).t().cpu().numpy(),
+                             NystromConfig(ell=6, k=k, shift_mode="trace"))
+        lmps.append(make_lmp(approx, "halfsum"))
+    for groups in (1, 2):
+        for lmp in [None] + lmps[:1] + lmps[:1]:  # capture, then replay twice
+            Xe, te = pcg_members(ens, B, cfg, precond=lmp, groups=groups, graph=False)
+            Xg, tg = pcg_members(ens, B, cfg, precond=lmp, groups=groups, graph=True)
+            assert torch.equal(Xe, Xg)
+            for a, b in zip(te, tg):
+                assert a.cost == b.cost and a.resnorm == b.resnorm and a.status == b.status
+        B2 = B * 1.5
+        Xe, te = pcg_members(ens, B2, cfg, precond=lmps[0], groups=groups, graph=False)
+        Xg, tg = pcg_members(ens, B2, cfg, precond=lmps[0], groups=groups, graph=True)
+        assert torch.equal(Xe, Xg)
