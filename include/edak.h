@@ -104,6 +104,9 @@ int edak_ad_sweep(const edak_problem* P, const double* forcing, double* g,
                   int ncols, const int32_t* col_traj, double* work, void* stream);
 
 /* ---- member problem (assim.py) -------------------------------------- */
+/* Empty blocks (ncols == 0, or a zero GEMM dimension) are no-ops that return
+ * EDAK_OK without touching any pointer, like the reference's loops over zero
+ * columns. */
 /* workspace (doubles) needed by edak_hessian_block / edak_rhs / edak_cost */
 int64_t edak_work_doubles(const edak_problem* P, int ncols);
 /* az[c] = ident * z[c] + A_traj(c) z[c],  A = U_B^T G^T R^-1 G U_B

@@ -141,6 +141,7 @@ static int tn_nsplit(int m, int nb, int64_t K, int64_t& kslice) {
 }
 
 int64_t gemm_tn_partials(int m, int nb, int64_t K) {
+  if (m < 1 || nb < 1 || K < 1) return 0;  // empty block: no partials
   int64_t ks;
   return (int64_t)tn_nsplit(m, nb, K, ks) * m * nb;
 }

@@ -85,25 +85,25 @@ int64_t edak_launch_count(void) { return g_launches.load(); }
 
 int edak_integrate(int n, int n_steps, double dt, double forcing, const double* x0, int ncols, double* states_out,
                    int64_t out_stride, double* stages_out, int64_t stg_stride, void* stream) {
+  if (ncols == 0) return EDAK_OK;
   if (n < 8 || n_steps < 0 || ncols < 0 || !x0 || !states_out || out_stride < (int64_t)(n_steps + 1) * n) {
     set_error("edak_integrate: bad arguments");
     return EDAK_EINVAL;
   }
-  if (ncols == 0) return EDAK_OK;
   return launch_integrate(n, n_steps, dt, forcing, x0, ncols, states_out, out_stride, stages_out, stg_stride,
                           as_stream(stream));
 }
 
 int edak_observe(const double* states, int64_t traj_stride, int n, const int32_t* grid, int G, const int32_t* times,
                  int T, int ncols, double* y, void* stream) {
-  if (!states || !grid || !times || !y || n < 1) return EDAK_EINVAL;
   if (ncols == 0 || G * T == 0) return EDAK_OK;
+  if (!states || !grid || !times || !y || n < 1) return EDAK_EINVAL;
   return launch_observe(states, traj_stride, n, grid, G, times, T, ncols, y, as_stream(stream));
 }
 
 int edak_circ_apply(const edak_problem* P, const double* in, double* out, int ncols, void* stream) {
-  if (!P || !P->taps || !in || !out) return EDAK_EINVAL;
   if (ncols == 0) return EDAK_OK;
+  if (!P || !P->taps || !in || !out) return EDAK_EINVAL;
   return launch_circ(P, in, out, ncols, 0.0, nullptr, as_stream(stream));
 }
 
@@ -114,15 +114,15 @@ int64_t edak_sweep_work_doubles(const edak_problem* P, int ncols) {
 
 int edak_tl_sweep(const edak_problem* P, const double* v0, double* obs, int ncols, const int32_t* col_traj,
                   double* work, void* stream) {
-  if (bad_problem(P) || !v0 || !obs) return EDAK_EINVAL;
   if (ncols == 0) return EDAK_OK;
+  if (bad_problem(P) || !v0 || !obs) return EDAK_EINVAL;
   return launch_tl(P, v0, obs, ncols, col_traj, as_stream(stream), work);
 }
 
 int edak_ad_sweep(const edak_problem* P, const double* forcing, double* g, int ncols, const int32_t* col_traj,
                   double* work, void* stream) {
-  if (bad_problem(P) || !forcing || !g) return EDAK_EINVAL;
   if (ncols == 0) return EDAK_OK;
+  if (bad_problem(P) || !forcing || !g) return EDAK_EINVAL;
   return launch_ad(P, forcing, g, ncols, col_traj, as_stream(stream), work);
 }
 
@@ -136,12 +136,12 @@ int64_t edak_hessian_dot_tiles(int n) { return circ_tiles(n); }
 
 int edak_hessian_block(const edak_problem* P, const double* z, double* az, int ncols, const int32_t* col_traj,
                        double ident, double* work, double* obs_out, double* dot_part, void* stream) {
-  if (bad_problem(P) || !z || !az || !work) return EDAK_EINVAL;
   if (dot_part && ident == 0.0) {
     set_error("edak_hessian_block: dot_part needs ident != 0 (p.Hp of the I + A apply)");
     return EDAK_EINVAL;
   }
   if (ncols == 0) return EDAK_OK;
+  if (bad_problem(P) || !z || !az || !work) return EDAK_EINVAL;
   cudaStream_t st = as_stream(stream);
   const int64_t n = P->n, p = (int64_t)P->G * P->T;
   double* v0 = work;
@@ -158,8 +158,8 @@ int edak_hessian_block(const edak_problem* P, const double* z, double* az, int n
 
 int edak_rhs(const edak_problem* P, const double* innov, double* b, int ncols, const int32_t* col_traj, double* work,
              void* stream) {
-  if (bad_problem(P) || !innov || !b || !work) return EDAK_EINVAL;
   if (ncols == 0) return EDAK_OK;
+  if (bad_problem(P) || !innov || !b || !work) return EDAK_EINVAL;
   cudaStream_t st = as_stream(stream);
   int rc;
   if ((rc = launch_ad(P, innov, work, ncols, col_traj, st, work + (size_t)ncols * P->n))) return rc;
@@ -168,8 +168,8 @@ int edak_rhs(const edak_problem* P, const double* innov, double* b, int ncols, c
 
 int edak_cost(const edak_problem* P, const double* z, const double* innov, double* J, int ncols,
               const int32_t* col_traj, double* work, void* stream) {
-  if (bad_problem(P) || !z || !innov || !J || !work) return EDAK_EINVAL;
   if (ncols == 0) return EDAK_OK;
+  if (bad_problem(P) || !z || !innov || !J || !work) return EDAK_EINVAL;
   cudaStream_t st = as_stream(stream);
   const int64_t n = P->n;
   const int p = P->G * P->T;
@@ -186,13 +186,15 @@ int64_t edak_gemm_tn_partials(int m, int nb, int64_t K) { return gemm_tn_partial
 
 int edak_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int ldc, int m, int nb,
                  int64_t K, double* partial, void* stream) {
-  if (!A || !B || !C || !partial || m < 1 || nb < 1 || K < 1) return EDAK_EINVAL;
+  if (m == 0 || nb == 0) return EDAK_OK;  // empty block
+  if (!A || !B || !C || !partial || m < 0 || nb < 0 || K < 1) return EDAK_EINVAL;
   return launch_gemm_tn(A, lda, B, ldb, C, ldc, m, nb, K, partial, as_stream(stream));
 }
 
 int edak_gemm_nn(const double* A, int64_t lda, const double* B, int ldb, const double* bscale, const double* Cin,
                  int64_t ldc, double beta, double* D, int64_t ldd, int64_t M, int N, int kk, void* stream) {
-  if (!A || !B || !D || M < 1 || N < 1 || kk < 1) return EDAK_EINVAL;
+  if (M == 0 || N == 0) return EDAK_OK;  // empty block
+  if (!A || !B || !D || M < 0 || N < 0 || kk < 1) return EDAK_EINVAL;
   return launch_gemm_nn(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M, N, kk, as_stream(stream));
 }
 
@@ -277,8 +279,8 @@ int64_t edak_lmp_work_doubles(int n, int k, int ncols) {
 
 int edak_lmp_apply(int n, int k, int ncols, const double* S, const double* coef, const double* r, double* z,
                    double* work, void* stream) {
-  if (!S || !coef || !r || !z || !work || n < 1 || k < 1) return EDAK_EINVAL;
   if (ncols == 0) return EDAK_OK;
+  if (!S || !coef || !r || !z || !work || n < 1 || k < 1) return EDAK_EINVAL;
   cudaStream_t st = as_stream(stream);
   double* W = work;
   double* part = work + (int64_t)k * ncols;
@@ -289,8 +291,8 @@ int edak_lmp_apply(int n, int k, int ncols, const double* S, const double* coef,
 }
 
 int edak_col_dots(int n, int ncols, const double* a, const double* b, double* out, void* stream) {
-  if (!a || !b || !out) return EDAK_EINVAL;
   if (ncols == 0) return EDAK_OK;
+  if (!a || !b || !out) return EDAK_EINVAL;
   return launch_col_dots(n, ncols, a, b, out, as_stream(stream));
 }
 
