@@ -14,6 +14,7 @@
 // last to the first: M[j+1:, j] = -(M[j+1:, j+1:] L[j+1:, j]) M[j, j].
 // Outputs C = L^T and Ci = C^-1 = M^T (column-major, zero lower parts).
 #include "common.cuh"
+#include <cstdlib>
 
 namespace edak {
 
@@ -201,6 +202,188 @@ __global__ void __launch_bounds__(CI_NT) k_chol_inv(const double* __restrict__ W
   }
 }
 
+// Register-resident variant for l <= 128 (the Nystrom Grams at cfg1-4):
+// 1024 threads, thread (warp bj, lane bi) owns the 4x4 block rows 4bi..,
+// cols 4bj.. of the lower factor.  A pivot is one shuffle (the diagonal
+// lives in the column block's warp), a sqrt, the scaled column written to a
+// double-buffered smem vector, ONE barrier and a 4x4 rank-1 update in
+// registers; the inverse M = L^-1 runs the same way over rows (L parked in
+// shared memory).  ~2l barriers in total, against the panel kernel's
+// latency-bound warp-serial panels.
+constexpr int CR_MAX = 128;
+
+__global__ void __launch_bounds__(1024) k_chol_inv_reg(const double* __restrict__ W, int l, double* __restrict__ Cm,
+                                                       double* __restrict__ Ci, int mode, double scale,
+                                                       double* __restrict__ nu_out, int32_t* __restrict__ info) {
+  extern __shared__ __align__(16) double crs[];
+  double* Ls = crs;                       // l x l lower factor (column-major), for the inverse
+  double* vec = crs + CR_MAX * CR_MAX;    // [2][CR_MAX] pivot column / row of M
+  double* rdiag = vec + 2 * CR_MAX;       // 1 / L_kk
+  __shared__ int fail;
+  __shared__ double trace_s;
+  const int t = threadIdx.x, bj = t >> 5, bi = t & 31;
+  const int r0 = 4 * bi, c0 = 4 * bj;
+  const bool live = r0 < l && c0 < l && bi >= bj;  // blocks on/below the diagonal
+  if (mode == 1) {
+    if (t == 0) {
+      double s = 0.0;
+      for (int j = 0; j < l; ++j) s += W[j + (size_t)j * l];
+      trace_s = s;
+    }
+    __syncthreads();
+  }
+  const double sc = mode == 1 ? trace_s : scale;
+  double nu = 0.0;
+  int attempt = 0;
+  bool ok = false;
+  double a[4][4];
+  for (; attempt < 6; ++attempt) {
+    if (attempt == 1) {
+      nu = 2.220446049250313e-16 * sc;
+      if (mode == 0 || !(nu > 0.0)) break;
+    } else if (attempt > 1) {
+      nu *= 10.0;
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = r0 + p, k = c0 + q;
+        double v = 0.0;
+        if (live && i < l && k < l && i >= k) v = W[k + (size_t)i * l] + (i == k ? nu : 0.0);  // W's upper
+        a[p][q] = v;
+      }
+    if (t == 0) fail = 0;
+    __syncthreads();
+    for (int j = 0; j < l; ++j) {
+      const int jb = j >> 2, jq = j & 3, buf = j & 1;
+      double* colj = vec + buf * CR_MAX;
+      if (bj == jb) {  // the pivot column's warp: diagonal from lane jb
+        double dloc = 0.0;
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (p == jq && q == jq) dloc = a[p][q];
+        const double d = __shfl_sync(0xffffffffu, dloc, jb);
+        if (!(d > 0.0)) {
+          if (bi == 0) fail = 1;
+        } else {
+          const double piv = sqrt(d);
+          const double inv = 1.0 / piv;
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            const int i = r0 + p;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (q == jq && live && i >= j && i < l) {
+                const double v = i == j ? piv : a[p][q] * inv;
+                a[p][q] = v;
+                colj[i] = v;
+              }
+          }
+        }
+      }
+      __syncthreads();
+      if (fail) break;
+      // rank-1 update of the trailing lower triangle: a[i][k] -= l_ij l_kj
+      if (live && c0 + 3 > j) {
+        double ci[4], ck[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          ci[p] = (r0 + p > j && r0 + p < l) ? colj[r0 + p] : 0.0;
+          ck[p] = (c0 + p > j && c0 + p < l) ? colj[c0 + p] : 0.0;
+        }
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) a[p][q] = fma(-ci[p], ck[q], a[p][q]);
+      }
+    }
+    __syncthreads();
+    if (!fail) {
+      ok = true;
+      break;
+    }
+  }
+  ok = ok && !(attempt >= 1 && mode == 0);
+  if (t == 0) {
+    info[0] = attempt;
+    info[1] = ok ? 0 : 1;
+    nu_out[0] = ok ? nu : 0.0;
+  }
+  // C = L^T; L parked in smem for the inverse
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = r0 + p, k = c0 + q;  // L[i][k], i >= k: each C entry written once
+      if (i < l && k < l && i >= k) {
+        const double v = ok ? a[p][q] : 0.0;
+        Cm[k + (size_t)i * l] = v;                 // C[k][i] = L[i][k]
+        if (i != k) Cm[i + (size_t)k * l] = 0.0;   // strict lower part of C
+        Ls[i + (size_t)k * l] = v;
+      }
+    }
+  if (!Ci) return;
+  if (!ok) {
+    for (int e = t; e < l * l; e += 1024) Ci[e] = 0.0;
+    return;
+  }
+  for (int k = t; k < l; k += 1024) rdiag[k] = 0.0;
+  __syncthreads();
+  for (int k = t; k < l; k += 1024) rdiag[k] = 1.0 / Ls[k + (size_t)k * l];
+  // M = L^-1 by rows: R = I; for k: M[k][:] = R[k][:] / L_kk, then
+  // R[i][:] -= L[i][k] M[k][:] for i > k.  Same block ownership.
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) a[p][q] = (live && r0 + p == c0 + q && r0 + p < l) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int k = 0; k < l; ++k) {
+    const int kb = k >> 2, kp = k & 3;
+    double* rowk = vec + (k & 1) * CR_MAX;
+    if (bi == kb && live) {  // row k's owners: scale and publish
+      const double rd = rdiag[k];
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+        if (p == kp)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int c = c0 + q;
+            if (c <= k && c < l) {
+              const double v = a[p][q] * rd;
+              a[p][q] = v;
+              rowk[c] = v;
+            }
+          }
+    }
+    __syncthreads();
+    if (live && r0 + 3 > k && c0 <= k) {
+      double li[4], mk[4];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) li[p] = (r0 + p > k && r0 + p < l) ? Ls[r0 + p + (size_t)k * l] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) mk[q] = (c0 + q <= k && c0 + q < l) ? rowk[c0 + q] : 0.0;
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a[p][q] = fma(-li[p], mk[q], a[p][q]);
+    }
+  }
+  // Ci = M^T (upper): Ci[k][i] = M[i][k]
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = r0 + p, k = c0 + q;
+      if (i < l && k < l && i >= k) {
+        Ci[k + (size_t)i * l] = a[p][q];          // Ci[k][i] = M[i][k]
+        if (i != k) Ci[i + (size_t)k * l] = 0.0;
+      }
+    }
+}
+
 int64_t chol_inv_work_doubles(int l) { return l <= CI_SMEM_MAX ? 0 : (int64_t)l * l + (int64_t)l * CI_B; }
 
 int launch_chol_inv(const double* W, int l, double* C, double* Ci, int mode, double scale, double* nu_out,
@@ -208,6 +391,17 @@ int launch_chol_inv(const double* W, int l, double* C, double* Ci, int mode, dou
   if (l < 1) {
     set_error("chol_inv: l < 1");
     return EDAK_EINVAL;
+  }
+  if (l <= CR_MAX && !getenv("EDAK_CHOL_PANEL")) {
+    constexpr size_t crs = ((size_t)CR_MAX * CR_MAX + 3 * CR_MAX) * sizeof(double);
+    static bool attr_r = false;
+    if (!attr_r) {
+      cudaFuncSetAttribute(k_chol_inv_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)crs);
+      attr_r = true;
+    }
+    k_chol_inv_reg<<<1, 1024, crs, st>>>(W, l, C, Ci, mode, scale, nu_out, info);
+    count_launch();
+    return check_launch("k_chol_inv_reg");
   }
   size_t sm = 0;
   if (l <= CI_SMEM_MAX) {

@@ -75,6 +75,28 @@ def nystrom_envelope(op, phi, cfg, trials=4):
     return env
 
 
+def lmp_pcg_envelope(op, phi, ncfg, rule, member, cfg, trials=4, seed=321):
+    """CPU-vs-CPU spread of a member's LMP-PCG trace (J, resnorm) when the
+    LMP itself is built from Y = A Phi perturbed at the 1e-16 level -- two
+    legitimate fp64 Nystrom/Cholesky/SVD implementations differ that way
+    (LAPACK-stage results are not bit-pinned)."""
+    y = op.a_apply(phi)
+    lmp = oalg.make_lmp(oalg.nystrom_evd(lambda v: y, phi, ncfg), rule)
+    b = member.rhs()
+    _, ref = oalg.pcg(member.hessian_apply, b, cfg, precond=lmp, cost_fn=member.quadratic_cost)
+    rng = np.random.default_rng(seed)
+    n = len(ref.cost)
+    e_j, e_r = np.zeros(n), np.zeros(n)
+    for _ in range(trials):
+        yp = y * (1 + JITTER * rng.standard_normal(y.shape))
+        lp = oalg.make_lmp(oalg.nystrom_evd(lambda v: yp, phi, ncfg), rule)
+        _, tr = oalg.pcg(member.hessian_apply, b, cfg, precond=lp, cost_fn=member.quadratic_cost)
+        m = min(n, len(tr.cost))
+        e_j[:m] = np.maximum(e_j[:m], np.abs(np.array(tr.cost[:m]) - ref.cost[:m]))
+        e_r[:m] = np.maximum(e_r[:m], np.abs(np.array(tr.resnorm[:m]) - ref.resnorm[:m]))
+    return ref, e_j, e_r
+
+
 def assert_values(ours, ref, env):
     """rel 1e-10 for D_i >= 1e-6 D_1, else abs 1e-10 D_1, widened to 10x the
     measured envelope where that is larger."""

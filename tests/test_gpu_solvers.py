@@ -11,7 +11,7 @@ import pytest
 import torch
 
 from conftest import GOLDEN, unpack_problem
-from parity import assert_trace, assert_values, nystrom_envelope, pcg_envelope
+from parity import lmp_pcg_envelope, assert_trace, assert_values, nystrom_envelope, pcg_envelope
 from oracle import algorithms as oalg
 from oracle.twin import TwinConfig, build_setup
 
@@ -195,7 +195,10 @@ def test_pcg_reference_fixtures(gpu):
 
 def test_cfg1_lmp_pcg_golden(gpu, ref_problem):
     """cfg1: Nystrom on Gamma (shared linearization) + halfsum LMP + 30 PCG
-    iterations for three members: J rel 1e-10, resnorm 1e-10 r0."""
+    iterations for three members against the reference's golden traces: J
+    rel 1e-10; resnorm 1e-10 r0, or 10x the spread the trace shows on the CPU
+    when its LMP is built from Y perturbed at 1e-16 (tests/parity.py
+    lmp_pcg_envelope: late residuals amplify LMP rounding ~1e4-fold)."""
     from paper_2605_23571_b200.krylov import SolverConfig, pcg
     from paper_2605_23571_b200.lmp import make_lmp
     from paper_2605_23571_b200.nystrom import NystromConfig, nystrom_evd
@@ -212,8 +215,12 @@ def test_cfg1_lmp_pcg_golden(gpu, ref_problem):
         _, tr = pcg(m.hessian_apply, m.rhs(), SolverConfig(max_iters=30), precond=lmp,
                     cost_fn=m.quadratic_cost)
         npt.assert_allclose(tr.cost, g[f"cfg1_m{j}_cost"], rtol=1e-10)
-        r0 = g[f"cfg1_m{j}_resnorm"][0]
-        assert np.max(np.abs(np.array(tr.resnorm) - g[f"cfg1_m{j}_resnorm"])) <= 1e-10 * r0
+        ref = np.asarray(g[f"cfg1_m{j}_resnorm"])
+        _, _, env_r = lmp_pcg_envelope(st.control, g["cfg1_gamma"],
+                                       oalg.NystromConfig(10, 10, shift_mode="trace"), "halfsum",
+                                       st.members[j], oalg.SolverConfig(max_iters=30))
+        tol = np.maximum(1e-10 * ref[0], 10 * env_r)
+        assert np.all(np.abs(np.array(tr.resnorm) - ref) <= tol)
 
 
 def test_pcg_members_batched_equals_single(gpu):
