@@ -269,3 +269,55 @@ def test_model_obs_dropins_and_device_setup(gpu):
     from oracle.streams import substream as osub
     np.testing.assert_array_equal(gm.spinup(40, 0.025, 8.0, 100, osub(1, "spinup")),
                                   ol96.spinup(40, 0.025, 8.0, 100, osub(1, "spinup")))
+
+
+def _random_case(seed):
+    """A seeded random window operator: ring size across every sweep family
+    (periodic C = 2/4/8 single tiles, tile mode with wrap, odd and even n),
+    window length across the chunking threshold, arbitrary (non-strided)
+    observed grids and time lists including levels 0 and N, sigma_o != 1,
+    diffusion or Gaussian B."""
+    from oracle.cov import diffusion_factor as o_diff
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.choice([12, 26, 40, 64, 100, 130, 512, 1000, 1030, 2050, 4101, 6000, 9000]))
+    N = int(rng.integers(1, 30))
+    G = int(rng.integers(1, max(2, n // 3)))
+    grid = np.sort(rng.choice(n, size=G, replace=False))
+    T = int(rng.integers(1, N + 2))
+    times = np.sort(rng.choice(N + 1, size=T, replace=False))
+    x0 = 8.0 + 3.0 * rng.standard_normal(n)
+    x0 = ol96.integrate(x0, 0.025, 40, 8.0).states[-1]
+    traj = ol96.integrate(x0, 0.025, N, 8.0)
+    net = OObs(grid, times)
+    sig = float(rng.choice([0.05, 1.0, 2.5]))
+    if rng.random() < 0.5:
+        ub = o_gaussian(n, 0.8, float(rng.choice([1.5, 3.0, 6.0])))
+    else:
+        ub = o_diff(n, 0.8, float(rng.choice([2.0, 6.0])), int(rng.choice([2, 10])))
+    d = rng.standard_normal(net.p)
+    return OProblem(traj, net, ub, ONoise(sig), d), rng
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_randomized_window_operators(gpu, seed):
+    """Fuzzed parity: A block (3 columns), I + A, rhs and J against the
+    oracle at rel 1e-12 across random geometries (see _random_case)."""
+    from paper_2605_23571_b200.assim import MemberProblem
+    from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
+    from paper_2605_23571_b200.covariance import factor_taps
+    op, rng = _random_case(seed)
+    n = op.traj.n
+    try:
+        factor_taps(op.ub)
+    except ValueError:
+        pytest.skip("factor needs more taps than the kernel takes")
+    prob = MemberProblem(op.traj, op.net, CirculantFactor(n, op.ub.symbol),
+                         DiagonalNoise(op.rn.sigma), op.innovation)
+    z = rng.standard_normal((n, 3))
+    az, ref = prob.a_apply(z), op.a_apply(z)
+    for j in range(3):
+        assert rel(az[:, j], ref[:, j]) < 1e-12, (n, op.traj.n_steps, j)
+    hz = prob.hessian_apply(z[:, 0])
+    assert rel(hz, z[:, 0] + ref[:, 0]) < 1e-12
+    assert rel(prob.rhs(), op.rhs()) < 1e-12
+    assert prob.quadratic_cost(z[:, 1]) == pytest.approx(op.quadratic_cost(z[:, 1]), rel=1e-12)
