@@ -1,0 +1,243 @@
+// One-sided (Hestenes) Jacobi SVD of the (l x l) Nystrom matrix T on a
+// thread-block cluster of 8 CTAs (8 SMs) instead of one CTA
+// (nystrom.py:130 np.linalg.svd; the single-CTA k_svd_jacobi is bound by one
+// SM's issue rate and shared-memory bandwidth: ~2.4 us per round at l = 128).
+//
+// Column pairs follow the same round-robin tournament as k_svd_jacobi.  Pair
+// k lives in registers of a half-warp (16 lanes x RPL rows per lane); pairs
+// are spread over the cluster's CTAs.  A round is: one dot (+ 4 shuffles),
+// the rotation from lane 0's sums (tracked column norms), the rotation in
+// registers, then each pair publishes its two columns in its own CTA's
+// double-buffered slot, ONE cluster barrier, and each pair pulls its next
+// columns from the neighbouring pairs' slots -- through distributed shared
+// memory when the neighbour sits on another SM.  Outputs as k_svd_jacobi:
+// U (unit columns, descending sigma), sig.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace edak {
+
+constexpr int JC_CL = 8;           // CTAs per cluster (portable size)
+constexpr int JC_MAXROWS = 256;    // rows <= 256 -> <= 16 rows per lane
+constexpr int JC_RPL = JC_MAXROWS / 16;
+
+__device__ __forceinline__ double jc_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// smem per CTA: slots [2 buf][ppc][2 (p, q)][rows] + meta [2][ppc][4]
+__global__ void __cluster_dims__(JC_CL, 1, 1) __launch_bounds__(256)
+    k_svd_jacobi_cluster(const double* __restrict__ M, int rows, int cols, int ppc, double* __restrict__ U,
+                         double* __restrict__ sig, double* __restrict__ work) {
+  extern __shared__ __align__(16) double jcs[];
+  __shared__ int rot_flag;
+  __shared__ int stop_all;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int t = threadIdx.x, hl = t & 15, lp = t >> 4;  // local pair
+  const int m = cols + (cols & 1), np = m / 2;
+  const int k = rank * ppc + lp;                        // global pair index
+  const bool act = lp < ppc && k < np;
+  const size_t slot_sz = (size_t)rows;
+  double* slots = jcs;                                  // [2][ppc][2][rows]
+  double* meta = jcs + 2 * (size_t)ppc * 2 * rows;      // [2][ppc][4]: idp, nrm_p, idq, nrm_q
+  const double tol2 = (double)rows * 2.220446049250313e-16 * 2.220446049250313e-16;
+  const int src = (t & 31) & 16;                        // lane 0 of this half-warp
+  auto hsum = [&](double v) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return __shfl_sync(0xffffffffu, v, src);
+  };
+  int idp = k, idq = m - 1 - k;
+  double xp[JC_RPL], xq[JC_RPL];
+#pragma unroll
+  for (int r = 0; r < JC_RPL; ++r) {
+    const int i = hl + 16 * r;
+    xp[r] = (act && i < rows && idp < cols) ? M[i + (size_t)idp * rows] : 0.0;
+    xq[r] = (act && i < rows && idq < cols) ? M[i + (size_t)idq * rows] : 0.0;
+  }
+  // where pair kk's slot lives: CTA kk / ppc, local kk % ppc
+  auto slot_of = [&](int buf, int kk, int which) -> double* {
+    double* local = slots + (((size_t)buf * ppc + (kk % ppc)) * 2 + which) * slot_sz;
+    return cluster.map_shared_rank(local, kk / ppc);
+  };
+  auto meta_of = [&](int buf, int kk) -> double* {
+    double* local = meta + ((size_t)buf * ppc + (kk % ppc)) * 4;
+    return cluster.map_shared_rank(local, kk / ppc);
+  };
+  int buf = 0, sweep = 0;
+  for (; sweep < 40; ++sweep) {
+    double al = 0.0, be = 0.0;
+#pragma unroll
+    for (int r = 0; r < JC_RPL; ++r) {
+      al = fma(xp[r], xp[r], al);
+      be = fma(xq[r], xq[r], be);
+    }
+    al = hsum(al);
+    be = hsum(be);
+    if (t == 0) rot_flag = 0;
+    __syncthreads();
+    for (int rd = 0; rd < m - 1; ++rd) {
+      double ga = 0.0;
+#pragma unroll
+      for (int r = 0; r < JC_RPL; ++r) ga = fma(xp[r], xq[r], ga);
+      ga = hsum(ga);
+      if (act && al > 0.0 && be > 0.0 && ga * ga > tol2 * (al * be)) {
+        const double zeta = (be - al) * jc_rcp(2.0 * ga);
+        const double z2 = fma(zeta, zeta, 1.0);
+        const double tt = copysign(jc_rcp(fabs(zeta) + z2 * rsqrt(z2)), zeta);
+        const double c = rsqrt(fma(tt, tt, 1.0)), sn = c * tt;
+#pragma unroll
+        for (int r = 0; r < JC_RPL; ++r) {
+          const double x = xp[r], y = xq[r];
+          xp[r] = c * x - sn * y;
+          xq[r] = sn * x + c * y;
+        }
+        al = fma(-tt, ga, al);
+        be = fma(tt, ga, be);
+        if (hl == 0) rot_flag = 1;
+      }
+      // publish own columns (local slots), one cluster barrier, pull the next
+      if (act) {
+        double* sp = slots + (((size_t)buf * ppc + lp) * 2 + 0) * slot_sz;
+        double* sq = slots + (((size_t)buf * ppc + lp) * 2 + 1) * slot_sz;
+#pragma unroll
+        for (int r = 0; r < JC_RPL; ++r) {
+          const int i = hl + 16 * r;
+          if (i < rows) {
+            sp[i] = xp[r];
+            sq[i] = xq[r];
+          }
+        }
+        if (hl == 0) {
+          double* mt = meta + ((size_t)buf * ppc + lp) * 4;
+          mt[0] = (double)idp;
+          mt[1] = al;
+          mt[2] = (double)idq;
+          mt[3] = be;
+        }
+      }
+      cluster.sync();
+      if (act) {
+        // new p(k) = p(k+1) (1 <= k < np-1); new p(np-1) = q(np-1); p(0) stays
+        // new q(k) = q(k-1) (k >= 1);        new q(0) = p(1)
+        const bool last = k == np - 1;
+        if (k >= 1) {
+          if (last) {
+#pragma unroll
+            for (int r = 0; r < JC_RPL; ++r) xp[r] = xq[r];
+            idp = idq;
+            al = be;
+          } else {
+            const double* rp = slot_of(buf, k + 1, 0);
+            const double* mt = meta_of(buf, k + 1);
+#pragma unroll
+            for (int r = 0; r < JC_RPL; ++r) {
+              const int i = hl + 16 * r;
+              xp[r] = i < rows ? rp[i] : 0.0;
+            }
+            idp = (int)mt[0];
+            al = mt[1];
+          }
+          const double* rq = slot_of(buf, k - 1, 1);
+          const double* mq = meta_of(buf, k - 1);
+#pragma unroll
+          for (int r = 0; r < JC_RPL; ++r) {
+            const int i = hl + 16 * r;
+            xq[r] = i < rows ? rq[i] : 0.0;
+          }
+          idq = (int)mq[2];
+          be = mq[3];
+        } else if (np > 1) {
+          const double* rp = slot_of(buf, 1, 0);
+          const double* mt = meta_of(buf, 1);
+#pragma unroll
+          for (int r = 0; r < JC_RPL; ++r) {
+            const int i = hl + 16 * r;
+            xq[r] = i < rows ? rp[i] : 0.0;
+          }
+          idq = (int)mt[0];
+          be = mt[1];
+        }
+      }
+      buf ^= 1;
+    }
+    // any rotation anywhere in the cluster this sweep?
+    cluster.sync();
+    if (t == 0) {
+      int any = 0;
+      for (int c = 0; c < JC_CL; ++c) any |= *cluster.map_shared_rank(&rot_flag, c);
+      stop_all = !any;
+    }
+    cluster.sync();  // every CTA has read every flag before they are reset
+    if (stop_all) break;
+  }
+  // columns back to the workspace by id; CTA 0 ranks and scatters
+  double* A = work;
+  double* nrm = work + (size_t)rows * cols;
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < JC_RPL; ++r) {
+      const int i = hl + 16 * r;
+      if (i < rows) {
+        if (idp < cols) A[i + (size_t)idp * rows] = xp[r];
+        if (idq < cols) A[i + (size_t)idq * rows] = xq[r];
+      }
+    }
+  }
+  if (rank == 0 && t == 0) work[(size_t)rows * cols + (size_t)cols * cols + cols] = (double)(sweep + 1);
+  __threadfence();
+  cluster.sync();
+  if (rank != 0) return;
+  const int lane = t & 31, warp = t >> 5, nw = 256 / 32;
+  for (int j = warp; j < cols; j += nw) {
+    double s = 0.0;
+    const double* a = A + (size_t)j * rows;
+    for (int i = lane; i < rows; i += 32) s += a[i] * a[i];
+    s = warp_sum(s);
+    if (lane == 0) nrm[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = warp; j < cols; j += nw) {
+    const double sj = nrm[j];
+    int rk = 0;
+    for (int i = lane; i < cols; i += 32) {
+      const double si = nrm[i];
+      rk += (si > sj || (si == sj && i < j)) ? 1 : 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) rk += __shfl_xor_sync(0xffffffffu, rk, o);
+    const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
+    const double* a = A + (size_t)j * rows;
+    double* u = U + (size_t)rk * rows;
+    for (int i = lane; i < rows; i += 32) u[i] = a[i] * inv;
+    if (lane == 0) sig[rk] = sj;
+  }
+}
+
+// returns -1 when the shape is not handled by the cluster kernel
+int launch_svd_jacobi_cluster(const double* M, int rows, int cols, double* U, double* sig, double* work,
+                              cudaStream_t st) {
+  if (rows > JC_MAXROWS || cols > rows || cols < 2) return -1;
+  const int m = cols + (cols & 1), np = m / 2;
+  const int ppc = (np + JC_CL - 1) / JC_CL;
+  if (ppc * 16 > 256) return -1;
+  const size_t smem = (2 * (size_t)ppc * 2 * rows + 2 * (size_t)ppc * 4) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_svd_jacobi_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_svd_jacobi_cluster<<<JC_CL, 256, smem, st>>>(M, rows, cols, ppc, U, sig, work);
+  count_launch();
+  return check_launch("k_svd_jacobi_cluster");
+}
+
+}  // namespace edak

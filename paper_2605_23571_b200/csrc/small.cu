@@ -4,6 +4,7 @@
 //   k_trinv_upper   : explicit inverse of an upper-triangular factor
 //   k_svd_jacobi    : one-sided (Hestenes) Jacobi SVD, descending order
 #include "common.cuh"
+#include <cstdlib>
 
 namespace edak {
 
@@ -381,6 +382,8 @@ __global__ void __launch_bounds__(JAC_NT) k_svd_jacobi(const double* __restrict_
   }
 }
 
+int launch_svd_jacobi_cluster(const double*, int, int, double*, double*, double*, cudaStream_t);
+
 int64_t svd_work_doubles(int rows, int cols) { return (int64_t)rows * cols + (int64_t)cols * cols + cols + 1; }
 
 int launch_svd_jacobi(const double* M, int rows, int cols, double* U, double* sig, double* V, double* work,
@@ -405,6 +408,10 @@ int launch_svd_jacobi(const double* M, int rows, int cols, double* U, double* si
   if (!attr) {
     cudaFuncSetAttribute(k_svd_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
     attr = true;
+  }
+  if (!V && !getenv("EDAK_JACOBI_SINGLE")) {  // 8-SM cluster variant (jacobi_cluster.cu)
+    const int rc = launch_svd_jacobi_cluster(M, rows, cols, U, sig, work, st);
+    if (rc >= 0) return rc;
   }
   k_svd_jacobi<<<1, JAC_NT, smem, st>>>(M, rows, cols, U, sig, V, work, mode);
   count_launch();
