@@ -27,6 +27,15 @@ __device__ __forceinline__ double l96_f(double xp1, double xm2, double xm1,
   return __dadd_rn(__dsub_rn(__dmul_rn(__dsub_rn(xp1, xm2), xm1), x0), F);
 #endif
 }
+// the same with the difference x[i+1] - x[i-2] supplied (shared with the TL
+// of that stage: the compiler does not CSE __dsub_rn against a plain '-')
+__device__ __forceinline__ double l96_f_d(double d, double xm1, double x0, double F) {
+#ifdef EDAK_EXP_FMA
+  return fma(d, xm1, -x0) + F;
+#else
+  return __dadd_rn(__dsub_rn(__dmul_rn(d, xm1), x0), F);
+#endif
+}
 // stage update x + c*k (model.py:41,43,45): rounded product then sum
 __device__ __forceinline__ double axpy_rn(double x, double c, double k) {
 #ifdef EDAK_EXP_FMA
@@ -46,6 +55,10 @@ __device__ __forceinline__ double l96_tl(double vp1, double vm2, double vm1,
 }
 // tendency_adj (model.py:31-35):
 //   x[i-2] w[i-1] + (x[i+2] - x[i-1]) w[i+1] - x[i+1] w[i+2] - w[i]
+// TL tendency with the state difference d = x[i+1] - x[i-2] supplied
+__device__ __forceinline__ double l96_tl_d(double vp1, double vm2, double vm1, double v0, double d, double xm1) {
+  return fma(vp1 - vm2, xm1, fma(d, vm1, -v0));
+}
 __device__ __forceinline__ double l96_ad(double xm2, double xm1, double xp1,
                                          double xp2, double wm1, double w0,
                                          double wp1, double wp2) {

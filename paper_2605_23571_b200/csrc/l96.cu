@@ -108,6 +108,13 @@ __device__ __forceinline__ void tl_sub(const double (&u)[C + 4], const double (&
   for (int j = 0; j < C; ++j)
     a[j] = l96_tl(u[j + 3], u[j], u[j + 1], u[j + 2], x[j + 3], x[j], x[j + 1]);
 }
+// the same with the stage's differences d[j] = x[j+3] - x[j] precomputed
+template <int C>
+__device__ __forceinline__ void tl_sub_d(const double (&u)[C + 4], const double (&x)[C + 4], const double (&d)[C],
+                                         double (&a)[C]) {
+#pragma unroll
+  for (int j = 0; j < C; ++j) a[j] = l96_tl_d(u[j + 3], u[j], u[j + 1], u[j + 2], d[j], x[j + 1]);
+}
 
 template <int C, int NT, bool STREAM, int MINB = 1, bool PAIR = false>
 __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* __restrict__ vin,
@@ -179,15 +186,17 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
       if (s + 1 < s1) SS::stage(((s + 1) & 1) ? XB1 : XB0, Xs + n, gst, n, used);
       SS::win((s & 1) ? XB1 : XB0, R.t, X);
     }
-    double acc[C], a[C], kk[C];
+    double acc[C], a[C], kk[C], dd[C];
     double x2[C + 4], u2[C + 4];
-    tl_sub<C>(v, X, a);
+#pragma unroll
+    for (int j = 0; j < C; ++j) dd[j] = __dsub_rn(X[j + 3], X[j]);
+    tl_sub_d<C>(v, X, dd, a);
     if (STREAM) {
       R.load_halo(Xs + n, x2);
     } else {
 #pragma unroll
       for (int j = 0; j < C; ++j) {
-        kk[j] = l96_f(X[j + 3], X[j], X[j + 1], X[j + 2], F);
+        kk[j] = l96_f_d(dd[j], X[j + 1], X[j + 2], F);
         x2[j + 2] = axpy_rn(X[j + 2], h, kk[j]);
       }
     }
@@ -199,13 +208,15 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
     if (STREAM) xchg1(R, xb, buf, u2); else xchg2(R, xb, buf, x2, u2);
 
     double x3[C + 4], u3[C + 4];
-    tl_sub<C>(u2, x2, a);
+#pragma unroll
+    for (int j = 0; j < C; ++j) dd[j] = __dsub_rn(x2[j + 3], x2[j]);
+    tl_sub_d<C>(u2, x2, dd, a);
     if (STREAM) {
       R.load_halo(Xs + 2 * n, x3);
     } else {
 #pragma unroll
       for (int j = 0; j < C; ++j) {
-        kk[j] = l96_f(x2[j + 3], x2[j], x2[j + 1], x2[j + 2], F);
+        kk[j] = l96_f_d(dd[j], x2[j + 1], x2[j + 2], F);
         x3[j + 2] = axpy_rn(X[j + 2], h, kk[j]);
       }
     }
@@ -217,13 +228,15 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
     if (STREAM) xchg1(R, xb, buf, u3); else xchg2(R, xb, buf, x3, u3);
 
     double x4[C + 4], u4[C + 4];
-    tl_sub<C>(u3, x3, a);
+#pragma unroll
+    for (int j = 0; j < C; ++j) dd[j] = __dsub_rn(x3[j + 3], x3[j]);
+    tl_sub_d<C>(u3, x3, dd, a);
     if (STREAM) {
       R.load_halo(Xs + 3 * n, x4);
     } else {
 #pragma unroll
       for (int j = 0; j < C; ++j) {
-        kk[j] = l96_f(x3[j + 3], x3[j], x3[j + 1], x3[j + 2], F);
+        kk[j] = l96_f_d(dd[j], x3[j + 1], x3[j + 2], F);
         x4[j + 2] = axpy_rn(X[j + 2], dt, kk[j]);
       }
     }
@@ -372,29 +385,36 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
         x4[j + 2] = axpy_rn(X[j + 2], dt, l96_f(x3[j + 3], x3[j], x3[j + 1], x3[j + 2], F));
       xchg1(R, xb, buf, x4);
     }
-    // step_adj (model.py:66-84)
-    double vh[C], u[C], a[C + 4];
+    // step_adj (model.py:66-84): with w = (dt/6) g and c3 = 2 c6, dt = 2h,
+    //   a3 = dt u4 + c3 g = 2 b3,  b3 = h u4 + w   (u3 = 2 J3^T b3)
+    //   a2 = h u3 + c3 g  = 2 b2,  b2 = h u3' + w  (u2 = 2 J2^T b2)
+    //   a1 = h u2 + c6 g  = dt u2' + w
+    // so the powers of two fold into the vh accumulation (exact scalings) and
+    // only w, not g, stays live through the stages
+    double vh[C], u[C], a[C + 4], w[C];
 #pragma unroll
-    for (int k = 0; k < C + 4; ++k) a[k] = c6 * g[k];  // a4 = (dt/6) w, halo included
+    for (int k = 0; k < C + 4; ++k) a[k] = c6 * g[k];  // a4 = (dt/6) g, halo included
+#pragma unroll
+    for (int j = 0; j < C; ++j) w[j] = a[j + 2];
     ad_sub<C>(a, x4, u);
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       vh[j] = g[j + 2] + u[j];
-      a[j + 2] = fma(dt, u[j], c3 * g[j + 2]);  // a3
+      a[j + 2] = fma(h, u[j], w[j]);  // b3
     }
     xchg1(R, xb, buf, a);
-    ad_sub<C>(a, x3, u);
+    ad_sub<C>(a, x3, u);  // u3'
 #pragma unroll
     for (int j = 0; j < C; ++j) {
-      vh[j] += u[j];
-      a[j + 2] = fma(h, u[j], c3 * g[j + 2]);  // a2
+      vh[j] = fma(2.0, u[j], vh[j]);
+      a[j + 2] = fma(h, u[j], w[j]);  // b2
     }
     xchg1(R, xb, buf, a);
-    ad_sub<C>(a, x2, u);
+    ad_sub<C>(a, x2, u);  // u2'
 #pragma unroll
     for (int j = 0; j < C; ++j) {
-      vh[j] += u[j];
-      a[j + 2] = fma(h, u[j], c6 * g[j + 2]);  // a1
+      vh[j] = fma(2.0, u[j], vh[j]);
+      a[j + 2] = fma(dt, u[j], w[j]);  // a1
     }
     if (!STREAM) cp_wait_all();  // X_{s-1} landed; published by this barrier
     xchg1(R, xb, buf, a);
