@@ -105,22 +105,25 @@ __global__ void __launch_bounds__(256) k_gemm_tn(const double* __restrict__ A, i
       }
 }
 
-__global__ void k_reduce_parts(const double* __restrict__ part, int nsplit, int m, int nb, double* __restrict__ C,
-                               int ldc) {
+// Fixed-order split-K reduction: 8 lanes per output, lane q sums splits
+// q, q+8, q+16, ... in order, then the 8 lane sums are combined in a fixed
+// butterfly order -- deterministic, and 8x the memory-level parallelism of
+// one thread per output (the reduction was latency-bound: 50 CTAs).
+__global__ void __launch_bounds__(256) k_reduce_parts(const double* __restrict__ part, int nsplit, int m, int nb,
+                                                      double* __restrict__ C, int ldc) {
   const int64_t tot = (int64_t)m * nb;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+  const int q = threadIdx.x & 7;
+  for (int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3; e < tot;
+       e += ((int64_t)gridDim.x * blockDim.x) >> 3) {
     double s = 0.0;
-    int z = 0;
-    for (; z + 8 <= nsplit; z += 8) {  // 8 loads in flight, same summation order
-      double v[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = part[(size_t)(z + q) * tot + e];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) s += v[q];
+    for (int z = q; z < nsplit; z += 8) s += part[(size_t)z * tot + e];
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (q == 0) {
+      const int a = (int)(e % m), b = (int)(e / m);
+      C[a + (size_t)b * ldc] = s;
     }
-    for (; z < nsplit; ++z) s += part[(size_t)z * tot + e];  // fixed order
-    const int a = (int)(e % m), b = (int)(e / m);
-    C[a + (size_t)b * ldc] = s;
   }
 }
 
@@ -160,8 +163,8 @@ int launch_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, d
   dim3 grid((m + G_BM - 1) / G_BM, (nb + G_BN - 1) / G_BN, s);
   k_gemm_tn<<<grid, 256, G_SMEM, st>>>(A, lda, B, ldb, m, nb, K, ks, part);
   int64_t tot = (int64_t)m * nb;
-  int nblk = (int)((tot + 255) / 256);
-  k_reduce_parts<<<nblk < 1024 ? nblk : 1024, 256, 0, st>>>(part, s, m, nb, C, ldc);
+  int nblk = (int)((tot * 8 + 255) / 256);
+  k_reduce_parts<<<nblk < 4096 ? nblk : 4096, 256, 0, st>>>(part, s, m, nb, C, ldc);
   count_launch(2);
   return check_launch("k_gemm_tn");
 }
