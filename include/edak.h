@@ -61,6 +61,14 @@ typedef struct edak_problem {
   const double* taps;
   int32_t ntaps;
   int32_t tap_w;
+  /* optional spectral form of the same factor (covariance.py:41-45: U_B v =
+   * irfft(symbol * rfft(v))): sym = the n/2+1 real symbol entries, fft_tw =
+   * exp(-2 pi i k / n) for k < n/2 as interleaved (re, im) doubles.  When
+   * both are set, n is a power of two in [1024, 16384] and EDAK_CIRC_FFT is
+   * set, U_B runs as a shared-memory FFT (one CTA, or a 2-CTA cluster, per
+   * column) instead of the tap convolution. */
+  const double* sym;
+  const double* fft_tw;
 } edak_problem;
 
 /* ---- library --------------------------------------------------------- */

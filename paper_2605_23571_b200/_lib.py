@@ -25,6 +25,7 @@ class Problem(C.Structure):
         ("stage_mode", i32), ("pad0", i32),
         ("gpos", vp), ("tpos", vp), ("G", i32), ("T", i32), ("sigma2", f64),
         ("taps", vp), ("ntaps", i32), ("tap_w", i32),
+        ("sym", vp), ("fft_tw", vp),
     ]
 
 

@@ -39,6 +39,7 @@ def _prob_struct(n, n_steps, dt, forcing, states, stages, traj_stride, stage_mod
     P.G, P.T = dnet.G, dnet.T
     P.sigma2 = float(sigma2)
     P.taps, P.ntaps, P.tap_w = dfac.taps.data_ptr(), dfac.ntaps, dfac.tap_w
+    P.sym, P.fft_tw = _lib.ptr(dfac.sym), _lib.ptr(dfac.fft_tw)
     return P
 
 

@@ -109,9 +109,25 @@ def factor_taps(ub):
     return np.ascontiguousarray(taps), w
 
 
+def fft_tables(n):
+    """(symbol-length check aside) the twiddle table exp(-2 pi i k / n),
+    k < n/2, as interleaved (re, im) float64 -- for the spectral U_B kernel
+    (circ_fft.cu), used when n is a power of two in [1024, 16384]."""
+    k = np.arange(n // 2, dtype=float)
+    ang = np.pi * (2.0 * k / n)  # 2k/n exact for power-of-two n
+    tw = np.empty(n, dtype=float)
+    tw[0::2] = np.cos(ang)
+    tw[1::2] = -np.sin(ang)
+    return tw
+
+
+FFT_MIN_N, FFT_MAX_N = 1024, 16384
+
+
 class DeviceFactor:
-    """Device-resident taps of a circulant factor + a minimal edak_problem
-    that the circulant kernel reads."""
+    """Device-resident taps (and, for power-of-two rings in [1024, 16384],
+    the rfft symbol + twiddles) of a circulant factor, plus a minimal
+    edak_problem that the U_B kernels read."""
 
     def __init__(self, ub):
         self.n = int(ub.n)
@@ -119,11 +135,18 @@ class DeviceFactor:
         self.taps = _dev.f64(taps)
         self.tap_w = w
         self.ntaps = taps.size
+        n = self.n
+        self.sym = self.fft_tw = None
+        if FFT_MIN_N <= n <= FFT_MAX_N and n & (n - 1) == 0:
+            self.sym = _dev.f64(np.asarray(ub.symbol, dtype=float))
+            self.fft_tw = _dev.f64(fft_tables(n))
         self._prob = _lib.Problem()
         self._prob.n = self.n
         self._prob.taps = self.taps.data_ptr()
         self._prob.ntaps = self.ntaps
         self._prob.tap_w = w
+        self._prob.sym = _lib.ptr(self.sym)
+        self._prob.fft_tw = _lib.ptr(self.fft_tw)
 
     def apply_cols(self, cols, out=None):
         """U_B applied to a (ncols, n) device block."""

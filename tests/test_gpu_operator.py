@@ -321,3 +321,30 @@ def test_randomized_window_operators(gpu, seed):
     assert rel(hz, z[:, 0] + ref[:, 0]) < 1e-12
     assert rel(prob.rhs(), op.rhs()) < 1e-12
     assert prob.quadratic_cost(z[:, 1]) == pytest.approx(op.quadratic_cost(z[:, 1]), rel=1e-12)
+
+
+def test_spectral_factor_equals_taps(gpu, monkeypatch):
+    """The opt-in spectral U_B (circ_fft.cu: one-CTA n = 1024, 2-CTA cluster
+    n = 16384) against the tap convolution and numpy's irfft(symbol rfft),
+    including the I + A epilogue and its p.Hp tile partials."""
+    from paper_2605_23571_b200.assim import Linearization
+    from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
+    for n, N, L in [(1024, 8, 8.0), (16384, 6, 16.0)]:
+        op = _oracle_problem(n, N, 4, 2, L, 21)
+        ub = CirculantFactor(n, op.ub.symbol)
+        lin = Linearization(op.traj.states[None], 0.025, 8.0, op.net, ub, DiagonalNoise(1.0))
+        z = torch.randn(5, n, dtype=torch.float64, device="cuda")
+        direct = lin.dfac.apply_cols(z)
+        monkeypatch.setenv("EDAK_CIRC_FFT", "1")
+        spec = lin.dfac.apply_cols(z)
+        ref = np.fft.irfft(np.fft.rfft(z.cpu().numpy(), axis=1) * op.ub.symbol, n=n, axis=1)
+        assert float((spec - direct).abs().max()) <= 1e-14 * float(direct.abs().max())
+        assert np.abs(spec.cpu().numpy() - ref).max() <= 1e-14 * np.abs(ref).max()
+        tiles = lin.dot_tiles()
+        dp = torch.empty((5, tiles), dtype=torch.float64, device="cuda")
+        hz = lin.hessian_cols(z, None, 1.0, None, None, None, dp)
+        monkeypatch.delenv("EDAK_CIRC_FFT")
+        dp2 = torch.empty_like(dp)
+        hz2 = lin.hessian_cols(z, None, 1.0, None, None, None, dp2)
+        assert float((hz - hz2).abs().max()) <= 1e-13 * float(hz2.abs().max())
+        assert torch.allclose(dp.sum(1), (z * hz).sum(1), rtol=1e-13)
