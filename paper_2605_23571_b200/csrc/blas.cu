@@ -151,8 +151,9 @@ int64_t gemm_tn_partials(int m, int nb, int64_t K) {
 
 static constexpr size_t G_SMEM = (2 * (size_t)(G_BM + G_BN) * (G_BK + G_PAD) + 2 * G_BK) * sizeof(double);
 
-int launch_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int ldc, int m, int nb,
-                   int64_t K, double* part, cudaStream_t st) {
+// split-K partials only (the consumer reduces them): returns the split count
+int launch_gemm_tn_parts(const double* A, int64_t lda, const double* B, int64_t ldb, int m, int nb, int64_t K,
+                         double* part, cudaStream_t st) {
   int64_t ks;
   const int s = tn_nsplit(m, nb, K, ks);
   static bool attr = false;
@@ -162,10 +163,17 @@ int launch_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, d
   }
   dim3 grid((m + G_BM - 1) / G_BM, (nb + G_BN - 1) / G_BN, s);
   k_gemm_tn<<<grid, 256, G_SMEM, st>>>(A, lda, B, ldb, m, nb, K, ks, part);
+  count_launch();
+  return s;
+}
+
+int launch_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int ldc, int m, int nb,
+                   int64_t K, double* part, cudaStream_t st) {
+  const int s = launch_gemm_tn_parts(A, lda, B, ldb, m, nb, K, part, st);
   int64_t tot = (int64_t)m * nb;
   int nblk = (int)((tot * 8 + 255) / 256);
   k_reduce_parts<<<nblk < 4096 ? nblk : 4096, 256, 0, st>>>(part, s, m, nb, C, ldc);
-  count_launch(2);
+  count_launch();
   return check_launch("k_gemm_tn");
 }
 

@@ -54,6 +54,9 @@ int launch_pcg_alpha(int, int, const double*, const double*, double*, double*, d
                      const double*, const double*, int, cudaStream_t);
 int launch_pcg_rz(int, int, int, const double*, const double*, double*, double, double*, double*, int, int32_t*,
                   int32_t*, int, cudaStream_t);
+int launch_pcg_reduce_rz(int, int, int, const double*, int, double*, const double*, double*, double, double*,
+                         double*, int, int32_t*, int32_t*, int, cudaStream_t);
+int launch_gemm_tn_parts(const double*, int64_t, const double*, int64_t, int, int, int64_t, double*, cudaStream_t);
 double* pcg_beta_ptr(int, int, double*);
 int launch_pcg_beta(int, int, const double*, const double*, double*, double*, double, double*, double*, int,
                     int32_t*, int32_t*, int, cudaStream_t);
@@ -265,9 +268,12 @@ int edak_pcg_lmp_beta(int n, int k, int ncols, const double* S, const double* co
   double* W = lmpwork;
   double* part = lmpwork + (int64_t)k * ncols;
   int rc;
-  // W = S^T r (lmp.py:63); rz_new = |r|^2 + W^T diag(coef) W; beta
-  if ((rc = launch_gemm_tn(S, n, r, n, W, k, k, ncols, n, part, st))) return rc;
-  if ((rc = launch_pcg_rz(n, ncols, k, W, coef, work, rtol, hist_rz, hist_J, hist_ld, status, iters, it, st)))
+  // W = S^T r (lmp.py:63) as split-K partials; their reduction, rz_new =
+  // |r|^2 + W^T diag(coef) W and beta in one kernel
+  const int nsplit = launch_gemm_tn_parts(S, n, r, n, k, ncols, n, part, st);
+  if ((rc = check_launch("k_gemm_tn"))) return rc;
+  if ((rc = launch_pcg_reduce_rz(n, ncols, k, part, nsplit, W, coef, work, rtol, hist_rz, hist_J, hist_ld, status,
+                                 iters, it, st)))
     return rc;
   // p = r + beta p + S (coef o W)  (= z + beta p, krylov.py:95 with z = P r)
   return launch_gemm_nn(S, n, W, k, coef, r, n, 1.0, p, n, n, ncols, k, st, pcg_beta_ptr(n, ncols, work), p);

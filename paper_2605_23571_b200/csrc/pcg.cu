@@ -245,6 +245,70 @@ int launch_pcg_alpha(int n, int M, const double* p, const double* hp, double* x,
   return check_launch("k_pcg_upd_x");
 }
 
+// k_pcg_rz with the split-K reduction of W = S^T r folded in: one CTA per
+// column reduces its k entries (2 lanes per entry, fixed order) from the
+// GEMM's partials, writes W for the p-update GEMM, and runs the rz step.
+__global__ void __launch_bounds__(256) k_pcg_reduce_rz(int T, int M, int k, const double* __restrict__ part,
+                                                       int nsplit, double* __restrict__ W,
+                                                       const double* __restrict__ coef,
+                                                       const double* __restrict__ part_rr,
+                                                       const double* __restrict__ part_x, double* __restrict__ rzb,
+                                                       double* __restrict__ beta, double rtol,
+                                                       double* __restrict__ hist_rz, double* __restrict__ hist_J,
+                                                       int hist_ld, int32_t* __restrict__ status,
+                                                       int32_t* __restrict__ iters, int it) {
+  __shared__ double sh[32];
+  const int c = blockIdx.x, t = threadIdx.x;
+  const int64_t tot = (int64_t)k * M;
+  double q = 0.0;
+  for (int i0 = 0; i0 < k; i0 += 128) {
+    const int i = i0 + (t >> 1), hh = t & 1;
+    double s = 0.0;
+    if (i < k)
+      for (int z = hh; z < nsplit; z += 2) s += part[(size_t)z * tot + i + (size_t)c * k];
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (i < k && hh == 0) {
+      W[i + (size_t)c * k] = s;
+      q += coef[i] * (s * s);
+    }
+  }
+  q = block_sum<256>(q, sh);
+  if (threadIdx.x < 32) {
+    const double rr = sum_parts(part_rr + (size_t)c * T, T);
+    const double xbr = hist_J ? sum_parts(part_x + (size_t)c * T, T) : 0.0;
+    if (threadIdx.x == 0) {
+      if (status[c] != 0) {
+        beta[c] = 0.0;
+        return;
+      }
+      const double rz_new = rr + q;
+      const double rz_old = rzb[(size_t)((it - 1) & 1) * M + c];
+      const bool stop = rz_new <= 0.0 ||
+                        (rtol >= 0.0 && sqrt(rz_new) <= rtol * sqrt(hist_rz[(size_t)c * hist_ld]));
+      hist_rz[(size_t)c * hist_ld + it] = rz_new;
+      if (hist_J) hist_J[(size_t)c * hist_ld + it] = hist_J[(size_t)c * hist_ld] - 0.5 * xbr;
+      iters[c] = it;
+      rzb[(size_t)(it & 1) * M + c] = rz_new;
+      if (stop) status[c] = 1;
+      beta[c] = stop ? 0.0 : rz_new / rz_old;
+    }
+  }
+}
+
+int launch_pcg_reduce_rz(int n, int M, int k, const double* part, int nsplit, double* W, const double* coef,
+                         double* work, double rtol, double* hist_rz, double* hist_J, int hist_ld, int32_t* status,
+                         int32_t* iters, int it, cudaStream_t st) {
+  const int T = pcg_tiles(n);
+  double* part_x = work + (size_t)M * T;
+  double* part_rr = work + 2 * (size_t)M * T;
+  double* rzb = work + 4 * (size_t)M * T;
+  double* beta = rzb + 2 * (size_t)M;
+  k_pcg_reduce_rz<<<M, 256, 0, st>>>(T, M, k, part, nsplit, W, coef, part_rr, part_x, rzb, beta, rtol, hist_rz,
+                                     hist_J, hist_ld, status, iters, it);
+  count_launch();
+  return check_launch("k_pcg_reduce_rz");
+}
+
 int launch_pcg_rz(int n, int M, int k, const double* W, const double* coef, double* work, double rtol,
                   double* hist_rz, double* hist_J, int hist_ld, int32_t* status, int32_t* iters, int it,
                   cudaStream_t st) {
