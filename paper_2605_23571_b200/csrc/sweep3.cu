@@ -17,38 +17,75 @@
 namespace edak {
 
 struct SweepGeom3 {
-  int W, HL, periodic, nact;
+  int W, HL, periodic, nact, pair;
 };
 
-// shared staging with a 4-element halo, padded one double per C
+// shared staging with a 4-element halo, padded 2 doubles per C (16-byte
+// aligned runs): 16-byte cp.async pairs with immediate offsets when the
+// window does not wrap and rows are 16-byte aligned (n even, even tile base),
+// 8-byte copies otherwise; both fill the same layout, read with 16-byte loads
 template <int C, int NT>
 struct Stage4 {
+  static_assert(C % 2 == 0, "pairs");
   static constexpr int H = 4;
   static constexpr int R = C * NT;
-  static constexpr int PLEN = (R + 2 * H) + (R + 2 * H) / C + 2;
-  __device__ static __forceinline__ int pi(int q) { return (q + H) + (q + H) / C; }
-  __device__ static __forceinline__ void stage(double* buf, const double* __restrict__ src, int g0, int n,
-                                               int used) {
-    int g = g0;
-    double* d = buf + pi((int)threadIdx.x - H);
-    for (int q = (int)threadIdx.x - H; q < used + H; q += NT) {
-      cp_async8(d, src + g);
-      d += NT + NT / C;
-      g += NT;
-      while (g >= n) g -= n;
+  static constexpr int NPAIR = (R + 2 * H) / 2;
+  static constexpr int IT = (NPAIR + NT - 1) / NT;
+  static constexpr int PLEN = (R + 2 * H) + 2 * ((R + 2 * H) / C) + 2;
+  __device__ static __forceinline__ int pi(int q) { return (q + H) + 2 * ((q + H) / C); }
+  // gm4 = ring index (unwrapped, may be < 0) of window element -4
+  __device__ static __forceinline__ void stage(double* buf, const double* __restrict__ src, int gm4, int n,
+                                               int used, bool pair) {
+    const int t = threadIdx.x;
+    if (pair) {
+      const int np = (used + 2 * H) >> 1;
+      double* d = buf + 2 * t + 2 * (t / (C / 2));
+      constexpr int DSTEP = 2 * NT + 2 * (NT / (C / 2));
+      if (gm4 >= 0 && gm4 + used + 2 * H <= n) {
+        const double* p = src + gm4 + 2 * t;
+#pragma unroll
+        for (int it = 0; it < IT; ++it)
+          if (t + it * NT < np) cp_async16(d + it * DSTEP, p + 2 * it * NT);
+      } else {
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+          const int m = t + it * NT;
+          if (m < np) {
+            int g = gm4 + 2 * m;
+            g = g < 0 ? g + n : (g >= n ? g - n : g);
+            cp_async16(d + it * DSTEP, src + g);
+          }
+        }
+      }
+      return;
+    }
+    for (int q = t - H; q < used + H; q += NT) {
+      int g = (gm4 + H + q) % n;
+      if (g < 0) g += n;
+      cp_async8(buf + pi(q), src + g);
     }
   }
   // window [-2, C + 2) of thread t
   __device__ static __forceinline__ void win2(const double* buf, int t, double (&a)[C + 4]) {
-    const double* w = buf + (C + 1) * t;
+    const double* w = buf + (C + 2) * t;
 #pragma unroll
-    for (int k = 0; k < C + 4; ++k) a[k] = w[(k + 2) + (k + 2) / C];
+    for (int k = 0; k < C + 4; k += 2) {
+      const int off = (2 + k) + 2 * ((2 + k) / C);
+      const double2 v = *reinterpret_cast<const double2*>(w + off);
+      a[k] = v.x;
+      a[k + 1] = v.y;
+    }
   }
   // window [-4, C + 4) of thread t
   __device__ static __forceinline__ void win4(const double* buf, int t, double (&a)[C + 8]) {
-    const double* w = buf + (C + 1) * t;
+    const double* w = buf + (C + 2) * t;
 #pragma unroll
-    for (int k = 0; k < C + 8; ++k) a[k] = w[k + k / C];
+    for (int k = 0; k < C + 8; k += 2) {
+      const int off = k + 2 * (k / C);
+      const double2 v = *reinterpret_cast<const double2*>(w + off);
+      a[k] = v.x;
+      a[k + 1] = v.y;
+    }
   }
 };
 
@@ -86,7 +123,8 @@ __global__ void __launch_bounds__(NT, MINB) k_tl3(edak_problem P, const double* 
   double* ob = obs + (size_t)col * G * P.T;
   const double dt = P.dt, h = 0.5 * dt, c6 = dt / 6.0, F = P.forcing;
   const int used = R.nact * C;
-  const int gst = wrap(R.base - SS::H + (int)threadIdx.x, n);
+  const int gst = R.base - SS::H;
+  const bool pair = geo.pair != 0;
   int buf = 0;
 
   int gw[C];
@@ -105,9 +143,9 @@ __global__ void __launch_bounds__(NT, MINB) k_tl3(edak_problem P, const double* 
   auto stage_step = [&](int s) {
     double* b = SB + (size_t)(s & 1) * 3 * SS::PLEN;
     const double* src = sg + (size_t)s * 4 * n;
-    SS::stage(b, src, gst, n, used);
-    SS::stage(b + SS::PLEN, src + n, gst, n, used);
-    SS::stage(b + 2 * SS::PLEN, src + 2 * n, gst, n, used);
+    SS::stage(b, src, gst, n, used, pair);
+    SS::stage(b + SS::PLEN, src + n, gst, n, used, pair);
+    SS::stage(b + 2 * SS::PLEN, src + 2 * n, gst, n, used, pair);
     cp_commit();
   };
 
@@ -200,7 +238,8 @@ __global__ void __launch_bounds__(NT, MINB) k_ad3(edak_problem P, const double* 
   const double c6 = dt / 6.0, c3 = 2.0 * dt / 6.0;
   const double inv_s2 = 1.0 / P.sigma2;
   const int used = R.nact * C;
-  const int gst = wrap(R.base - SS::H + (int)threadIdx.x, n);
+  const int gst = R.base - SS::H;
+  const bool pair = geo.pair != 0;
   int buf = 0;
 
   int gp[C];
@@ -217,9 +256,9 @@ __global__ void __launch_bounds__(NT, MINB) k_ad3(edak_problem P, const double* 
   auto stage_step = [&](int s) {
     double* b = SB + (size_t)(s & 1) * 3 * SS::PLEN;
     const double* src = sg + (size_t)s * 4 * n;
-    SS::stage(b, src, gst, n, used);
-    SS::stage(b + SS::PLEN, src + n, gst, n, used);
-    SS::stage(b + 2 * SS::PLEN, src + 2 * n, gst, n, used);
+    SS::stage(b, src, gst, n, used, pair);
+    SS::stage(b + SS::PLEN, src + n, gst, n, used, pair);
+    SS::stage(b + 2 * SS::PLEN, src + 2 * n, gst, n, used, pair);
     cp_commit();
   };
 
@@ -321,7 +360,7 @@ static int env3(const char* name, int dflt) {
 static bool plan3(int n, int hl, int hr, SweepGeom3& geo, int& nt) {
   constexpr int C = 8, NT = 128, RNG = C * NT;
   if (n % C == 0 && n / C <= NT && n / C >= 64) {
-    geo = {n, 0, 1, n / C};
+    geo = {n, 0, 1, n / C, n % 2 == 0};
     nt = 1;
     return true;
   }
@@ -329,7 +368,9 @@ static bool plan3(int n, int hl, int hr, SweepGeom3& geo, int& nt) {
   const int W = RNG - hl - hr;
   if (W < 256) return false;
   nt = (n + W - 1) / W;
-  geo = {(n + nt - 1) / nt, hl, 0, NT};
+  int Wt = ((n + nt - 1) / nt + 1) & ~1;  // even tile width (pair staging)
+  if (Wt > W) Wt = W;
+  geo = {Wt, hl, 0, NT, (n % 2 == 0 && Wt % 2 == 0 && hl % 2 == 0) ? 1 : 0};
   return true;
 }
 
@@ -347,6 +388,7 @@ int launch_tl3(const edak_problem* P, const double* vin, double* obs, int ncols,
   int nt;
   const int K = s1 - s0;
   if (!plan3(P->n, 8 * K + 4, 4 * K + 4, geo, nt)) return EDAK_EUNSUPPORTED;
+  if (((uintptr_t)P->stages & 15) || (P->traj_stride & 1) || getenv("EDAK_NO_PAIR")) geo.pair = 0;
   const size_t sm = smem3<8, 128>();
   if (env3("EDAK_TL3_MINB", 4) == 3) {
     attr3(k_tl3<8, 128, 3>, sm);
@@ -365,6 +407,7 @@ int launch_ad3(const edak_problem* P, const double* forcing, double* gout, int n
   int nt;
   const int K = s1 - s0;
   if (!plan3(P->n, 4 * K + 8, 8 * K + 8, geo, nt)) return EDAK_EUNSUPPORTED;
+  if (((uintptr_t)P->stages & 15) || (P->traj_stride & 1) || getenv("EDAK_NO_PAIR")) geo.pair = 0;
   const size_t sm = smem3<8, 128>();
   if (env3("EDAK_AD3_MINB", 3) == 2) {
     attr3(k_ad3<8, 128, 2>, sm);
