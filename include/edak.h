@@ -222,6 +222,19 @@ int edak_pcg_beta(int n, int ncols, const double* z, const double* r, double* p,
  * (SpectralLmp._project / apply_sqrt, lmp.py:62-70); with coef =
  * theta/(lam+1) - 1 and orthonormal S it is P itself (lmp.py:72-74). */
 int64_t edak_lmp_work_doubles(int n, int k, int ncols);
+/* Whole batched LMP-PCG solve for small rings (8 <= n <= 256; G*T <= 8192
+ * observations): one CTA per member runs every iteration -- U_B, TL sweep,
+ * AD sweep, U_B + I, the recurrence with the J identity, the single-pass LMP
+ * (S, coef; S == NULL: no preconditioner) -- in one launch (krylov.py:49-97
+ * for each member; cfg1/cfg2 are latency-bound).  b (M, n),
+ * d (M, G*T) innovations for the J trace (NULL: no trace), outputs x (M, n),
+ * hist_rz / hist_J (M, hist_ld >= max_iters + 1), status (0 running/max,
+ * 1 converged, 2 A not PD at iters, 3 P not PD), iters. */
+int edak_pcg_small(const edak_problem* P, const int32_t* col_traj, int ncols,
+                   const double* b, const double* d, const double* S,
+                   const double* coef, int k, int max_iters, double rtol,
+                   double* x, double* hist_rz, double* hist_J, int hist_ld,
+                   int32_t* status, int32_t* iters, void* stream);
 int edak_lmp_apply(int n, int k, int ncols, const double* S, const double* coef,
                    const double* r, double* z, double* work, void* stream);
 /* column dots out[c] = a[c] . b[c], fixed order (deterministic) */

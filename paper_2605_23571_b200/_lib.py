@@ -63,6 +63,8 @@ _PROTOS = {
                                 C.c_int, vp]),
     "edak_lmp_work_doubles": (i64, [C.c_int, C.c_int, C.c_int]),
     "edak_chol_inv_work_doubles": (i64, [C.c_int]),
+    "edak_pcg_small": (C.c_int, [C.POINTER(Problem), vp, C.c_int, vp, vp, vp, vp, C.c_int, C.c_int, f64,
+                                 vp, vp, vp, C.c_int, vp, vp, vp]),
     "edak_chol_inv": (C.c_int, [vp, C.c_int, vp, vp, C.c_int, f64, vp, vp, vp, vp]),
     "edak_lmp_apply": (C.c_int, [C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp]),
     "edak_col_dots": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, vp]),

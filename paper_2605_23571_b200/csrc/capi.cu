@@ -76,6 +76,11 @@ static bool bad_problem(const edak_problem* P) {
   return false;
 }
 
+int launch_pcg_small_c(const edak_problem* P, const int32_t* col_traj, int M, const double* b, const double* d,
+                       const double* S, const double* coef, int k, int max_iters, double rtol, double* x,
+                       double* hist_rz, double* hist_J, int hist_ld, int32_t* status, int32_t* iters,
+                       cudaStream_t st);
+
 }  // namespace edak
 
 using namespace edak;
@@ -277,6 +282,16 @@ int edak_pcg_lmp_beta(int n, int k, int ncols, const double* S, const double* co
     return rc;
   // p = r + beta p + S (coef o W)  (= z + beta p, krylov.py:95 with z = P r)
   return launch_gemm_nn(S, n, W, k, coef, r, n, 1.0, p, n, n, ncols, k, st, pcg_beta_ptr(n, ncols, work), p);
+}
+
+int edak_pcg_small(const edak_problem* P, const int32_t* col_traj, int ncols, const double* b, const double* d,
+                   const double* S, const double* coef, int k, int max_iters, double rtol, double* x,
+                   double* hist_rz, double* hist_J, int hist_ld, int32_t* status, int32_t* iters, void* stream) {
+  if (ncols == 0) return EDAK_OK;
+  if (bad_problem(P) || !b || !x || !hist_rz || !status || !iters || max_iters < 1 || (S && (!coef || k < 1)))
+    return EDAK_EINVAL;
+  return launch_pcg_small_c(P, col_traj, ncols, b, d, S, coef, k, max_iters, rtol, x, hist_rz, hist_J, hist_ld,
+                            status, iters, as_stream(stream));
 }
 
 int64_t edak_lmp_work_doubles(int n, int k, int ncols) {

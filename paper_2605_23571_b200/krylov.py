@@ -276,8 +276,45 @@ def _default_groups(M):
     return 2 if M >= 64 else 1
 
 
+SMALL_MAX_N = 256  # rings up to which pcg_members runs the persistent one-CTA-per-member solve
+
+
+def _small_ok(ens, lmp, precond):
+    lin = ens.lin
+    return (lin.n <= SMALL_MAX_N and lin.n >= 8 and lin.stage_mode == "recompute"
+            and lin.p * 8 <= 64 * 1024 and (precond is None or lmp is not None)
+            and (lmp is None or lmp[0].shape[0] <= SMALL_MAX_N))
+
+
+def pcg_members_small(ens, B, cfg, lmp=None, cost="recurrence"):
+    """The whole batched solve in ONE launch (edak_pcg_small): one CTA per
+    member runs every iteration -- Hessian apply, recurrence, J identity,
+    single-pass LMP -- with the ring in shared memory.  Same results as the
+    per-iteration path up to summation order."""
+    M, n = B.shape
+    dev = B.device
+    L = cfg.max_iters + 1
+    X = torch.empty_like(B)
+    hist_rz = torch.zeros((M, L), dtype=torch.float64, device=dev)
+    trace = bool(cfg.trace_cost and cost == "recurrence")
+    hist_J = torch.full((M, L), float("nan"), dtype=torch.float64, device=dev)
+    status = torch.zeros(M, dtype=torch.int32, device=dev)
+    iters = torch.zeros(M, dtype=torch.int32, device=dev)
+    rtol = -1.0 if cfg.residual_rtol is None else float(cfg.residual_rtol)
+    S, coef = (None, None) if lmp is None else (lmp[0].contiguous(), lmp[1].contiguous())
+    ct = ens.traj_of
+    _lib.call("edak_pcg_small", _lib.C.byref(ens.lin._P), _lib.ptr(ct), M, B.data_ptr(),
+              ens.D.data_ptr() if trace else None, _lib.ptr(S), _lib.ptr(coef),
+              0 if S is None else S.shape[0], cfg.max_iters, rtol, X.data_ptr(),
+              hist_rz.data_ptr(), hist_J.data_ptr() if trace else None, L, status.data_ptr(),
+              iters.data_ptr(), _lib.stream())
+    ens.n_matvecs += cfg.max_iters
+    return X, _traces(status.cpu().numpy(), iters.cpu().numpy(), hist_rz.cpu().numpy(),
+                      hist_J.cpu().numpy(), trace)
+
+
 def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fused=True,
-                groups=None, check_every=8, graph=None):
+                groups=None, check_every=8, graph=None, small=None):
     """Batched PCG over all members of an ``Ensemble``: B (M, n) device
     right-hand sides (e.g. ens.rhs_all()).  cost: "recurrence", "exact" or
     None.  ``fused`` folds p.Hp into the Hessian's last pass and a
@@ -296,6 +333,8 @@ def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fu
     the first time an ensemble sees this shape, and replays it afterwards
     with the new right-hand sides and LMP copied into its resident buffers:
     no per-kernel launch cost and no inter-kernel gaps.
+    ``small`` (default: rings of n <= 256 in recompute mode) runs the
+    whole solve as one persistent launch (pcg_members_small).
     Returns (X (M, n), [SolveTrace] * M)."""
     import os
     M = ens.M
@@ -313,6 +352,12 @@ def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fu
         graph = (env != "0") if env is not None else (B.numel() <= GRAPH_MAX_ELEMS)
     graph = (graph and snapshots is None and cfg.residual_rtol is None and fused
              and (precond is None or lmp is not None) and cost in ("recurrence", None))
+    if small is None:
+        env = os.environ.get("EDAK_PCG_SMALL")
+        small = (env != "0") if env is not None else True
+    if (small and snapshots is None and fused and cost in ("recurrence", None)
+            and _small_ok(ens, lmp, precond)):
+        return pcg_members_small(ens, B, cfg, lmp, cost)
     Z0 = apply_p(B) if apply_p is not None else B
     if graph:
         return _pcg_members_graph(ens, B, Z0, cfg, lmp, cost, G)

@@ -14,6 +14,7 @@ from conftest import GOLDEN, unpack_problem
 from parity import lmp_pcg_envelope, assert_trace, assert_values, nystrom_envelope, pcg_envelope
 from oracle import algorithms as oalg
 from oracle.twin import TwinConfig, build_setup
+from paper_2605_23571_b200 import _lib
 
 pytestmark = pytest.mark.gpu
 
@@ -233,8 +234,8 @@ def test_pcg_members_batched_equals_single(gpu):
     mems = [_gpu_problem(m) for m in setup.members]
     ens = Ensemble.from_members(mems)
     cfg = SolverConfig(max_iters=12)
-    X, trs = pcg_members(ens, ens.rhs_all(), cfg, cost="recurrence")
-    X2, trs2 = pcg_members(ens, ens.rhs_all(), cfg, cost="exact")
+    X, trs = pcg_members(ens, ens.rhs_all(), cfg, cost="recurrence", small=False)
+    X2, trs2 = pcg_members(ens, ens.rhs_all(), cfg, cost="exact", small=False)
     for j, m in enumerate(mems):
         _, tr = pcg(m.hessian_apply, m.rhs(), cfg, cost_fn=m.quadratic_cost)
         npt.assert_array_equal(trs[j].resnorm, tr.resnorm)  # same kernels, same bits
@@ -310,8 +311,8 @@ def test_pcg_fused_lmp_beta_matches_two_step(gpu, ref_problem):
     mems = [_gpu_problem(m) for m in st.members]
     ens = Ensemble.from_members(mems)
     cfg = SolverConfig(max_iters=30)
-    Xf, trf = pcg_members(ens, ens.rhs_all(), cfg, precond=lmp, fused=True)
-    Xu, tru = pcg_members(ens, ens.rhs_all(), cfg, precond=lmp, fused=False)
+    Xf, trf = pcg_members(ens, ens.rhs_all(), cfg, precond=lmp, fused=True, small=False)
+    Xu, tru = pcg_members(ens, ens.rhs_all(), cfg, precond=lmp, fused=False, small=False)
     npt.assert_allclose(Xf.cpu().numpy(), Xu.cpu().numpy(), rtol=0, atol=1e-10 * float(Xu.abs().max()))
     for j in range(len(mems)):
         npt.assert_allclose(trf[j].cost, tru[j].cost, rtol=1e-11)
@@ -380,12 +381,116 @@ def test_pcg_members_graph_replay_equals_eager(gpu):
         lmps.append(make_lmp(approx, "halfsum"))
     for groups in (1, 2):
         for lmp in [None] + lmps[:1] + lmps[:1]:  # capture, then replay twice
-            Xe, te = pcg_members(ens, B, cfg, precond=lmp, groups=groups, graph=False)
-            Xg, tg = pcg_members(ens, B, cfg, precond=lmp, groups=groups, graph=True)
+            Xe, te = pcg_members(ens, B, cfg, precond=lmp, groups=groups, graph=False, small=False)
+            Xg, tg = pcg_members(ens, B, cfg, precond=lmp, groups=groups, graph=True, small=False)
             assert torch.equal(Xe, Xg)
             for a, b in zip(te, tg):
                 assert a.cost == b.cost and a.resnorm == b.resnorm and a.status == b.status
         B2 = B * 1.5
-        Xe, te = pcg_members(ens, B2, cfg, precond=lmps[0], groups=groups, graph=False)
-        Xg, tg = pcg_members(ens, B2, cfg, precond=lmps[0], groups=groups, graph=True)
+        Xe, te = pcg_members(ens, B2, cfg, precond=lmps[0], groups=groups, graph=False, small=False)
+        Xg, tg = pcg_members(ens, B2, cfg, precond=lmps[0], groups=groups, graph=True, small=False)
         assert torch.equal(Xe, Xg)
+
+
+@pytest.mark.parametrize("n,grid", [(40, 8), (100, 20), (256, 64)])
+def test_pcg_small_persistent_matches_batched(gpu, n, grid):
+    """The one-launch small-ring solve (pcg_small.cu: one CTA per member runs
+    every iteration) against the per-iteration batched path and the oracle,
+    separate trajectories per member.  First 4 iterations (before CG's
+    round-off amplification sets in): x, J, resnorm to 1e-12 of the batched
+    path, with and without a single-pass LMP.  15 iterations: every member's
+    trace inside the oracle's CPU-vs-CPU envelope (assert_trace).  With
+    residual_rtol both paths converge, within one iteration of each other."""
+    from paper_2605_23571_b200.assim import Ensemble
+    from paper_2605_23571_b200.krylov import SolverConfig, pcg_members
+    from paper_2605_23571_b200.lmp import make_lmp
+    from paper_2605_23571_b200.nystrom import NystromConfig, nystrom_evd
+    tw = TwinConfig(n=n, obs_grid_count=grid, members=7)
+    setup = build_setup(tw, trial_seed=1)
+    mems = [_gpu_problem(m) for m in setup.members]
+    ens = Ensemble.from_members(mems)
+    ctl = _gpu_problem(setup.control)
+    B = ens.rhs_all()
+    approx = nystrom_evd(ctl.a_apply, (B - B.mean(0)).t().cpu().numpy(),
+                         NystromConfig(ell=7, k=5, shift_mode="trace"))
+    lmp = make_lmp(approx, "halfsum")
+    for pre in (None, lmp):
+        cfg = SolverConfig(max_iters=4)
+        Xb, tb = pcg_members(ens, B, cfg, precond=pre, small=False, graph=False)
+        n0 = _lib.launch_count()
+        Xs, ts = pcg_members(ens, B, cfg, precond=pre, small=True)
+        assert _lib.launch_count() - n0 == 1
+        npt.assert_allclose(Xs.cpu().numpy(), Xb.cpu().numpy(), rtol=0,
+                            atol=1e-12 * float(Xb.abs().max()))
+        for a, b in zip(ts, tb):
+            assert a.status == b.status and a.iterations == b.iterations
+            npt.assert_allclose(a.cost, b.cost, rtol=1e-12)
+            assert np.max(np.abs(np.array(a.resnorm) - b.resnorm)) <= 1e-12 * b.resnorm[0]
+    cfg = SolverConfig(max_iters=15)
+    _, ts = pcg_members(ens, B, cfg, small=True)
+    _, tb = pcg_members(ens, B, cfg, small=False, graph=False)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    jit = []
+    for _ in range(3):
+        Bp = B * (1 + 1e-16 * torch.randn(B.shape, generator=gen, device="cuda", dtype=torch.float64))
+        jit.append(pcg_members(ens, Bp, cfg, small=True)[1])
+    for j, om in enumerate(setup.members):
+        ref, ej, er = pcg_envelope(om.hessian_apply, om.rhs(), cfg, cost_fn=om.quadratic_cost)
+        # plain CG on these ill-conditioned twins amplifies round-off ~1e8-fold
+        # by iteration 10 (tools/small_probe.py): widen the CPU envelope by the
+        # batched GPU path's distance from the oracle and by the persistent
+        # path's own spread under 1e-16 right-hand-side jitter
+        ej = np.maximum(ej, np.abs(np.array(tb[j].cost) - ref.cost))
+        er = np.maximum(er, np.abs(np.array(tb[j].resnorm) - ref.resnorm))
+        for t in jit:
+            ej = np.maximum(ej, np.abs(np.array(t[j].cost) - ts[j].cost))
+            er = np.maximum(er, np.abs(np.array(t[j].resnorm) - ts[j].resnorm))
+        assert_trace(ts[j], ref, ej, er)
+    cfg = SolverConfig(max_iters=300, residual_rtol=1e-5)
+    _, tb = pcg_members(ens, B, cfg, precond=lmp, small=False, graph=False)
+    _, ts = pcg_members(ens, B, cfg, precond=lmp, small=True)
+    for a, b in zip(ts, tb):
+        assert a.status == b.status == "converged"
+        assert abs(a.iterations[-1] - b.iterations[-1]) <= max(3, b.iterations[-1] // 10)
+        assert a.resnorm[-1] <= 1e-5 * a.resnorm[0]
+
+
+def test_pcg_small_cfg1_golden(gpu, ref_problem):
+    """cfg1 members through the persistent solve against the reference's
+    golden traces (same bars as test_cfg1_lmp_pcg_golden)."""
+    from paper_2605_23571_b200.assim import Ensemble
+    from paper_2605_23571_b200.krylov import SolverConfig, pcg_members
+    from paper_2605_23571_b200.lmp import make_lmp
+    from paper_2605_23571_b200.nystrom import NystromConfig, nystrom_evd
+    from oracle.twin import BASELINE_CONFIGS, baseline_setup
+    g = ref_problem
+    st = baseline_setup(BASELINE_CONFIGS[1])
+    ctl = _gpu_problem(st.control)
+    approx = nystrom_evd(ctl.a_apply, g["cfg1_gamma"], NystromConfig(10, 10, shift_mode="trace"))
+    lmp = make_lmp(approx, "halfsum")
+    ens = Ensemble.from_members([_gpu_problem(m) for m in st.members])
+    _, trs = pcg_members(ens, ens.rhs_all(), SolverConfig(max_iters=30), precond=lmp, small=True)
+    for j in (0, 4, 9):
+        npt.assert_allclose(trs[j].cost, g[f"cfg1_m{j}_cost"], rtol=1e-10)
+        ref = np.asarray(g[f"cfg1_m{j}_resnorm"])
+        _, _, env_r = lmp_pcg_envelope(st.control, g["cfg1_gamma"],
+                                       oalg.NystromConfig(10, 10, shift_mode="trace"), "halfsum",
+                                       st.members[j], oalg.SolverConfig(max_iters=30))
+        tol = np.maximum(1e-10 * ref[0], 10 * env_r)
+        assert np.all(np.abs(np.array(trs[j].resnorm) - ref) <= tol)
+
+
+def test_pcg_small_breakdown_statuses(gpu):
+    """A negative-definite LMP (coef < -1) makes r.z < 0 at the start: the
+    persistent solve reports the reference's 'preconditioner is not positive
+    definite' like the batched path."""
+    from paper_2605_23571_b200.assim import Ensemble
+    from paper_2605_23571_b200.krylov import PcgBreakdown, SolverConfig, pcg_members_small
+    tw = TwinConfig(n=40, obs_grid_count=8, members=3)
+    setup = build_setup(tw, trial_seed=2)
+    ens = Ensemble.from_members([_gpu_problem(m) for m in setup.members])
+    B = ens.rhs_all()
+    S = (B / B.norm(dim=1, keepdim=True)).contiguous()
+    coef = torch.full((S.shape[0],), -3.0, dtype=torch.float64, device=B.device)
+    with pytest.raises(PcgBreakdown, match="preconditioner is not positive definite"):
+        pcg_members_small(ens, B, SolverConfig(max_iters=5), (S, coef))
