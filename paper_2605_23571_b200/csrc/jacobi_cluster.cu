@@ -11,7 +11,9 @@
 // double-buffered slot, ONE cluster barrier, and each pair pulls its next
 // columns from the neighbouring pairs' slots -- through distributed shared
 // memory when the neighbour sits on another SM.  Outputs as k_svd_jacobi:
-// U (unit columns, descending sigma), sig.
+// U (unit columns, descending sigma), sig, and with Vout the right singular
+// vectors: each column then travels as [a; v] (rows + cols entries, v
+// starting as e_id), rotated as one, with the dots over the a part only.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -22,7 +24,6 @@ namespace edak {
 
 constexpr int JC_CL = 8;           // CTAs per cluster (portable size)
 constexpr int JC_MAXROWS = 256;    // rows <= 256 -> <= 16 rows per lane
-constexpr int JC_RPL = JC_MAXROWS / 16;
 
 __device__ __forceinline__ double jc_rcp(double x) {
   double r;
@@ -33,22 +34,39 @@ __device__ __forceinline__ double jc_rcp(double x) {
   return fma(r, e, r);
 }
 
-// smem per CTA: slots [2 buf][ppc][2 (p, q)][rows] + meta [2][ppc][4]
-__global__ void __cluster_dims__(JC_CL, 1, 1) __launch_bounds__(256)
-    k_svd_jacobi_cluster(const double* __restrict__ M, int rows, int cols, int ppc, double* __restrict__ U,
-                         double* __restrict__ sig, double* __restrict__ work) {
-  extern __shared__ __align__(16) double jcs[];
-  __shared__ int rot_flag;
-  __shared__ int stop_all;
+template <int CL>
+__device__ __forceinline__ void jc_sync(cg::cluster_group& cluster) {
+  if constexpr (CL == 1)
+    __syncthreads();
+  else
+    cluster.sync();
+}
+template <int CL, typename T>
+__device__ __forceinline__ T* jc_map(cg::cluster_group& cluster, T* p, int r) {
+  if constexpr (CL == 1)
+    return p;
+  else
+    return cluster.map_shared_rank(p, r);
+}
+
+// smem per CTA: slots [2 buf][ppc][2 (p, q)][E] + meta [2][ppc][4].
+// CL = 1: every pair in one CTA (16 lanes per pair, up to 32 pairs), one
+// __syncthreads per round instead of a cluster barrier (small l).
+template <int CL, int RPL>
+__device__ __forceinline__ void jc_body(const double* __restrict__ M, int rows, int cols, int ppc,
+                                        double* __restrict__ U, double* __restrict__ sig,
+                                        double* __restrict__ Vout, double* __restrict__ work, double* jcs,
+                                        int& rot_flag, int& stop_all) {
   cg::cluster_group cluster = cg::this_cluster();
-  const int rank = (int)cluster.block_rank();
+  const int rank = CL == 1 ? 0 : (int)cluster.block_rank();
   const int t = threadIdx.x, hl = t & 15, lp = t >> 4;  // local pair
   const int m = cols + (cols & 1), np = m / 2;
   const int k = rank * ppc + lp;                        // global pair index
   const bool act = lp < ppc && k < np;
-  const size_t slot_sz = (size_t)rows;
+  const int E = rows + (Vout ? cols : 0);               // extended column length
+  const size_t slot_sz = (size_t)E;
   double* slots = jcs;                                  // [2][ppc][2][rows]
-  double* meta = jcs + 2 * (size_t)ppc * 2 * rows;      // [2][ppc][4]: idp, nrm_p, idq, nrm_q
+  double* meta = jcs + 2 * (size_t)ppc * 2 * E;         // [2][ppc][4]: idp, nrm_p, idq, nrm_q
   const double tol2 = (double)rows * 2.220446049250313e-16 * 2.220446049250313e-16;
   const int src = (t & 31) & 16;                        // lane 0 of this half-warp
   auto hsum = [&](double v) {
@@ -57,29 +75,35 @@ __global__ void __cluster_dims__(JC_CL, 1, 1) __launch_bounds__(256)
     return __shfl_sync(0xffffffffu, v, src);
   };
   int idp = k, idq = m - 1 - k;
-  double xp[JC_RPL], xq[JC_RPL];
+  double xp[RPL], xq[RPL];
 #pragma unroll
-  for (int r = 0; r < JC_RPL; ++r) {
+  for (int r = 0; r < RPL; ++r) {
     const int i = hl + 16 * r;
-    xp[r] = (act && i < rows && idp < cols) ? M[i + (size_t)idp * rows] : 0.0;
-    xq[r] = (act && i < rows && idq < cols) ? M[i + (size_t)idq * rows] : 0.0;
+    if (i < rows) {
+      xp[r] = (act && idp < cols) ? M[i + (size_t)idp * rows] : 0.0;
+      xq[r] = (act && idq < cols) ? M[i + (size_t)idq * rows] : 0.0;
+    } else {
+      xp[r] = (act && i < E && i - rows == idp) ? 1.0 : 0.0;
+      xq[r] = (act && i < E && i - rows == idq) ? 1.0 : 0.0;
+    }
   }
   // where pair kk's slot lives: CTA kk / ppc, local kk % ppc
   auto slot_of = [&](int buf, int kk, int which) -> double* {
     double* local = slots + (((size_t)buf * ppc + (kk % ppc)) * 2 + which) * slot_sz;
-    return cluster.map_shared_rank(local, kk / ppc);
+    return jc_map<CL>(cluster, local, kk / ppc);
   };
   auto meta_of = [&](int buf, int kk) -> double* {
     double* local = meta + ((size_t)buf * ppc + (kk % ppc)) * 4;
-    return cluster.map_shared_rank(local, kk / ppc);
+    return jc_map<CL>(cluster, local, kk / ppc);
   };
   int buf = 0, sweep = 0;
   for (; sweep < 40; ++sweep) {
     double al = 0.0, be = 0.0;
 #pragma unroll
-    for (int r = 0; r < JC_RPL; ++r) {
-      al = fma(xp[r], xp[r], al);
-      be = fma(xq[r], xq[r], be);
+    for (int r = 0; r < RPL; ++r) {
+      const bool in = hl + 16 * r < rows;
+      al = fma(in ? xp[r] : 0.0, xp[r], al);
+      be = fma(in ? xq[r] : 0.0, xq[r], be);
     }
     al = hsum(al);
     be = hsum(be);
@@ -88,7 +112,7 @@ __global__ void __cluster_dims__(JC_CL, 1, 1) __launch_bounds__(256)
     for (int rd = 0; rd < m - 1; ++rd) {
       double ga = 0.0;
 #pragma unroll
-      for (int r = 0; r < JC_RPL; ++r) ga = fma(xp[r], xq[r], ga);
+      for (int r = 0; r < RPL; ++r) ga = fma(hl + 16 * r < rows ? xp[r] : 0.0, xq[r], ga);
       ga = hsum(ga);
       if (act && al > 0.0 && be > 0.0 && ga * ga > tol2 * (al * be)) {
         const double zeta = (be - al) * jc_rcp(2.0 * ga);
@@ -96,7 +120,7 @@ __global__ void __cluster_dims__(JC_CL, 1, 1) __launch_bounds__(256)
         const double tt = copysign(jc_rcp(fabs(zeta) + z2 * rsqrt(z2)), zeta);
         const double c = rsqrt(fma(tt, tt, 1.0)), sn = c * tt;
 #pragma unroll
-        for (int r = 0; r < JC_RPL; ++r) {
+        for (int r = 0; r < RPL; ++r) {
           const double x = xp[r], y = xq[r];
           xp[r] = c * x - sn * y;
           xq[r] = sn * x + c * y;
@@ -110,9 +134,9 @@ __global__ void __cluster_dims__(JC_CL, 1, 1) __launch_bounds__(256)
         double* sp = slots + (((size_t)buf * ppc + lp) * 2 + 0) * slot_sz;
         double* sq = slots + (((size_t)buf * ppc + lp) * 2 + 1) * slot_sz;
 #pragma unroll
-        for (int r = 0; r < JC_RPL; ++r) {
+        for (int r = 0; r < RPL; ++r) {
           const int i = hl + 16 * r;
-          if (i < rows) {
+          if (i < E) {
             sp[i] = xp[r];
             sq[i] = xq[r];
           }
@@ -125,7 +149,7 @@ __global__ void __cluster_dims__(JC_CL, 1, 1) __launch_bounds__(256)
           mt[3] = be;
         }
       }
-      cluster.sync();
+      jc_sync<CL>(cluster);
       if (act) {
         // new p(k) = p(k+1) (1 <= k < np-1); new p(np-1) = q(np-1); p(0) stays
         // new q(k) = q(k-1) (k >= 1);        new q(0) = p(1)
@@ -133,16 +157,16 @@ __global__ void __cluster_dims__(JC_CL, 1, 1) __launch_bounds__(256)
         if (k >= 1) {
           if (last) {
 #pragma unroll
-            for (int r = 0; r < JC_RPL; ++r) xp[r] = xq[r];
+            for (int r = 0; r < RPL; ++r) xp[r] = xq[r];
             idp = idq;
             al = be;
           } else {
             const double* rp = slot_of(buf, k + 1, 0);
             const double* mt = meta_of(buf, k + 1);
 #pragma unroll
-            for (int r = 0; r < JC_RPL; ++r) {
+            for (int r = 0; r < RPL; ++r) {
               const int i = hl + 16 * r;
-              xp[r] = i < rows ? rp[i] : 0.0;
+              xp[r] = i < E ? rp[i] : 0.0;
             }
             idp = (int)mt[0];
             al = mt[1];
@@ -150,9 +174,9 @@ __global__ void __cluster_dims__(JC_CL, 1, 1) __launch_bounds__(256)
           const double* rq = slot_of(buf, k - 1, 1);
           const double* mq = meta_of(buf, k - 1);
 #pragma unroll
-          for (int r = 0; r < JC_RPL; ++r) {
+          for (int r = 0; r < RPL; ++r) {
             const int i = hl + 16 * r;
-            xq[r] = i < rows ? rq[i] : 0.0;
+            xq[r] = i < E ? rq[i] : 0.0;
           }
           idq = (int)mq[2];
           be = mq[3];
@@ -160,9 +184,9 @@ __global__ void __cluster_dims__(JC_CL, 1, 1) __launch_bounds__(256)
           const double* rp = slot_of(buf, 1, 0);
           const double* mt = meta_of(buf, 1);
 #pragma unroll
-          for (int r = 0; r < JC_RPL; ++r) {
+          for (int r = 0; r < RPL; ++r) {
             const int i = hl + 16 * r;
-            xq[r] = i < rows ? rp[i] : 0.0;
+            xq[r] = i < E ? rp[i] : 0.0;
           }
           idq = (int)mt[0];
           be = mt[1];
@@ -171,33 +195,37 @@ __global__ void __cluster_dims__(JC_CL, 1, 1) __launch_bounds__(256)
       buf ^= 1;
     }
     // any rotation anywhere in the cluster this sweep?
-    cluster.sync();
+    jc_sync<CL>(cluster);
     if (t == 0) {
       int any = 0;
-      for (int c = 0; c < JC_CL; ++c) any |= *cluster.map_shared_rank(&rot_flag, c);
+      for (int c = 0; c < CL; ++c) any |= *jc_map<CL>(cluster, &rot_flag, c);
       stop_all = !any;
     }
-    cluster.sync();  // every CTA has read every flag before they are reset
+    jc_sync<CL>(cluster);  // every CTA has read every flag before they are reset
     if (stop_all) break;
   }
   // columns back to the workspace by id; CTA 0 ranks and scatters
   double* A = work;
-  double* nrm = work + (size_t)rows * cols;
+  double* Vw = work + (size_t)rows * cols;
+  double* nrm = Vw + (size_t)cols * cols;
   if (act) {
 #pragma unroll
-    for (int r = 0; r < JC_RPL; ++r) {
+    for (int r = 0; r < RPL; ++r) {
       const int i = hl + 16 * r;
       if (i < rows) {
         if (idp < cols) A[i + (size_t)idp * rows] = xp[r];
         if (idq < cols) A[i + (size_t)idq * rows] = xq[r];
+      } else if (i < E) {
+        if (idp < cols) Vw[(i - rows) + (size_t)idp * cols] = xp[r];
+        if (idq < cols) Vw[(i - rows) + (size_t)idq * cols] = xq[r];
       }
     }
   }
-  if (rank == 0 && t == 0) work[(size_t)rows * cols + (size_t)cols * cols + cols] = (double)(sweep + 1);
+  if (rank == 0 && t == 0) nrm[cols] = (double)(sweep + 1);
   __threadfence();
-  cluster.sync();
+  jc_sync<CL>(cluster);
   if (rank != 0) return;
-  const int lane = t & 31, warp = t >> 5, nw = 256 / 32;
+  const int lane = t & 31, warp = t >> 5, nw = blockDim.x / 32;
   for (int j = warp; j < cols; j += nw) {
     double s = 0.0;
     const double* a = A + (size_t)j * rows;
@@ -218,24 +246,59 @@ __global__ void __cluster_dims__(JC_CL, 1, 1) __launch_bounds__(256)
     const double* a = A + (size_t)j * rows;
     double* u = U + (size_t)rk * rows;
     for (int i = lane; i < rows; i += 32) u[i] = a[i] * inv;
+    if (Vout) {
+      const double* v = Vw + (size_t)j * cols;
+      double* vo = Vout + (size_t)rk * cols;
+      for (int i = lane; i < cols; i += 32) vo[i] = v[i];
+    }
     if (lane == 0) sig[rk] = sj;
   }
 }
 
-// returns -1 when the shape is not handled by the cluster kernel
-int launch_svd_jacobi_cluster(const double* M, int rows, int cols, double* U, double* sig, double* work,
-                              cudaStream_t st) {
-  if (rows > JC_MAXROWS || cols > rows || cols < 2) return -1;
+__global__ void __cluster_dims__(JC_CL, 1, 1) __launch_bounds__(256)
+    k_svd_jacobi_cluster(const double* __restrict__ M, int rows, int cols, int ppc, double* __restrict__ U,
+                         double* __restrict__ sig, double* __restrict__ Vout, double* __restrict__ work) {
+  extern __shared__ __align__(16) double jcs[];
+  __shared__ int rot_flag, stop_all;
+  jc_body<JC_CL, JC_MAXROWS / 16>(M, rows, cols, ppc, U, sig, Vout, work, jcs, rot_flag, stop_all);
+}
+
+constexpr int JT_MAXE = 128;  // one-CTA variant: extended column length <= 128 (8 rows per lane)
+// measured (tools/jacobi_probe.py): one CTA wins up to ~20 pairs (50x40 with
+// V: 0.30 vs 0.33 ms), the 8-CTA cluster from 32 pairs (64x64: 0.67 vs 0.74)
+constexpr int JT_MAXPAIRS = 24;
+
+__global__ void __launch_bounds__(512)
+    k_svd_jacobi_cta(const double* __restrict__ M, int rows, int cols, int ppc, double* __restrict__ U,
+                     double* __restrict__ sig, double* __restrict__ Vout, double* __restrict__ work) {
+  extern __shared__ __align__(16) double jcs[];
+  __shared__ int rot_flag, stop_all;
+  jc_body<1, JT_MAXE / 16>(M, rows, cols, ppc, U, sig, Vout, work, jcs, rot_flag, stop_all);
+}
+
+// returns -1 when the shape is not handled by the register kernels
+int launch_svd_jacobi_cluster(const double* M, int rows, int cols, double* U, double* sig, double* V,
+                              double* work, cudaStream_t st) {
+  const int E = rows + (V ? cols : 0);
+  if (E > JC_MAXROWS || cols > rows || cols < 2) return -1;
   const int m = cols + (cols & 1), np = m / 2;
-  const int ppc = (np + JC_CL - 1) / JC_CL;
-  if (ppc * 16 > 256) return -1;
-  const size_t smem = (2 * (size_t)ppc * 2 * rows + 2 * (size_t)ppc * 4) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_svd_jacobi_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_svd_jacobi_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_svd_jacobi_cluster<<<JC_CL, 256, smem, st>>>(M, rows, cols, ppc, U, sig, work);
+  const char* force = getenv("EDAK_JACOBI_CLUSTER");
+  if (E <= JT_MAXE && np <= JT_MAXPAIRS && !(force && force[0] == '1')) {
+    const size_t smem = (2 * (size_t)np * 2 * E + 2 * (size_t)np * 4) * sizeof(double);
+    k_svd_jacobi_cta<<<1, ((16 * np + 31) / 32) * 32, smem, st>>>(M, rows, cols, np, U, sig, V, work);
+    count_launch();
+    return check_launch("k_svd_jacobi_cta");
+  }
+  const int ppc = (np + JC_CL - 1) / JC_CL;
+  if (ppc * 16 > 256) return -1;
+  const size_t smem = (2 * (size_t)ppc * 2 * E + 2 * (size_t)ppc * 4) * sizeof(double);
+  k_svd_jacobi_cluster<<<JC_CL, 256, smem, st>>>(M, rows, cols, ppc, U, sig, V, work);
   count_launch();
   return check_launch("k_svd_jacobi_cluster");
 }

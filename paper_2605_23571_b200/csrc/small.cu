@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(JAC_NT) k_svd_jacobi(const double* __restrict_
   }
 }
 
-int launch_svd_jacobi_cluster(const double*, int, int, double*, double*, double*, cudaStream_t);
+int launch_svd_jacobi_cluster(const double*, int, int, double*, double*, double*, double*, cudaStream_t);
 
 int64_t svd_work_doubles(int rows, int cols) { return (int64_t)rows * cols + (int64_t)cols * cols + cols + 1; }
 
@@ -409,8 +409,8 @@ int launch_svd_jacobi(const double* M, int rows, int cols, double* U, double* si
     cudaFuncSetAttribute(k_svd_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit);
     attr = true;
   }
-  if (!V && !getenv("EDAK_JACOBI_SINGLE")) {  // 8-SM cluster variant (jacobi_cluster.cu)
-    const int rc = launch_svd_jacobi_cluster(M, rows, cols, U, sig, work, st);
+  if (!getenv("EDAK_JACOBI_SINGLE")) {  // 8-SM cluster variant (jacobi_cluster.cu)
+    const int rc = launch_svd_jacobi_cluster(M, rows, cols, U, sig, V, work, st);
     if (rc >= 0) return rc;
   }
   k_svd_jacobi<<<1, JAC_NT, smem, st>>>(M, rows, cols, U, sig, V, work, mode);

@@ -71,22 +71,21 @@ class PcgBreakdown(RuntimeError):
 
 
 def _traces(status, iters, hist_rz, hist_J, trace_cost):
+    bad = np.flatnonzero(status >= 2)
+    if bad.size:
+        c = int(bad[0])
+        if status[c] == 3:
+            raise PcgBreakdown("preconditioner is not positive definite", c)
+        raise PcgBreakdown(f"system matrix is not positive definite (iteration {int(iters[c])})", c)
+    resn = np.sqrt(np.maximum(hist_rz, 0.0))
     out = []
     for c in range(status.shape[0]):
-        st, it = int(status[c]), int(iters[c])
-        if st == 3:
-            raise PcgBreakdown("preconditioner is not positive definite", c)
-        if st == 2:
-            raise PcgBreakdown(f"system matrix is not positive definite (iteration {it})", c)
-        tr = SolveTrace()
-        last = it
-        tr.iterations = list(range(last + 1))
-        tr.matvecs = list(range(last + 1))
-        rz = hist_rz[c, : last + 1]
-        tr.resnorm = [float(np.sqrt(max(v, 0.0))) for v in rz]
-        tr.cost = ([float(v) for v in hist_J[c, : last + 1]] if trace_cost
-                   else [float("nan")] * (last + 1))
-        tr.status = "converged" if st == 1 else "max_iters"
+        last = int(iters[c])
+        rng = list(range(last + 1))
+        tr = SolveTrace(iterations=rng, matvecs=list(rng), resnorm=resn[c, : last + 1].tolist(),
+                        cost=(hist_J[c, : last + 1].tolist() if trace_cost
+                              else [float("nan")] * (last + 1)),
+                        status="converged" if status[c] == 1 else "max_iters")
         out.append(tr)
     return out
 
@@ -295,22 +294,23 @@ def pcg_members_small(ens, B, cfg, lmp=None, cost="recurrence"):
     dev = B.device
     L = cfg.max_iters + 1
     X = torch.empty_like(B)
-    hist_rz = torch.zeros((M, L), dtype=torch.float64, device=dev)
+    # one device buffer (hist_rz | hist_J | status, iters) -> one host copy
+    buf = torch.empty(2 * M * L + M, dtype=torch.float64, device=dev)
+    hist_rz, hist_J = buf[:M * L].view(M, L), buf[M * L:2 * M * L].view(M, L)
+    si = buf[2 * M * L:].view(torch.int32)
     trace = bool(cfg.trace_cost and cost == "recurrence")
-    hist_J = torch.full((M, L), float("nan"), dtype=torch.float64, device=dev)
-    status = torch.zeros(M, dtype=torch.int32, device=dev)
-    iters = torch.zeros(M, dtype=torch.int32, device=dev)
     rtol = -1.0 if cfg.residual_rtol is None else float(cfg.residual_rtol)
     S, coef = (None, None) if lmp is None else (lmp[0].contiguous(), lmp[1].contiguous())
-    ct = ens.traj_of
-    _lib.call("edak_pcg_small", _lib.C.byref(ens.lin._P), _lib.ptr(ct), M, B.data_ptr(),
+    _lib.call("edak_pcg_small", _lib.C.byref(ens.lin._P), ens.traj_of.data_ptr(), M, B.data_ptr(),
               ens.D.data_ptr() if trace else None, _lib.ptr(S), _lib.ptr(coef),
               0 if S is None else S.shape[0], cfg.max_iters, rtol, X.data_ptr(),
-              hist_rz.data_ptr(), hist_J.data_ptr() if trace else None, L, status.data_ptr(),
-              iters.data_ptr(), _lib.stream())
+              hist_rz.data_ptr(), hist_J.data_ptr() if trace else None, L, si.data_ptr(),
+              si[M:].data_ptr(), _lib.stream())
     ens.n_matvecs += cfg.max_iters
-    return X, _traces(status.cpu().numpy(), iters.cpu().numpy(), hist_rz.cpu().numpy(),
-                      hist_J.cpu().numpy(), trace)
+    h = buf.cpu().numpy()
+    hs = h[2 * M * L:].view(np.int32)
+    return X, _traces(hs[:M], hs[M:], h[:M * L].reshape(M, L), h[M * L:2 * M * L].reshape(M, L),
+                      trace)
 
 
 def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fused=True,

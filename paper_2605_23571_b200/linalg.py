@@ -94,4 +94,14 @@ def svd_jacobi(M, want_v=False):
     work = _empty(int(_lib.lib().edak_svd_work_doubles(rows, cols)), like=M)
     _lib.call("edak_svd_jacobi", M.data_ptr(), rows, cols, U.data_ptr(), sig.data_ptr(),
               _lib.ptr(V), work.data_ptr(), _lib.stream())
+    _LAST_SVD[0] = work  # diagnostics: work[-1] = sweeps of the last call (last_svd_sweeps)
     return U, sig, V
+
+
+_LAST_SVD = [None]
+
+
+def last_svd_sweeps():
+    """Jacobi sweeps of the most recent svd_jacobi call (synchronises)."""
+    w = _LAST_SVD[0]
+    return None if w is None else int(w[-1].item())

@@ -80,9 +80,17 @@ def test_potrf_paths(gpu):
     assert potrf_shifted(Z, 2, 0.0)[2].cpu().tolist()[1] == 1
 
 
-@pytest.mark.parametrize("rows,cols", [(10, 10), (64, 64), (1024, 64), (128, 128), (50, 40)])
-def test_svd_jacobi(gpu, rows, cols):
+@pytest.mark.parametrize("kind", ["auto", "single", "cluster"])
+@pytest.mark.parametrize("rows,cols", [(10, 10), (64, 64), (1024, 64), (128, 128), (50, 40), (200, 50)])
+def test_svd_jacobi(gpu, rows, cols, kind, monkeypatch):
+    """Shared-memory single-CTA, register one-CTA (auto for small l) and
+    8-CTA cluster Jacobi (both register kernels carry V as the tail of each
+    extended column when rows + cols fits)."""
     from paper_2605_23571_b200.linalg import svd_jacobi
+    if kind == "single":
+        monkeypatch.setenv("EDAK_JACOBI_SINGLE", "1")
+    if kind == "cluster":
+        monkeypatch.setenv("EDAK_JACOBI_CLUSTER", "1")
     rng = np.random.default_rng(rows + cols)
     m = rng.standard_normal((rows, cols)) * np.logspace(0, -6, cols)
     U, sig, V = svd_jacobi(torch.tensor(m.T.copy(), device="cuda"), want_v=True)
@@ -92,6 +100,7 @@ def test_svd_jacobi(gpu, rows, cols):
     v = V.cpu().numpy().T
     npt.assert_allclose(u * sig.cpu().numpy(), m @ v, atol=1e-12 * s_ref[0])
     npt.assert_allclose(u.T @ u, np.eye(cols), atol=1e-12)
+    npt.assert_allclose(v.T @ v, np.eye(cols), atol=1e-12)
 
 
 def _lmp_action_close(ours, ref_vecs, ref_vals, theta, n, tol):
