@@ -451,7 +451,8 @@ static void go(K kernel, dim3 grid, cudaStream_t st, Args... args) {
 }
 
 // pick (C, NT) and tile geometry for a sweep with halos (hl, hr) per step
-static bool plan(int n, int hl_total, int hr_total, int& C, int& NT, SweepGeom& geo, int& ntiles) {
+static bool plan(int n, int hl_total, int hr_total, int& C, int& NT, SweepGeom& geo, int& ntiles,
+                 bool sweep = true) {
   // periodic single tile: the whole ring in one CTA (no halo redundancy)
   const int cand_p[][2] = {{8, 128}, {4, 64}, {4, 128}, {4, 256}, {4, 512},
                            {2, 64}, {2, 128}, {2, 256}, {2, 512}};
@@ -471,7 +472,8 @@ static bool plan(int n, int hl_total, int hr_total, int& C, int& NT, SweepGeom& 
   // fastest on B200 for the cfg4 sweeps (tools/ab_sweeps.py, profiles/)
   C = 8;
   NT = 128;
-  if (const char* f = getenv("EDAK_SWEEP_FAMILY")) {  // A/B testing: "C,NT"
+  const char* f = sweep ? getenv("EDAK_SWEEP_FAMILY") : nullptr;
+  if (f) {  // A/B testing of the TL/AD sweeps: "C,NT"
     int c2 = 0, t2 = 0;
     if (sscanf(f, "%d,%d", &c2, &t2) == 2) {
       C = c2;
@@ -539,6 +541,18 @@ static bool pair_ok(const edak_problem* P, const SweepGeom& geo) {
          (geo.periodic || (geo.W % 2 == 0 && geo.HL % 2 == 0));
 }
 
+// the tile family the pair-staged sweeps run: same 1024-element range as
+// (8, 128) but 16 elements per thread on 64 threads -- twice the independent
+// DP chains per thread and half the exchange traffic per element (cfg4: TL
+// 0.354 -> 0.341, AD 0.412 -> 0.398 ms per sweep, tools/ab_tiles.py)
+static void widen_pairs(const edak_problem* P, bool stream, int& C, int& NT, SweepGeom& geo) {
+  const char* fam = getenv("EDAK_SWEEP_FAMILY");  // explicit A/B family wins
+  if (C != 8 || NT != 128 || stream || geo.periodic || !pair_ok(P, geo) || (fam && *fam)) return;
+  C = 16;
+  NT = 64;
+  geo.nact = NT;
+}
+
 int sweep2_mode(const edak_problem* P, int K);
 int sweep3_mode(const edak_problem* P, int K);
 int launch_tl3(const edak_problem*, const double*, double*, int, const int32_t*, int, int, double*, cudaStream_t);
@@ -600,6 +614,7 @@ v1:
       set_error("window chunk too long for the tile family");
       return EDAK_EUNSUPPORTED;
     }
+    widen_pairs(P, stream, C, NT, geo);
     const double* vin = c == 0 ? v0 : work2 + (size_t)((c - 1) & 1) * blk;
     double* vout = c + 1 < nch ? work2 + (size_t)(c & 1) * blk : nullptr;
     dim3 grid(nt, ncols);
@@ -607,6 +622,12 @@ v1:
     const int mb = env_int("EDAK_TL_MINB", 4);
     if (C == 8 && NT == 128 && !stream && mb == 4 && pair_ok(P, geo)) {
       go<128, 8>(k_tl<8, 128, false, 4, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
+    } else if (C == 16 && NT == 64 && !stream && pair_ok(P, geo)) {  // A/B (EDAK_SWEEP_FAMILY=16,64)
+      go<64, 16>(k_tl<16, 64, false, 4, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
+    } else if (C == 16 && NT == 128 && !stream && pair_ok(P, geo)) {
+      go<128, 16>(k_tl<16, 128, false, 2, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
+    } else if (C == 12 && NT == 96 && !stream && pair_ok(P, geo)) {
+      go<96, 12>(k_tl<12, 96, false, 4, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
     } else if (C == 8 && NT == 256 && !stream && pair_ok(P, geo)) {
       go<256, 8>(k_tl<8, 256, false, 2, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
     } else if (C == 8 && NT == 128 && !stream && mb == 3) {
@@ -675,6 +696,7 @@ v1:
       set_error("window chunk too long for the tile family");
       return EDAK_EUNSUPPORTED;
     }
+    widen_pairs(P, stream, C, NT, geo);
     const double* gin = k == 0 ? nullptr : work2 + (size_t)((k - 1) & 1) * blk;
     double* gout = c == 0 ? g : work2 + (size_t)(k & 1) * blk;
     dim3 grid(nt, ncols);
@@ -682,6 +704,15 @@ v1:
     const int mb = env_int("EDAK_AD_MINB", 3);
     if (C == 8 && NT == 128 && !stream && mb == 3 && pair_ok(P, geo)) {
       go<128, 8, 2 * 8 * 128>(k_ad<8, 128, false, 3, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1,
+                              gin);
+    } else if (C == 16 && NT == 64 && !stream && pair_ok(P, geo)) {  // A/B (EDAK_SWEEP_FAMILY=16,64)
+      go<64, 16, 2 * 16 * 64>(k_ad<16, 64, false, 3, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1,
+                              gin);
+    } else if (C == 16 && NT == 128 && !stream && pair_ok(P, geo)) {
+      go<128, 16, 2 * 16 * 128>(k_ad<16, 128, false, 1, true>, grid, st, *P, forcing, gout, col_traj, geo, s0,
+                                s1, gin);
+    } else if (C == 12 && NT == 96 && !stream && pair_ok(P, geo)) {
+      go<96, 12, 2 * 12 * 96>(k_ad<12, 96, false, 2, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1,
                               gin);
     } else if (C == 8 && NT == 256 && !stream && pair_ok(P, geo)) {
       go<256, 8, 2 * 8 * 256>(k_ad<8, 256, false, 1, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1,
@@ -719,9 +750,9 @@ int launch_integrate(int n, int n_steps, double dt, double F, const double* x0, 
   }
   while (s0 < n_steps) {
     int K = n_steps - s0;
-    if (!plan(n, 8 * K + 4, 4 * K + 4, C, NT, geo, nt) || (!geo.periodic && K > Kmax)) {
+    if (!plan(n, 8 * K + 4, 4 * K + 4, C, NT, geo, nt, false) || (!geo.periodic && K > Kmax)) {
       K = K < Kmax ? K : Kmax;
-      if (!plan(n, 8 * K + 4, 4 * K + 4, C, NT, geo, nt)) {
+      if (!plan(n, 8 * K + 4, 4 * K + 4, C, NT, geo, nt, false)) {
         set_error("integrate: no tile plan");
         return EDAK_EUNSUPPORTED;
       }
