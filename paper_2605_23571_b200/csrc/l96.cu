@@ -116,7 +116,7 @@ __device__ __forceinline__ void tl_sub_d(const double (&u)[C + 4], const double 
   for (int j = 0; j < C; ++j) a[j] = l96_tl_d(u[j + 3], u[j], u[j + 1], u[j + 2], d[j], x[j + 1]);
 }
 
-template <int C, int NT, bool STREAM, int MINB = 1, bool PAIR = false>
+template <int C, int NT, bool STREAM, int MINB = 1, bool PAIR = false, int DEPTH = 1>
 __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* __restrict__ vin,
                                            double* __restrict__ obs, const int32_t* __restrict__ col_traj,
                                            SweepGeom geo, int s0, int s1, double* __restrict__ vout) {
@@ -166,25 +166,36 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
   // software pipeline: the state of step s+1 is staged (cp.async, coalesced)
   // into the other shared buffer while step s runs; STREAM reads stored
   // stages straight from memory
+  // DEPTH = 1: X_{s+1} is staged during step s (two buffers); DEPTH = 2: X_{s+2}
+  // (three buffers, one empty commit group past the window end so that
+  // wait_group DEPTH - 1 always means "X_s has landed")
   using SS = std::conditional_t<PAIR, Stage2<C, NT>, Stage<C, NT>>;
+  constexpr int NB = DEPTH + 1;
   double* XB0 = dsm_ + sizeof(XBuf<NT>) / sizeof(double);
-  double* XB1 = XB0 + SS::PLEN;
   const int used = R.nact * C;
   const int gst = PAIR ? R.base - 2 : wrap(R.base - 2 + (int)threadIdx.x, n);
   const size_t sstride = STREAM ? (size_t)4 * n : (size_t)n;
-  if (!STREAM) SS::stage((s0 & 1) ? XB1 : XB0, tr + (size_t)s0 * n, gst, n, used);
+  auto sbuf = [&](int level) { return XB0 + (size_t)(level % NB) * SS::PLEN; };
+  if (!STREAM) {
+#pragma unroll
+    for (int d = 0; d < DEPTH; ++d) {
+      if (s0 + d < s1) SS::stage(sbuf(s0 + d), tr + (size_t)(s0 + d) * n, gst, n, used);
+      else cp_commit();
+    }
+  }
 #pragma unroll 1
   for (int s = s0; s < s1; ++s) {
     const double* Xs = tr + (size_t)s * sstride;
     const int tp_next = __ldg(P.tpos + s + 1);  // consumed at the end of the step
     double X[C + 4];
-    if (!STREAM) cp_wait_all();
+    if (!STREAM) cp_wait_group<DEPTH - 1>();
     xchg1(R, xb, buf, v);  // barrier: staged X_s visible, X_{s-1}'s buffer free
     if (STREAM) {
       R.load_halo(Xs, X);
     } else {
-      if (s + 1 < s1) SS::stage(((s + 1) & 1) ? XB1 : XB0, Xs + n, gst, n, used);
-      SS::win((s & 1) ? XB1 : XB0, R.t, X);
+      if (s + DEPTH < s1) SS::stage(sbuf(s + DEPTH), Xs + (size_t)DEPTH * n, gst, n, used);
+      else if (DEPTH > 1) cp_commit();
+      SS::win(sbuf(s), R.t, X);
     }
     double acc[C], a[C], kk[C], dd[C];
     double x2[C + 4], u2[C + 4];
@@ -271,7 +282,7 @@ __device__ __forceinline__ void ad_sub(const double (&w)[C + 4], const double (&
     u[j] = l96_ad(x[j], x[j + 1], x[j + 3], x[j + 4], w[j + 1], w[j + 2], w[j + 3], w[j + 4]);
 }
 
-template <int C, int NT, bool STREAM, int MINB = 1, bool PAIR = false>
+template <int C, int NT, bool STREAM, int MINB = 1, bool PAIR = false, int DEPTH = 1>
 __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* __restrict__ forcing,
                                            double* __restrict__ gout, const int32_t* __restrict__ col_traj,
                                            SweepGeom geo, int s0, int s1, const double* __restrict__ gin) {
@@ -295,9 +306,12 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
 
   // forcing w_all[level] at own elements: R^-1 d at observed points
   // (obs.py:54-56 with covariance.py:71: w / sigma**2), 0 elsewhere
+  double* FS = dsm_ + sizeof(XBuf<NT>) / sizeof(double) + (DEPTH + 1) * Stage2<C, NT>::PLEN;
   int gp[C];
 #pragma unroll
   for (int j = 0; j < C; ++j) gp[j] = __ldg(P.gpos + R.gidx(j));
+  auto is_obs = [&](int j) { return gp[j] >= 0; };
+  auto gpos_of = [&](int j) { return gp[j]; };
   // (the reference divides by sigma**2; we multiply by its reciprocal, a
   // 0.5-ulp difference inside the 1e-12 parity budget, and hoist the level
   // lookup: an IEEE division per observed element cost ~12 DP instructions)
@@ -308,27 +322,26 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
     const double* f = fc + (size_t)tp * G;
 #pragma unroll
     for (int j = 0; j < C; ++j)
-      if (gp[j] >= 0) gg[j + 2] += __ldg(f + gp[j]) * inv_s2;
+      if (is_obs(j)) gg[j + 2] += __ldg(f + gpos_of(j)) * inv_s2;
   };
   // PAIR path: the forcing of level s is fetched by cp.async into per-thread
   // smem slots at the start of step s (with the next state tile) and added at
   // its end, so its global latency hides behind the step instead of stalling
   // every warp of the CTA at once (long_scoreboard in the ncu profile)
-  double* FS = dsm_ + sizeof(XBuf<NT>) / sizeof(double) + 2 * Stage2<C, NT>::PLEN;
   auto fetch_force = [&](int tp, int sbuf) {
     if (tp < 0) return;
     const double* f = fc + (size_t)tp * G;
     double* d = FS + (size_t)sbuf * C * NT + threadIdx.x;
 #pragma unroll
     for (int j = 0; j < C; ++j)
-      if (gp[j] >= 0) cp_async8(d + j * NT, f + gp[j]);
+      if (is_obs(j)) cp_async8(d + j * NT, f + gpos_of(j));
   };
   auto add_fetched = [&](int tp, int sbuf, double (&gg)[C + 4]) {
     if (tp < 0) return;
     const double* d = FS + (size_t)sbuf * C * NT + threadIdx.x;
 #pragma unroll
     for (int j = 0; j < C; ++j)
-      if (gp[j] >= 0) gg[j + 2] += d[j * NT] * inv_s2;
+      if (is_obs(j)) gg[j + 2] += d[j * NT] * inv_s2;
   };
 
   // window chunk [s0, s1), swept backward: g enters at level s1 (w_all[N]
@@ -342,17 +355,30 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
     add_force(N, g);
   }
 
+  // DEPTH = 1: X_{s-1} (and the forcing of level s-1) is staged during step s
+  // into the buffer X_{s+1} used.  DEPTH = 2: X_{s-2} is staged during step s
+  // (three buffers); the forcing of level s is fetched at the start of step s
+  // into per-thread slots, in its own commit group ahead of X_{s-2}'s, so the
+  // end-of-step wait_group 1 covers both it and X_{s-1}
   using SS = std::conditional_t<PAIR, Stage2<C, NT>, Stage<C, NT>>;
+  constexpr int NB = DEPTH + 1;
   double* XB0 = dsm_ + sizeof(XBuf<NT>) / sizeof(double);
-  double* XB1 = XB0 + SS::PLEN;
   const int used = R.nact * C;
   const int gst = PAIR ? R.base - 2 : wrap(R.base - 2 + (int)threadIdx.x, n);
   const size_t sstride = STREAM ? (size_t)4 * n : (size_t)n;
+  auto sbuf = [&](int level) { return XB0 + (size_t)(level % NB) * SS::PLEN; };
   int tp_cur = PAIR ? __ldg(P.tpos + s1 - 1) : -1;
   if (!STREAM) {
-    if (PAIR) fetch_force(tp_cur, (s1 - 1) & 1);
-    SS::stage(((s1 - 1) & 1) ? XB1 : XB0, tr + (size_t)(s1 - 1) * n, gst, n, used);
-    cp_wait_all();
+    if (DEPTH == 1) {
+      if (PAIR) fetch_force(tp_cur, (s1 - 1) & 1);
+      SS::stage(sbuf(s1 - 1), tr + (size_t)(s1 - 1) * n, gst, n, used);
+      cp_wait_all();
+    } else {
+      SS::stage(sbuf(s1 - 1), tr + (size_t)(s1 - 1) * n, gst, n, used);
+      if (s1 - 2 >= s0) SS::stage(sbuf(s1 - 2), tr + (size_t)(s1 - 2) * n, gst, n, used);
+      else cp_commit();
+      cp_wait_group<1>();
+    }
     __syncthreads();
   }
 #pragma unroll 1
@@ -361,7 +387,7 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
     const int tp_next = (PAIR && s > s0) ? __ldg(P.tpos + s - 1) : -1;
     double X[C + 4], x2[C + 4], x3[C + 4], x4[C + 4];
     if (STREAM) R.load_halo(Xs, X);
-    else SS::win((s & 1) ? XB1 : XB0, R.t, X);  // staged, published by the last barrier
+    else SS::win(sbuf(s), R.t, X);  // staged, published by the last barrier
     if (STREAM) {
       R.load_halo(Xs + n, x2);
       R.load_halo(Xs + 2 * n, x3);
@@ -371,10 +397,19 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
 #pragma unroll
       for (int j = 0; j < C; ++j) x2[j + 2] = axpy_rn(X[j + 2], h, l96_f(X[j + 3], X[j], X[j + 1], X[j + 2], F));
       xchg2(R, xb, buf, x2, g);
-      // X_{s-1} goes to the buffer X_{s+1} used: every thread read it last step
-      if (s > s0) {
-        if (PAIR) fetch_force(tp_next, (s - 1) & 1);  // same commit group as X_{s-1}
-        SS::stage(((s - 1) & 1) ? XB1 : XB0, Xs - n, gst, n, used);
+      if (DEPTH == 1) {
+        // X_{s-1} goes to the buffer X_{s+1} used: every thread read it last step
+        if (s > s0) {
+          if (PAIR) fetch_force(tp_next, (s - 1) & 1);  // same commit group as X_{s-1}
+          SS::stage(sbuf(s - 1), Xs - n, gst, n, used);
+        }
+      } else {
+        // X_{s-2} goes to the buffer X_{s+1} used (every thread is past this
+        // step's first barrier, so done with step s + 1)
+        if (PAIR) fetch_force(tp_cur, 0);
+        cp_commit();
+        if (s - 2 >= s0) SS::stage(sbuf(s - 2), Xs - 2 * n, gst, n, used);
+        else cp_commit();
       }
 #pragma unroll
       for (int j = 0; j < C; ++j)
@@ -416,13 +451,16 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
       vh[j] = fma(2.0, u[j], vh[j]);
       a[j + 2] = fma(dt, u[j], w[j]);  // a1
     }
-    if (!STREAM) cp_wait_all();  // X_{s-1} landed; published by this barrier
+    if (!STREAM) {  // X_{s-1} landed; published by this barrier
+      if (DEPTH == 1) cp_wait_all();
+      else cp_wait_group<1>();
+    }
     xchg1(R, xb, buf, a);
     ad_sub<C>(a, X, u);
 #pragma unroll
     for (int j = 0; j < C; ++j) g[j + 2] = vh[j] + u[j];
     if (PAIR) {
-      add_fetched(tp_cur, s & 1, g);
+      add_fetched(tp_cur, DEPTH == 1 ? (s & 1) : 0, g);
       tp_cur = tp_next;
     } else {
       add_force(s, g);
@@ -441,10 +479,10 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
 // ------------------------------------------------------------ launchers --
 
 // opt a kernel into > 48 KB of dynamic shared memory (idempotent)
-template <int NT, int C = 0, int EXTRA = 0, typename K, typename... Args>
+template <int NT, int C = 0, int EXTRA = 0, int NSB = 2, typename K, typename... Args>
 static void go(K kernel, dim3 grid, cudaStream_t st, Args... args) {
   const size_t bytes = sizeof(XBuf<NT>) +
-                       (C ? 2 * (size_t)Stage2<C ? (C + 1) / 2 * 2 : 2, NT>::PLEN * sizeof(double) : 0) +
+                       (C ? NSB * (size_t)Stage2<C ? (C + 1) / 2 * 2 : 2, NT>::PLEN * sizeof(double) : 0) +
                        (size_t)EXTRA * sizeof(double);
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   kernel<<<grid, NT, bytes, st>>>(args...);
@@ -525,6 +563,15 @@ static int sweep_chunk() {
   const char* e = getenv("EDAK_SWEEP_CHUNK");  // A/B knob
   const int v = e ? atoi(e) : SWEEP_CHUNK;
   return v >= 1 ? v : SWEEP_CHUNK;
+}
+
+// state-staging prefetch distance (1 or 2 steps ahead) of the pair-staged
+// sweeps.  Measured on B200 (tools/ab_knobs.py): TL 2 (cfg4 0.341 -> 0.334 ms
+// per sweep), AD 1 (2 is no faster at cfg4 and 2% slower at cfg5)
+static int sweep_depth(const char* knob, int dflt) {
+  const char* e = getenv(knob);
+  const int v = e ? atoi(e) : dflt;
+  return v == 2 ? 2 : 1;
 }
 
 static int plan_chunks(int N, bool periodic, const double* work2) {
@@ -622,8 +669,11 @@ v1:
     const int mb = env_int("EDAK_TL_MINB", 4);
     if (C == 8 && NT == 128 && !stream && mb == 4 && pair_ok(P, geo)) {
       go<128, 8>(k_tl<8, 128, false, 4, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
-    } else if (C == 16 && NT == 64 && !stream && pair_ok(P, geo)) {  // A/B (EDAK_SWEEP_FAMILY=16,64)
-      go<64, 16>(k_tl<16, 64, false, 4, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
+    } else if (C == 16 && NT == 64 && !stream && pair_ok(P, geo)) {  // the pair-staged default
+      if (sweep_depth("EDAK_TL_DEPTH", 2) == 2)
+        go<64, 16, 0, 3>(k_tl<16, 64, false, 4, true, 2>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
+      else
+        go<64, 16>(k_tl<16, 64, false, 4, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
     } else if (C == 16 && NT == 128 && !stream && pair_ok(P, geo)) {
       go<128, 16>(k_tl<16, 128, false, 2, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
     } else if (C == 12 && NT == 96 && !stream && pair_ok(P, geo)) {
@@ -705,9 +755,13 @@ v1:
     if (C == 8 && NT == 128 && !stream && mb == 3 && pair_ok(P, geo)) {
       go<128, 8, 2 * 8 * 128>(k_ad<8, 128, false, 3, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1,
                               gin);
-    } else if (C == 16 && NT == 64 && !stream && pair_ok(P, geo)) {  // A/B (EDAK_SWEEP_FAMILY=16,64)
-      go<64, 16, 2 * 16 * 64>(k_ad<16, 64, false, 3, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1,
-                              gin);
+    } else if (C == 16 && NT == 64 && !stream && pair_ok(P, geo)) {  // the pair-staged default
+      if (sweep_depth("EDAK_AD_DEPTH", 1) == 2)
+        go<64, 16, 16 * 64, 3>(k_ad<16, 64, false, 3, true, 2>, grid, st, *P, forcing, gout, col_traj, geo, s0,
+                                s1, gin);
+      else
+        go<64, 16, 2 * 16 * 64>(k_ad<16, 64, false, 3, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1,
+                                gin);
     } else if (C == 16 && NT == 128 && !stream && pair_ok(P, geo)) {
       go<128, 16, 2 * 16 * 128>(k_ad<16, 128, false, 1, true>, grid, st, *P, forcing, gout, col_traj, geo, s0,
                                 s1, gin);

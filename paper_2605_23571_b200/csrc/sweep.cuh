@@ -153,6 +153,8 @@ __device__ __forceinline__ void cp_async8z(double* dst, const double* src, bool 
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 template <int C, int NT>
 struct Stage {

@@ -229,6 +229,13 @@ def test_pair_staging_equals_generic(gpu, monkeypatch):
         assert torch.equal(hz, a.hessian_cols(z))
         assert torch.equal(rd, a.rhs_cols(d))
         monkeypatch.delenv("EDAK_NO_PAIR")
+        # staging prefetch distance 1 vs 2 steps (three-buffer ring): same bits
+        for knob in ("EDAK_TL_DEPTH", "EDAK_AD_DEPTH"):
+            for depth in ("1", "2"):
+                monkeypatch.setenv(knob, depth)
+                assert torch.equal(hz, a.hessian_cols(z)), (n, knob, depth)
+                assert torch.equal(rd, a.rhs_cols(d)), (n, knob, depth)
+            monkeypatch.delenv(knob)
 
 
 def test_model_obs_dropins_and_device_setup(gpu):
