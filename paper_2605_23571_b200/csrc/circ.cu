@@ -19,13 +19,13 @@ constexpr int CIRC_R = 8;
 constexpr int CIRC_NT = 128;
 constexpr int CIRC_MAXTAPS = 4096;
 
-__device__ __forceinline__ int padi(int q) { return q + q / CIRC_R; }
 
 template <int R, int NT>
 __global__ void __launch_bounds__(NT) k_circ(int n, const double* __restrict__ taps, int K, int Kp, int w,
                                              const double* __restrict__ in, double* __restrict__ out,
                                              double ident, const double* __restrict__ zadd,
                                              double* __restrict__ dotp) {
+  auto padi = [](int q) { return q + q / R; };
   extern __shared__ double sm[];
   double* st = sm;                      // reversed taps, Kp (zero padded)
   double* sg = sm + Kp;                 // segment, padded
@@ -38,10 +38,18 @@ __global__ void __launch_bounds__(NT) k_circ(int n, const double* __restrict__ t
   for (int m = t; m < Kp; m += NT) st[m] = m < K ? taps[K - 1 - m] : 0.0;
   const int seglen = NT * R + Kp + R;
   int g0 = wrap(i0 + w - K + 1, n);
-  for (int q = t; q < seglen; q += NT) {
-    int g = g0 + q % n;
-    if (g >= n) g -= n;
-    sg[padi(q)] = src[g];
+  if (seglen <= n) {  // the segment wraps the ring at most once: no modulo
+    for (int q = t; q < seglen; q += NT) {
+      int g = g0 + q;
+      if (g >= n) g -= n;
+      sg[padi(q)] = src[g];
+    }
+  } else {
+    for (int q = t; q < seglen; q += NT) {
+      int g = g0 + q % n;
+      if (g >= n) g -= n;
+      sg[padi(q)] = src[g];
+    }
   }
   __syncthreads();
 
@@ -109,17 +117,30 @@ int launch_circ(const edak_problem* P, const double* in, double* out, int ncols,
     set_error("circulant factor: tap count outside [1, 4096]");
     return EDAK_EUNSUPPORTED;
   }
-  const int Kp = (K + CIRC_R - 1) / CIRC_R * CIRC_R;
-  const int tile = CIRC_NT * CIRC_R;
+  // register blocking: R outputs per thread, 8 or 16 (knob EDAK_CIRC_R); both
+  // use 1024-output tiles, so the dot-partial layout is the same.  Measured
+  // on B200 (tools/ab_knobs.py): R = 16 takes cfg5's 377-tap U_B pair from
+  // ~2.2 to ~1.75 ms and cfg4's (189 taps) 3% faster, but is slower on
+  // one-tile rings (cfg3, n = 1024), so it is the default for long tap lists
+  // on long rings
+  const char* er = getenv("EDAK_CIRC_R");
+  const int R = er ? (atoi(er) == 16 ? 16 : CIRC_R) : (K >= 128 && n >= 8192 ? 16 : CIRC_R);
+  const int NT = CIRC_NT * CIRC_R / R;
+  const int Kp = (K + R - 1) / R * R;
+  const int tile = NT * R;
   dim3 grid((n + tile - 1) / tile, ncols);
-  const int seglen = tile + Kp + CIRC_R;
-  const size_t smem = (size_t)(Kp + seglen + seglen / CIRC_R + 1) * sizeof(double);
+  const int seglen = tile + Kp + R;
+  const size_t smem = (size_t)(Kp + seglen + seglen / R + 1) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_circ<CIRC_R, CIRC_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_circ<16, CIRC_NT / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_circ<CIRC_R, CIRC_NT><<<grid, CIRC_NT, smem, st>>>(n, P->taps, K, Kp, P->tap_w, in, out, ident, zadd, dotp);
+  if (R == 16)
+    k_circ<16, CIRC_NT / 2><<<grid, NT, smem, st>>>(n, P->taps, K, Kp, P->tap_w, in, out, ident, zadd, dotp);
+  else
+    k_circ<CIRC_R, CIRC_NT><<<grid, NT, smem, st>>>(n, P->taps, K, Kp, P->tap_w, in, out, ident, zadd, dotp);
   count_launch();
   return check_launch("k_circ");
 }

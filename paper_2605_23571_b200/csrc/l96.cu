@@ -116,13 +116,15 @@ __device__ __forceinline__ void tl_sub_d(const double (&u)[C + 4], const double 
   for (int j = 0; j < C; ++j) a[j] = l96_tl_d(u[j + 3], u[j], u[j + 1], u[j + 2], d[j], x[j + 1]);
 }
 
-template <int C, int NT, bool STREAM, int MINB = 1, bool PAIR = false, int DEPTH = 1>
+// WT: warp tile (NT == 32): halos by shuffles, no CTA barrier (sweep.cuh)
+template <int C, int NT, bool STREAM, int MINB = 1, bool PAIR = false, int DEPTH = 1, bool WT = false>
 __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* __restrict__ vin,
                                            double* __restrict__ obs, const int32_t* __restrict__ col_traj,
                                            SweepGeom geo, int s0, int s1, double* __restrict__ vout) {
+  static_assert(!WT || (NT == 32 && PAIR && !STREAM), "warp tiles: one warp, pair staging");
   extern __shared__ __align__(16) double dsm_[];
   XBuf<NT>& xb = *reinterpret_cast<XBuf<NT>*>(dsm_);
-  xb.init_pads();
+  if (!WT) xb.init_pads();
   Ring<C, NT> R;
   const int n = P.n;
   const int i0 = blockIdx.x * geo.W;
@@ -171,11 +173,17 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
   // wait_group DEPTH - 1 always means "X_s has landed")
   using SS = std::conditional_t<PAIR, Stage2<C, NT>, Stage<C, NT>>;
   constexpr int NB = DEPTH + 1;
-  double* XB0 = dsm_ + sizeof(XBuf<NT>) / sizeof(double);
+  double* XB0 = dsm_ + (WT ? 0 : sizeof(XBuf<NT>) / sizeof(double));
   const int used = R.nact * C;
   const int gst = PAIR ? R.base - 2 : wrap(R.base - 2 + (int)threadIdx.x, n);
   const size_t sstride = STREAM ? (size_t)4 * n : (size_t)n;
   auto sbuf = [&](int level) { return XB0 + (size_t)(level % NB) * SS::PLEN; };
+  auto X1 = [&](double (&a)[C + 4]) {
+    if constexpr (WT) wxchg1<C>(a); else xchg1(R, xb, buf, a);
+  };
+  auto X2 = [&](double (&a)[C + 4], double (&b)[C + 4]) {
+    if constexpr (WT) { wxchg1<C>(a); wxchg1<C>(b); } else xchg2(R, xb, buf, a, b);
+  };
   if (!STREAM) {
 #pragma unroll
     for (int d = 0; d < DEPTH; ++d) {
@@ -189,7 +197,8 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
     const int tp_next = __ldg(P.tpos + s + 1);  // consumed at the end of the step
     double X[C + 4];
     if (!STREAM) cp_wait_group<DEPTH - 1>();
-    xchg1(R, xb, buf, v);  // barrier: staged X_s visible, X_{s-1}'s buffer free
+    if constexpr (WT) __syncwarp();  // staged X_s visible, X_{s-1}'s buffer free
+    X1(v);  // (CTA tiles: its barrier does the same)
     if (STREAM) {
       R.load_halo(Xs, X);
     } else {
@@ -216,7 +225,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
       acc[j] = a[j];
       u2[j + 2] = fma(h, a[j], v[j + 2]);
     }
-    if (STREAM) xchg1(R, xb, buf, u2); else xchg2(R, xb, buf, x2, u2);
+    if (STREAM) X1(u2); else X2(x2, u2);
 
     double x3[C + 4], u3[C + 4];
 #pragma unroll
@@ -236,7 +245,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
       acc[j] = fma(2.0, a[j], acc[j]);
       u3[j + 2] = fma(h, a[j], v[j + 2]);
     }
-    if (STREAM) xchg1(R, xb, buf, u3); else xchg2(R, xb, buf, x3, u3);
+    if (STREAM) X1(u3); else X2(x3, u3);
 
     double x4[C + 4], u4[C + 4];
 #pragma unroll
@@ -256,7 +265,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
       acc[j] = fma(2.0, a[j], acc[j]);
       u4[j + 2] = fma(dt, a[j], v[j + 2]);
     }
-    if (STREAM) xchg1(R, xb, buf, u4); else xchg2(R, xb, buf, x4, u4);
+    if (STREAM) X1(u4); else X2(x4, u4);
 
     tl_sub<C>(u4, x4, a);
 #pragma unroll
@@ -282,13 +291,14 @@ __device__ __forceinline__ void ad_sub(const double (&w)[C + 4], const double (&
     u[j] = l96_ad(x[j], x[j + 1], x[j + 3], x[j + 4], w[j + 1], w[j + 2], w[j + 3], w[j + 4]);
 }
 
-template <int C, int NT, bool STREAM, int MINB = 1, bool PAIR = false, int DEPTH = 1>
+template <int C, int NT, bool STREAM, int MINB = 1, bool PAIR = false, int DEPTH = 1, bool WT = false>
 __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* __restrict__ forcing,
                                            double* __restrict__ gout, const int32_t* __restrict__ col_traj,
                                            SweepGeom geo, int s0, int s1, const double* __restrict__ gin) {
+  static_assert(!WT || (NT == 32 && PAIR && !STREAM), "warp tiles: one warp, pair staging");
   extern __shared__ __align__(16) double dsm_[];
   XBuf<NT>& xb = *reinterpret_cast<XBuf<NT>*>(dsm_);
-  xb.init_pads();
+  if (!WT) xb.init_pads();
   Ring<C, NT> R;
   const int n = P.n, N = P.n_steps;
   const int i0 = blockIdx.x * geo.W;
@@ -306,7 +316,7 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
 
   // forcing w_all[level] at own elements: R^-1 d at observed points
   // (obs.py:54-56 with covariance.py:71: w / sigma**2), 0 elsewhere
-  double* FS = dsm_ + sizeof(XBuf<NT>) / sizeof(double) + (DEPTH + 1) * Stage2<C, NT>::PLEN;
+  double* FS = dsm_ + (WT ? 0 : sizeof(XBuf<NT>) / sizeof(double)) + (DEPTH + 1) * Stage2<C, NT>::PLEN;
   int gp[C];
 #pragma unroll
   for (int j = 0; j < C; ++j) gp[j] = __ldg(P.gpos + R.gidx(j));
@@ -362,11 +372,14 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
   // end-of-step wait_group 1 covers both it and X_{s-1}
   using SS = std::conditional_t<PAIR, Stage2<C, NT>, Stage<C, NT>>;
   constexpr int NB = DEPTH + 1;
-  double* XB0 = dsm_ + sizeof(XBuf<NT>) / sizeof(double);
+  double* XB0 = dsm_ + (WT ? 0 : sizeof(XBuf<NT>) / sizeof(double));
   const int used = R.nact * C;
   const int gst = PAIR ? R.base - 2 : wrap(R.base - 2 + (int)threadIdx.x, n);
   const size_t sstride = STREAM ? (size_t)4 * n : (size_t)n;
   auto sbuf = [&](int level) { return XB0 + (size_t)(level % NB) * SS::PLEN; };
+  auto X1 = [&](double (&a)[C + 4]) {
+    if constexpr (WT) wxchg1<C>(a); else xchg1(R, xb, buf, a);
+  };
   int tp_cur = PAIR ? __ldg(P.tpos + s1 - 1) : -1;
   if (!STREAM) {
     if (DEPTH == 1) {
@@ -379,7 +392,7 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
       else cp_commit();
       cp_wait_group<1>();
     }
-    __syncthreads();
+    if constexpr (WT) __syncwarp(); else __syncthreads();
   }
 #pragma unroll 1
   for (int s = s1 - 1; s >= s0; --s) {
@@ -392,11 +405,17 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
       R.load_halo(Xs + n, x2);
       R.load_halo(Xs + 2 * n, x3);
       R.load_halo(Xs + 3 * n, x4);
-      xchg1(R, xb, buf, g);
+      X1(g);
     } else {
 #pragma unroll
       for (int j = 0; j < C; ++j) x2[j + 2] = axpy_rn(X[j + 2], h, l96_f(X[j + 3], X[j], X[j + 1], X[j + 2], F));
-      xchg2(R, xb, buf, x2, g);
+      if constexpr (WT) {
+        wxchg1<C>(x2);
+        wxchg1<C>(g);
+        __syncwarp();  // every lane is done reading step s + 1's buffer
+      } else {
+        xchg2(R, xb, buf, x2, g);
+      }
       if (DEPTH == 1) {
         // X_{s-1} goes to the buffer X_{s+1} used: every thread read it last step
         if (s > s0) {
@@ -414,11 +433,11 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
 #pragma unroll
       for (int j = 0; j < C; ++j)
         x3[j + 2] = axpy_rn(X[j + 2], h, l96_f(x2[j + 3], x2[j], x2[j + 1], x2[j + 2], F));
-      xchg1(R, xb, buf, x3);
+      X1(x3);
 #pragma unroll
       for (int j = 0; j < C; ++j)
         x4[j + 2] = axpy_rn(X[j + 2], dt, l96_f(x3[j + 3], x3[j], x3[j + 1], x3[j + 2], F));
-      xchg1(R, xb, buf, x4);
+      X1(x4);
     }
     // step_adj (model.py:66-84): with w = (dt/6) g and c3 = 2 c6, dt = 2h,
     //   a3 = dt u4 + c3 g = 2 b3,  b3 = h u4 + w   (u3 = 2 J3^T b3)
@@ -437,14 +456,14 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
       vh[j] = g[j + 2] + u[j];
       a[j + 2] = fma(h, u[j], w[j]);  // b3
     }
-    xchg1(R, xb, buf, a);
+    X1(a);
     ad_sub<C>(a, x3, u);  // u3'
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       vh[j] = fma(2.0, u[j], vh[j]);
       a[j + 2] = fma(h, u[j], w[j]);  // b2
     }
-    xchg1(R, xb, buf, a);
+    X1(a);
     ad_sub<C>(a, x2, u);  // u2'
 #pragma unroll
     for (int j = 0; j < C; ++j) {
@@ -454,8 +473,9 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
     if (!STREAM) {  // X_{s-1} landed; published by this barrier
       if (DEPTH == 1) cp_wait_all();
       else cp_wait_group<1>();
+      if constexpr (WT) __syncwarp();
     }
-    xchg1(R, xb, buf, a);
+    X1(a);
     ad_sub<C>(a, X, u);
 #pragma unroll
     for (int j = 0; j < C; ++j) g[j + 2] = vh[j] + u[j];
@@ -479,9 +499,9 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
 // ------------------------------------------------------------ launchers --
 
 // opt a kernel into > 48 KB of dynamic shared memory (idempotent)
-template <int NT, int C = 0, int EXTRA = 0, int NSB = 2, typename K, typename... Args>
+template <int NT, int C = 0, int EXTRA = 0, int NSB = 2, bool XB = true, typename K, typename... Args>
 static void go(K kernel, dim3 grid, cudaStream_t st, Args... args) {
-  const size_t bytes = sizeof(XBuf<NT>) +
+  const size_t bytes = (XB ? sizeof(XBuf<NT>) : 0) +
                        (C ? NSB * (size_t)Stage2<C ? (C + 1) / 2 * 2 : 2, NT>::PLEN * sizeof(double) : 0) +
                        (size_t)EXTRA * sizeof(double);
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -609,6 +629,28 @@ int launch_tl2(const edak_problem*, const double*, double*, int, const int32_t*,
 int launch_ad2(const edak_problem*, const double*, double*, int, const int32_t*, int, int, const double*,
                cudaStream_t);
 
+// warp-tile sweeps (EDAK_SWEEP_WARP): one warp per tile of 16 x 32 = 512
+// ring elements, halos by shuffles, no CTA barrier.  Window chunks of K steps
+// (EDAK_WARP_CHUNK) keep the redundant halo (12K + 8) a small share of the
+// 512-element range.  Returns false when the problem does not qualify
+// (periodic single-tile rings, odd n / unaligned rows, streamed stages).
+static int warp_chunk() { return env_int("EDAK_WARP_CHUNK", 6); }
+static bool warp_plan(const edak_problem* P, int hl, int hr, SweepGeom& geo, int& nt) {
+  constexpr int RANGE = 16 * 32;
+  const int W = RANGE - hl - hr;
+  if (W < 64 || P->n < 2 * RANGE) return false;
+  nt = (P->n + W - 1) / W;
+  geo.W = ((P->n + nt - 1) / nt + 1) & ~1;
+  if (geo.W > W) geo.W = W;
+  geo.HL = hl;
+  geo.periodic = 0;
+  geo.nact = 32;
+  return pair_ok(P, geo);
+}
+static bool warp_mode(const edak_problem* P, const double* work2) {
+  return env_int("EDAK_SWEEP_WARP", 0) != 0 && P->stage_mode == 0 && (work2 || P->n_steps <= warp_chunk());
+}
+
 int launch_tl(const edak_problem* P, const double* v0, double* obs, int ncols, const int32_t* col_traj,
               cudaStream_t st, double* work2) {
   int C, NT, nt;
@@ -645,6 +687,28 @@ int launch_tl(const edak_problem* P, const double* v0, double* obs, int ncols, c
     }
   }
 v1:
+  if (warp_mode(P, work2)) {
+    const int K = warp_chunk();
+    const int nch = (N + K - 1) / K;
+    const size_t blk = (size_t)ncols * P->n;
+    bool ok = true;
+    for (int c = 0; c < nch && ok; ++c) {
+      const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch), Kc = s1 - s0;
+      ok = warp_plan(P, 8 * Kc + 4, 4 * Kc + 4, geo, nt);
+    }
+    for (int c = 0; c < nch && ok; ++c) {
+      const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch), Kc = s1 - s0;
+      warp_plan(P, 8 * Kc + 4, 4 * Kc + 4, geo, nt);
+      const double* vin = c == 0 ? v0 : work2 + (size_t)((c - 1) & 1) * blk;
+      double* vout = c + 1 < nch ? work2 + (size_t)(c & 1) * blk : nullptr;
+      go<32, 16, 0, 3, false>(k_tl<16, 32, false, 8, true, 2, true>, dim3(nt, ncols), st, *P,
+                                                 vin, obs, col_traj, geo, s0, s1, vout);
+      count_launch();
+      int rc = check_launch("k_tl (warp tiles)");
+      if (rc) return rc;
+    }
+    if (ok) return EDAK_OK;
+  }
   // probe geometry with the full window to learn the mode
   if (!plan(P->n, 8 * N + 4, 4 * N + 4, C, NT, geo, nt) && !work2) {
     set_error("window too long for the tile family");
@@ -733,6 +797,28 @@ int launch_ad(const edak_problem* P, const double* forcing, double* g, int ncols
     }
   }
 v1:
+  if (warp_mode(P, work2)) {
+    const int K = warp_chunk();
+    const int nch = (N + K - 1) / K;
+    const size_t blk = (size_t)ncols * P->n;
+    bool ok = true;
+    for (int c = 0; c < nch && ok; ++c) {
+      const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch), Kc = s1 - s0;
+      ok = warp_plan(P, 4 * Kc + 8, 8 * Kc + 8, geo, nt);
+    }
+    for (int c = nch - 1, k = 0; c >= 0 && ok; --c, ++k) {
+      const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch), Kc = s1 - s0;
+      warp_plan(P, 4 * Kc + 8, 8 * Kc + 8, geo, nt);
+      const double* gin = k == 0 ? nullptr : work2 + (size_t)((k - 1) & 1) * blk;
+      double* gout = c == 0 ? g : work2 + (size_t)(k & 1) * blk;
+      go<32, 16, 2 * 16 * 32, 2, false>(k_ad<16, 32, false, 8, true, 1, true>, dim3(nt, ncols),
+                                                           st, *P, forcing, gout, col_traj, geo, s0, s1, gin);
+      count_launch();
+      int rc = check_launch("k_ad (warp tiles)");
+      if (rc) return rc;
+    }
+    if (ok) return EDAK_OK;
+  }
   if (!plan(P->n, 4 * N + 8, 8 * N + 8, C, NT, geo, nt) && !work2) {
     set_error("window too long for the tile family");
     return EDAK_EUNSUPPORTED;

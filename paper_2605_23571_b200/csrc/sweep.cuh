@@ -134,6 +134,20 @@ __device__ __forceinline__ void xchg2(const Ring<C, NT>& R, XBuf<NT>& X, int& bu
   buf ^= 1;
 }
 
+// ---- warp tiles: the range is one warp's, halos move by shuffles ----------
+// Lane t's left halo is lane t-1's last two own values, its right halo lane
+// t+1's first two.  Lane 0 / 31 receive their own values instead: finite
+// garbage inside the budgeted halo zone, like the zero pads of the CTA
+// exchange.  No barrier and no shared memory, so ptxas can schedule the next
+// sub-stage's interior elements across the exchange.
+template <int C>
+__device__ __forceinline__ void wxchg1(double (&a)[C + 4]) {
+  a[0] = __shfl_up_sync(0xffffffffu, a[C], 1);
+  a[1] = __shfl_up_sync(0xffffffffu, a[C + 1], 1);
+  a[C + 2] = __shfl_down_sync(0xffffffffu, a[2], 1);
+  a[C + 3] = __shfl_down_sync(0xffffffffu, a[3], 1);
+}
+
 // ---- coalesced staging of state tiles through shared memory -------------
 // Loading each thread's (C + 4)-element window straight from global memory
 // costs C + 4 loads whose lanes are C*8 bytes apart (one L1 wavefront per

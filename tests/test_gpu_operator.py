@@ -229,6 +229,19 @@ def test_pair_staging_equals_generic(gpu, monkeypatch):
         assert torch.equal(hz, a.hessian_cols(z))
         assert torch.equal(rd, a.rhs_cols(d))
         monkeypatch.delenv("EDAK_NO_PAIR")
+        # warp tiles (shuffled halos, no CTA barrier) at several window chunks
+        monkeypatch.setenv("EDAK_SWEEP_WARP", "1")
+        for k in ("3", "6", "8"):
+            monkeypatch.setenv("EDAK_WARP_CHUNK", k)
+            assert torch.equal(hz, a.hessian_cols(z)), (n, "warp", k)
+            assert torch.equal(rd, a.rhs_cols(d)), (n, "warp", k)
+        monkeypatch.delenv("EDAK_WARP_CHUNK")
+        monkeypatch.delenv("EDAK_SWEEP_WARP")
+        # U_B register blocking 8 vs 16 outputs per thread: same tap order, same bits
+        for r in ("8", "16"):
+            monkeypatch.setenv("EDAK_CIRC_R", r)
+            assert torch.equal(hz, a.hessian_cols(z)), (n, "circ", r)
+        monkeypatch.delenv("EDAK_CIRC_R")
         # staging prefetch distance 1 vs 2 steps (three-buffer ring): same bits
         for knob in ("EDAK_TL_DEPTH", "EDAK_AD_DEPTH"):
             for depth in ("1", "2"):
