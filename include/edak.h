@@ -69,6 +69,15 @@ typedef struct edak_problem {
    * column) instead of the tap convolution. */
   const double* sym;
   const double* fft_tw;
+  /* optional overlap-save form of the same factor (circ_os.cu): with
+   * M = 2^os_logm (10 or 11) and K = ntaps <= M/2 + 1, os_spec holds the M
+   * complex values fft(h)/M of the block kernel h[m mod M] = taps[m + tap_w]
+   * in bit-reversed order and os_tw = exp(-2 pi i m / (2M)), m < M, both
+   * as interleaved (re, im) doubles.  NULL: U_B is the tap convolution. */
+  const double* os_spec;
+  const double* os_tw;
+  int32_t os_logm;
+  int32_t pad1;
 } edak_problem;
 
 /* ---- library --------------------------------------------------------- */

@@ -40,6 +40,7 @@ def _prob_struct(n, n_steps, dt, forcing, states, stages, traj_stride, stage_mod
     P.sigma2 = float(sigma2)
     P.taps, P.ntaps, P.tap_w = dfac.taps.data_ptr(), dfac.ntaps, dfac.tap_w
     P.sym, P.fft_tw = _lib.ptr(dfac.sym), _lib.ptr(dfac.fft_tw)
+    P.os_spec, P.os_tw, P.os_logm = _lib.ptr(dfac.os_spec), _lib.ptr(dfac.os_tw), dfac.os_logm
     return P
 
 

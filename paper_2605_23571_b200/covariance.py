@@ -124,6 +124,39 @@ def fft_tables(n):
 FFT_MIN_N, FFT_MAX_N = 1024, 16384
 
 
+def os_tables(taps, w, logm):
+    """Overlap-save tables for circ_os.cu: the block kernel
+    h[m mod M] = taps[m + w] (m = k - w, k < K), its spectrum fft(h) / M in
+    bit-reversed order (the forward DIF's output order), and the twiddles
+    exp(-2 pi i m / (2M)), m < M -- both as interleaved (re, im) float64."""
+    M = 1 << logm
+    h = np.zeros(M)
+    k = np.arange(taps.size)
+    np.add.at(h, (k - w) % M, taps)
+    H = np.fft.fft(h) / M
+    rev = np.array([int(format(j, f"0{logm}b")[::-1], 2) for j in range(M)])
+    Hr = H[rev]
+    spec = np.empty(2 * M)
+    spec[0::2], spec[1::2] = Hr.real, Hr.imag
+    ang = np.pi * (np.arange(M, dtype=float) / M)  # m / M exact for power-of-two M
+    tw = np.empty(2 * M)
+    tw[0::2], tw[1::2] = np.cos(ang), -np.sin(ang)
+    return spec, tw
+
+
+def os_logm_for(n, ntaps):
+    """Block size (log2) of the overlap-save U_B, or 0 for the tap
+    convolution: blocks of M = 1024 (K <= 256) or 2048 (K <= 512) complex
+    points on rings of at least 4096 points with a genuinely banded factor."""
+    if n < 4096 or 2 * ntaps > n:
+        return 0
+    if ntaps <= 256:
+        return 10
+    if ntaps <= 512:
+        return 11
+    return 0
+
+
 class DeviceFactor:
     """Device-resident taps (and, for power-of-two rings in [1024, 16384],
     the rfft symbol + twiddles) of a circulant factor, plus a minimal
@@ -140,6 +173,11 @@ class DeviceFactor:
         if FFT_MIN_N <= n <= FFT_MAX_N and n & (n - 1) == 0:
             self.sym = _dev.f64(np.asarray(ub.symbol, dtype=float))
             self.fft_tw = _dev.f64(fft_tables(n))
+        self.os_spec = self.os_tw = None
+        self.os_logm = os_logm_for(n, self.ntaps)
+        if self.os_logm:
+            spec, tw = os_tables(taps, w, self.os_logm)
+            self.os_spec, self.os_tw = _dev.f64(spec), _dev.f64(tw)
         self._prob = _lib.Problem()
         self._prob.n = self.n
         self._prob.taps = self.taps.data_ptr()
@@ -147,6 +185,8 @@ class DeviceFactor:
         self._prob.tap_w = w
         self._prob.sym = _lib.ptr(self.sym)
         self._prob.fft_tw = _lib.ptr(self.fft_tw)
+        self._prob.os_spec, self._prob.os_tw = _lib.ptr(self.os_spec), _lib.ptr(self.os_tw)
+        self._prob.os_logm = self.os_logm
 
     def apply_cols(self, cols, out=None):
         """U_B applied to a (ncols, n) device block."""

@@ -24,7 +24,7 @@ template <int R, int NT>
 __global__ void __launch_bounds__(NT) k_circ(int n, const double* __restrict__ taps, int K, int Kp, int w,
                                              const double* __restrict__ in, double* __restrict__ out,
                                              double ident, const double* __restrict__ zadd,
-                                             double* __restrict__ dotp) {
+                                             double* __restrict__ dotp, int dtiles) {
   auto padi = [](int q) { return q + q / R; };
   extern __shared__ double sm[];
   double* st = sm;                      // reversed taps, Kp (zero padded)
@@ -94,17 +94,24 @@ __global__ void __launch_bounds__(NT) k_circ(int n, const double* __restrict__ t
     if (t == 0) {
       double s = 0.0;
       for (int w = 0; w < NT / 32; ++w) s += sm[w];
-      dotp[(size_t)col * gridDim.x + blockIdx.x] = s;
+      dotp[(size_t)col * dtiles + blockIdx.x] = s;
     }
+    if (blockIdx.x == 0)  // slots past the last tile (circ_tiles counts 512-point tiles)
+      for (int q = (int)gridDim.x + t; q < dtiles; q += NT) dotp[(size_t)col * dtiles + q] = 0.0;
   }
 }
 
 // out = U_B in (+ ident * zadd when zadd != NULL: the I + A of assim.py:70-72)
-int circ_tiles(int n) { return (n + CIRC_NT * CIRC_R - 1) / (CIRC_NT * CIRC_R); }
+// dot-partial slots per column: one per 512 outputs, enough for the 1024-point
+// tiles of the tap convolution and the >= 512-output blocks of circ_os.cu
+int circ_tiles(int n) { return (n + 511) / 512; }
 
 bool circ_fft_ok(const edak_problem* P);
 int launch_circ_fft(const edak_problem* P, const double* in, double* out, int ncols, double ident,
                     const double* zadd, cudaStream_t st, double* dotp, int dtiles);
+
+int launch_circ_os(const edak_problem* P, const double* in, double* out, int ncols, double ident,
+                   const double* zadd, cudaStream_t st, double* dotp, int dtiles);
 
 int launch_circ(const edak_problem* P, const double* in, double* out, int ncols, double ident,
                 const double* zadd, cudaStream_t st, double* dotp) {
@@ -112,6 +119,13 @@ int launch_circ(const edak_problem* P, const double* in, double* out, int ncols,
   // the tap convolution at cfg4 (70.6 vs 68.9 us per 200 columns), so opt-in
   if (circ_fft_ok(P) && getenv("EDAK_CIRC_FFT"))
     return launch_circ_fft(P, in, out, ncols, ident, zadd, st, dotp, circ_tiles(P->n));
+  // overlap-save block FFTs (circ_os.cu) when the factor carries their
+  // tables; EDAK_CIRC_OS=0 forces the tap convolution
+  const char* eo = getenv("EDAK_CIRC_OS");
+  if (!(eo && atoi(eo) == 0) && P->os_spec) {
+    const int rc = launch_circ_os(P, in, out, ncols, ident, zadd, st, dotp, circ_tiles(P->n));
+    if (rc != EDAK_EUNSUPPORTED) return rc;
+  }
   const int n = P->n, K = P->ntaps;
   if (K < 1 || K > CIRC_MAXTAPS) {
     set_error("circulant factor: tap count outside [1, 4096]");
@@ -138,9 +152,11 @@ int launch_circ(const edak_problem* P, const double* in, double* out, int ncols,
     attr = true;
   }
   if (R == 16)
-    k_circ<16, CIRC_NT / 2><<<grid, NT, smem, st>>>(n, P->taps, K, Kp, P->tap_w, in, out, ident, zadd, dotp);
+    k_circ<16, CIRC_NT / 2><<<grid, NT, smem, st>>>(n, P->taps, K, Kp, P->tap_w, in, out, ident, zadd, dotp,
+                                                   circ_tiles(n));
   else
-    k_circ<CIRC_R, CIRC_NT><<<grid, NT, smem, st>>>(n, P->taps, K, Kp, P->tap_w, in, out, ident, zadd, dotp);
+    k_circ<CIRC_R, CIRC_NT><<<grid, NT, smem, st>>>(n, P->taps, K, Kp, P->tap_w, in, out, ident, zadd, dotp,
+                                                   circ_tiles(n));
   count_launch();
   return check_launch("k_circ");
 }

@@ -1,0 +1,270 @@
+// Circulant U_B (GridCovFactor.apply, covariance.py:41-47) by overlap-save
+// block FFTs: out = u (*) v with the banded generator u (taps, circ.cu).
+//
+// One CTA = one block of V = M - K + 1 consecutive outputs of TWO columns,
+// packed as one complex vector z_q = a_q + i b_q (q < M) over the block's
+// input window.  Because u is real, the circular convolution of the block
+// with u is (u * a) + i (u * b): no real-FFT split or merge.  z is
+// transformed in shared memory by a radix-2/radix-8 decimation-in-frequency
+// FFT (natural -> bit-reversed order), multiplied by the block kernel's
+// spectrum H (host-computed, stored in the same bit-reversed order, 1/M
+// folded in), and brought back by the mirrored decimation-in-time inverse
+// (bit-reversed -> natural): no permutation pass.  Outputs q in [L, L + V)
+// of the block are exact linear-convolution values (L = left reach of u).
+//
+// Work per output: ~2 log2(M) complex butterflies for two columns at
+// (M / V) redundancy, against K FMAs per column for the tap convolution
+// (cfg4: M = 1024, K = 189, V = 836).
+#include "common.cuh"
+
+namespace edak {
+
+namespace os {
+
+__device__ __forceinline__ int pz(int j) { return j + (j >> 3); }  // 1 pad per 8 (16-byte banks)
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cmul_mi(double2 a) { return make_double2(a.y, -a.x); }
+__device__ __forceinline__ double2 cmul_pi(double2 a) { return make_double2(-a.y, a.x); }
+
+// W_M^e = exp(-2 pi i e / M) from T[m] = exp(-2 pi i m / (2M)), m < M
+template <int M>
+__device__ __forceinline__ double2 tw(const double2* __restrict__ T, int e) {
+  const int m = 2 * e;
+  if (m < M) return __ldg(T + m);
+  const double2 v = __ldg(T + (m - M));
+  return make_double2(-v.x, -v.y);
+}
+
+// multiply by the eighth roots exp(-+2 pi i m / 8), m = 0..3
+template <bool INV>
+__device__ __forceinline__ double2 w8(double2 a, int m) {
+  const double r = 0.70710678118654752440;
+  if (m == 0) return a;
+  if (m == 2) return INV ? cmul_pi(a) : cmul_mi(a);
+  if (m == 1) return INV ? make_double2(r * (a.x - a.y), r * (a.x + a.y)) : make_double2(r * (a.x + a.y), r * (a.y - a.x));
+  return INV ? make_double2(-r * (a.x + a.y), r * (a.x - a.y)) : make_double2(r * (a.y - a.x), -r * (a.x + a.y));
+}
+
+// forward DIF over Z[pz(.)], M = 2^LOGM points: LOGM % 3 radix-2 stages,
+// then radix-8 passes; output in bit-reversed order
+template <int LOGM, int NT>
+__device__ __forceinline__ void dif(double2* Z, const double2* __restrict__ T) {
+  constexpr int M = 1 << LOGM;
+  const int t = threadIdx.x;
+  int h = M >> 1;
+#pragma unroll
+  for (int r = 0; r < LOGM % 3; ++r, h >>= 1) {
+#pragma unroll
+    for (int p = t; p < M / 2; p += NT) {
+      const int j = (p / h) * 2 * h + p % h;
+      const double2 x = Z[pz(j)], y = Z[pz(j + h)];
+      Z[pz(j)] = cadd(x, y);
+      Z[pz(j + h)] = cmul(csub(x, y), tw<M>(T, (p % h) * (M / (2 * h))));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int pass = 0; pass < LOGM / 3; ++pass, h >>= 3) {
+    const int q = h >> 2;
+#pragma unroll
+    for (int g = t; g < M / 8; g += NT) {
+      const int r0 = g % q, j0 = (g / q) * 2 * h + r0;
+      double2 a[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) a[m] = Z[pz(j0 + m * q)];
+      const double2 b1 = tw<M>(T, r0 * (M / (2 * h)));
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const double2 x = a[m], y = a[m + 4];
+        a[m] = cadd(x, y);
+        a[m + 4] = cmul(w8<false>(csub(x, y), m), b1);
+      }
+      const double2 b2 = cmul(b1, b1);
+#pragma unroll
+      for (int mm = 0; mm < 4; ++mm) {
+        const int m = (mm & 1) + 4 * (mm >> 1);  // 0, 1, 4, 5
+        const double2 x = a[m], y = a[m + 2];
+        a[m] = cadd(x, y);
+        const double2 d = cmul(csub(x, y), b2);
+        a[m + 2] = (m & 1) ? cmul_mi(d) : d;
+      }
+      const double2 b4 = cmul(b2, b2);
+#pragma unroll
+      for (int m = 0; m < 8; m += 2) {
+        const double2 x = a[m], y = a[m + 1];
+        a[m] = cadd(x, y);
+        a[m + 1] = cmul(csub(x, y), b4);
+      }
+#pragma unroll
+      for (int m = 0; m < 8; ++m) Z[pz(j0 + m * q)] = a[m];
+    }
+    __syncthreads();
+  }
+}
+
+// inverse DIT (unscaled), bit-reversed -> natural: radix-8 passes from span
+// 1, then LOGM % 3 radix-2 stages (the exact mirror of dif)
+template <int LOGM, int NT>
+__device__ __forceinline__ void dit(double2* Z, const double2* __restrict__ T) {
+  constexpr int M = 1 << LOGM;
+  const int t = threadIdx.x;
+  int h = 1;
+#pragma unroll
+  for (int pass = 0; pass < LOGM / 3; ++pass, h <<= 3) {
+#pragma unroll
+    for (int g = t; g < M / 8; g += NT) {
+      const int r0 = g % h, j0 = (g / h) * 8 * h + r0;
+      double2 a[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) a[m] = Z[pz(j0 + m * h)];
+      const double2 c1 = cconj(tw<M>(T, r0 * (M / (8 * h))));
+      const double2 c2 = cmul(c1, c1), c4 = cmul(c2, c2);
+#pragma unroll
+      for (int m = 0; m < 8; m += 2) {
+        const double2 x = a[m], y = cmul(a[m + 1], c4);
+        a[m] = cadd(x, y);
+        a[m + 1] = csub(x, y);
+      }
+#pragma unroll
+      for (int mm = 0; mm < 4; ++mm) {
+        const int m = (mm & 1) + 4 * (mm >> 1);
+        const double2 d = cmul(a[m + 2], c2);
+        const double2 x = a[m], y = (m & 1) ? cmul_pi(d) : d;
+        a[m] = cadd(x, y);
+        a[m + 2] = csub(x, y);
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const double2 x = a[m], y = w8<true>(cmul(a[m + 4], c1), m);
+        a[m] = cadd(x, y);
+        a[m + 4] = csub(x, y);
+      }
+#pragma unroll
+      for (int m = 0; m < 8; ++m) Z[pz(j0 + m * h)] = a[m];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < LOGM % 3; ++r, h <<= 1) {
+#pragma unroll
+    for (int p = t; p < M / 2; p += NT) {
+      const int j = (p / h) * 2 * h + p % h;
+      const double2 x = Z[pz(j)], y = cmul(Z[pz(j + h)], cconj(tw<M>(T, (p % h) * (M / (2 * h)))));
+      Z[pz(j)] = cadd(x, y);
+      Z[pz(j + h)] = csub(x, y);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace os
+
+// grid (blocks of V outputs, column pairs); L = left reach of u (taps k <
+// K act on in[i + tap_w - k]: reach K - 1 - tap_w to the left, tap_w right)
+template <int LOGM, int NT>
+__global__ void __launch_bounds__(NT) k_circ_os(int n, int L, int V, int ncols, const double2* __restrict__ T,
+                                                const double2* __restrict__ H, const double* __restrict__ in,
+                                                double* __restrict__ out, double ident,
+                                                const double* __restrict__ zadd, double* __restrict__ dotp,
+                                                int dtiles) {
+  using namespace os;
+  constexpr int M = 1 << LOGM;
+  __shared__ __align__(16) double2 Z[M + M / 8];
+  __shared__ double red[2][NT / 32];
+  const int t = threadIdx.x, blk = blockIdx.x;
+  const int ca = 2 * blockIdx.y, cb = ca + 1;
+  const bool hb = cb < ncols;
+  const int i0 = blk * V;
+  const double* A = in + (size_t)ca * n;
+  const double* B = in + (size_t)(hb ? cb : ca) * n;
+  int g = i0 - L + t;
+  g = g < 0 ? g + n : g;
+  while (g >= n) g -= n;
+  const int step = NT % n;
+#pragma unroll 4
+  for (int q = t; q < M; q += NT) {
+    Z[pz(q)] = make_double2(__ldg(A + g), hb ? __ldg(B + g) : 0.0);
+    g += step;
+    if (g >= n) g -= n;
+  }
+  __syncthreads();
+  dif<LOGM, NT>(Z, T);
+#pragma unroll
+  for (int j = t; j < M; j += NT) Z[pz(j)] = cmul(Z[pz(j)], __ldg(H + j));
+  __syncthreads();
+  dit<LOGM, NT>(Z, T);
+  // epilogue: outputs i0 + j, j < V, at block position L + j
+  double da = 0.0, db = 0.0;
+  const int nv = min(V, n - i0);
+  double* oa = out + (size_t)ca * n;
+  double* ob = out + (size_t)cb * n;
+  const double* za = zadd ? zadd + (size_t)ca * n : nullptr;
+  const double* zb = zadd ? zadd + (size_t)cb * n : nullptr;
+  for (int j = t; j < nv; j += NT) {
+    const double2 y = Z[pz(L + j)];
+    double va = y.x, vb = y.y;
+    const int i = i0 + j;
+    if (za) {
+      const double z1 = za[i];
+      va = fma(ident, z1, va);
+      da = fma(z1, va, da);
+      if (hb) {
+        const double z2 = zb[i];
+        vb = fma(ident, z2, vb);
+        db = fma(z2, vb, db);
+      }
+    }
+    oa[i] = va;
+    if (hb) ob[i] = vb;
+  }
+  if (dotp) {  // fixed-order CTA reduction -> dotp[col][blk]; slots past the last block get 0
+    da = warp_sum(da);
+    db = warp_sum(db);
+    if ((t & 31) == 0) {
+      red[0][t >> 5] = da;
+      red[1][t >> 5] = db;
+    }
+    __syncthreads();
+    if (t < 2 && (t == 0 || hb)) {
+      double s = 0.0;
+      for (int w = 0; w < NT / 32; ++w) s += red[t][w];
+      dotp[(size_t)(ca + t) * dtiles + blk] = s;
+    }
+    if (blk == 0) {
+      for (int q = (int)gridDim.x + t; q < dtiles; q += NT) {
+        dotp[(size_t)ca * dtiles + q] = 0.0;
+        if (hb) dotp[(size_t)cb * dtiles + q] = 0.0;
+      }
+    }
+  }
+}
+
+// U_B by overlap-save when the problem carries the block spectrum
+// (edak_problem.os_logm/os_spec/os_tw, covariance.py DeviceFactor); returns
+// EDAK_EUNSUPPORTED when it does not apply (the caller then convolves)
+int launch_circ_os(const edak_problem* P, const double* in, double* out, int ncols, double ident,
+                   const double* zadd, cudaStream_t st, double* dotp, int dtiles) {
+  const int logm = P->os_logm, K = P->ntaps, n = P->n;
+  if (!P->os_spec || !P->os_tw || (logm != 10 && logm != 11)) return EDAK_EUNSUPPORTED;
+  const int M = 1 << logm, V = M - K + 1, L = K - 1 - P->tap_w;
+  if (V < M / 2 || L < 0 || P->tap_w < 0) return EDAK_EUNSUPPORTED;
+  const int nb = (n + V - 1) / V;
+  if (dotp && nb > dtiles) return EDAK_EUNSUPPORTED;
+  dim3 grid(nb, (ncols + 1) / 2);
+  const double2* T = reinterpret_cast<const double2*>(P->os_tw);
+  const double2* H = reinterpret_cast<const double2*>(P->os_spec);
+  if (logm == 10)
+    k_circ_os<10, 128><<<grid, 128, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
+  else
+    k_circ_os<11, 256><<<grid, 256, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
+  count_launch();
+  return check_launch("k_circ_os");
+}
+
+}  // namespace edak

@@ -91,3 +91,31 @@ def test_product_twin_streams_match_oracle():
     a = substream(0, "bg", 17).standard_normal(5)
     b = osub(0, "bg", 17).standard_normal(5)
     assert (a == b).all()
+
+
+def test_overlap_save_tables_reproduce_the_tap_convolution():
+    """covariance.os_tables (circ_os.cu's block spectrum in bit-reversed
+    order, 1/M folded in): un-permuted and used in a numpy circular block
+    convolution, the valid outputs equal the tap convolution
+    out_i = sum_k taps[k] x[(i + w - k) mod n] (circ.cu), and the block
+    sizes follow os_logm_for."""
+    import numpy as np
+    from paper_2605_23571_b200.covariance import os_logm_for, os_tables
+    rng = np.random.default_rng(5)
+    for n, K, w, logm in [(16384, 189, 94, 10), (9000, 61, 20, 10), (262144, 377, 188, 11)]:
+        assert os_logm_for(n, K) == logm
+        taps = rng.standard_normal(K)
+        spec, tw = os_tables(taps, w, logm)
+        M, V, L = 1 << logm, (1 << logm) - K + 1, K - 1 - w
+        rev = np.array([int(format(j, f"0{logm}b")[::-1], 2) for j in range(M)])
+        H = np.empty(M, complex)
+        H[rev] = spec[0::2] + 1j * spec[1::2]
+        assert np.allclose(tw[0::2] - 1j * tw[1::2], np.exp(2j * np.pi * np.arange(M) / (2 * M)), atol=1e-16)
+        x = rng.standard_normal(n)
+        i0 = n - V // 2  # a block that wraps the ring
+        z = x[(i0 - L + np.arange(M)) % n]
+        y = (np.fft.ifft(np.fft.fft(z) * H) * M)[L:L + V]
+        i = (i0 + np.arange(V)) % n
+        direct = sum(taps[k] * x[(i + w - k) % n] for k in range(K))
+        assert np.abs(y.real - direct).max() <= 1e-13 * np.abs(direct).max()
+    assert os_logm_for(40, 40) == 0 and os_logm_for(1024, 97) == 0 and os_logm_for(16384, 600) == 0

@@ -368,3 +368,33 @@ def test_spectral_factor_equals_taps(gpu, monkeypatch):
         hz2 = lin.hessian_cols(z, None, 1.0, None, None, None, dp2)
         assert float((hz - hz2).abs().max()) <= 1e-13 * float(hz2.abs().max())
         assert torch.allclose(dp.sum(1), (z * hz).sum(1), rtol=1e-13)
+
+
+def test_overlap_save_factor_equals_taps(gpu, monkeypatch):
+    """Overlap-save U_B (circ_os.cu: M = 1024 blocks at cfg4's 189 taps, M =
+    2048 at cfg5's 377, two columns per CTA as one complex vector, odd
+    column count, ragged ring) against the tap convolution and numpy's
+    irfft(symbol rfft), including the I + A epilogue and its p.Hp partials."""
+    from paper_2605_23571_b200.assim import Linearization
+    from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
+    for n, L, nc, logm in [(16384, 16.0, 5, 10), (8190, 8.0, 4, 10), (262144, 32.0, 3, 11)]:
+        op = _oracle_problem(n, 2, 8, 2, L, 23)
+        ub = CirculantFactor(n, op.ub.symbol)
+        lin = Linearization(op.traj.states[None], 0.025, 8.0, op.net, ub, DiagonalNoise(1.0))
+        assert lin.dfac.os_logm == logm, (n, lin.dfac.ntaps)
+        z = torch.randn(nc, n, dtype=torch.float64, device="cuda")
+        osv = lin.dfac.apply_cols(z)
+        monkeypatch.setenv("EDAK_CIRC_OS", "0")
+        direct = lin.dfac.apply_cols(z)
+        ref = np.fft.irfft(np.fft.rfft(z.cpu().numpy(), axis=1) * op.ub.symbol, n=n, axis=1)
+        assert float((osv - direct).abs().max()) <= 1e-14 * float(direct.abs().max()), n
+        assert np.abs(osv.cpu().numpy() - ref).max() <= 1e-14 * np.abs(ref).max(), n
+        tiles = lin.dot_tiles()
+        dp = torch.full((nc, tiles), float("nan"), dtype=torch.float64, device="cuda")
+        hz = lin.hessian_cols(z, None, 1.0, None, None, None, dp)
+        monkeypatch.delenv("EDAK_CIRC_OS")
+        dp2 = torch.full_like(dp, float("nan"))
+        hz2 = lin.hessian_cols(z, None, 1.0, None, None, None, dp2)
+        assert float((hz - hz2).abs().max()) <= 1e-13 * float(hz.abs().max()), n
+        assert torch.allclose(dp.sum(1), (z * hz).sum(1), rtol=1e-13)
+        assert torch.allclose(dp2.sum(1), (z * hz2).sum(1), rtol=1e-13)
