@@ -51,59 +51,83 @@ __device__ __forceinline__ double2 w8(double2 a, int m) {
   return INV ? make_double2(-r * (a.x + a.y), r * (a.x - a.y)) : make_double2(r * (a.y - a.x), -r * (a.x + a.y));
 }
 
+// Twiddles of every pass, fetched once per thread at kernel start (their
+// loads then overlap the input loads instead of stalling each pass): the
+// DIF pass of radix-8 group stride q and the DIT pass of span q use the same
+// W_M^e (conjugated), and so do the radix-2 stages of equal span.
+template <int LOGM, int NT>
+struct Tw {
+  static constexpr int M = 1 << LOGM, R2 = LOGM % 3, R8 = LOGM / 3, P2 = M / 2 / NT;
+  static_assert(M / 8 == NT, "one radix-8 group per thread and pass");
+  double2 w2[R2 > 0 ? R2 : 1][P2];
+  double2 w8[R8];
+  __device__ __forceinline__ void load(const double2* __restrict__ T) {
+    const int t = threadIdx.x;
+    int h = M >> 1;
+#pragma unroll
+    for (int r = 0; r < R2; ++r, h >>= 1)
+#pragma unroll
+      for (int k = 0; k < P2; ++k) w2[r][k] = tw<M>(T, ((t + k * NT) % h) * (M / (2 * h)));
+#pragma unroll
+    for (int pass = 0; pass < R8; ++pass, h >>= 3) {
+      const int q = h >> 2;
+      w8[pass] = q > 1 ? tw<M>(T, (t % q) * (M / (2 * h))) : make_double2(1.0, 0.0);
+    }
+  }
+};
+
 // forward DIF over Z[pz(.)], M = 2^LOGM points: LOGM % 3 radix-2 stages,
 // then radix-8 passes; output in bit-reversed order
 template <int LOGM, int NT>
-__device__ __forceinline__ void dif(double2* Z, const double2* __restrict__ T) {
+__device__ __forceinline__ void dif(double2* Z, const Tw<LOGM, NT>& W) {
   constexpr int M = 1 << LOGM;
   const int t = threadIdx.x;
   int h = M >> 1;
 #pragma unroll
   for (int r = 0; r < LOGM % 3; ++r, h >>= 1) {
 #pragma unroll
-    for (int p = t; p < M / 2; p += NT) {
+    for (int k = 0; k < M / 2 / NT; ++k) {
+      const int p = t + k * NT;
       const int j = (p / h) * 2 * h + p % h;
       const double2 x = Z[pz(j)], y = Z[pz(j + h)];
       Z[pz(j)] = cadd(x, y);
-      Z[pz(j + h)] = cmul(csub(x, y), tw<M>(T, (p % h) * (M / (2 * h))));
+      Z[pz(j + h)] = cmul(csub(x, y), W.w2[r][k]);
     }
     __syncthreads();
   }
 #pragma unroll
   for (int pass = 0; pass < LOGM / 3; ++pass, h >>= 3) {
     const int q = h >> 2;
+    const int g = t;
+    const int r0 = g % q, j0 = (g / q) * 2 * h + r0;
+    double2 a[8];
 #pragma unroll
-    for (int g = t; g < M / 8; g += NT) {
-      const int r0 = g % q, j0 = (g / q) * 2 * h + r0;
-      double2 a[8];
+    for (int m = 0; m < 8; ++m) a[m] = Z[pz(j0 + m * q)];
+    const double2 b1 = W.w8[pass];
 #pragma unroll
-      for (int m = 0; m < 8; ++m) a[m] = Z[pz(j0 + m * q)];
-      const double2 b1 = tw<M>(T, r0 * (M / (2 * h)));
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const double2 x = a[m], y = a[m + 4];
-        a[m] = cadd(x, y);
-        a[m + 4] = cmul(w8<false>(csub(x, y), m), b1);
-      }
-      const double2 b2 = cmul(b1, b1);
-#pragma unroll
-      for (int mm = 0; mm < 4; ++mm) {
-        const int m = (mm & 1) + 4 * (mm >> 1);  // 0, 1, 4, 5
-        const double2 x = a[m], y = a[m + 2];
-        a[m] = cadd(x, y);
-        const double2 d = cmul(csub(x, y), b2);
-        a[m + 2] = (m & 1) ? cmul_mi(d) : d;
-      }
-      const double2 b4 = cmul(b2, b2);
-#pragma unroll
-      for (int m = 0; m < 8; m += 2) {
-        const double2 x = a[m], y = a[m + 1];
-        a[m] = cadd(x, y);
-        a[m + 1] = cmul(csub(x, y), b4);
-      }
-#pragma unroll
-      for (int m = 0; m < 8; ++m) Z[pz(j0 + m * q)] = a[m];
+    for (int m = 0; m < 4; ++m) {
+      const double2 x = a[m], y = a[m + 4];
+      a[m] = cadd(x, y);
+      a[m + 4] = cmul(w8<false>(csub(x, y), m), b1);
     }
+    const double2 b2 = cmul(b1, b1);
+#pragma unroll
+    for (int mm = 0; mm < 4; ++mm) {
+      const int m = (mm & 1) + 4 * (mm >> 1);  // 0, 1, 4, 5
+      const double2 x = a[m], y = a[m + 2];
+      a[m] = cadd(x, y);
+      const double2 d = cmul(csub(x, y), b2);
+      a[m + 2] = (m & 1) ? cmul_mi(d) : d;
+    }
+    const double2 b4 = cmul(b2, b2);
+#pragma unroll
+    for (int m = 0; m < 8; m += 2) {
+      const double2 x = a[m], y = a[m + 1];
+      a[m] = cadd(x, y);
+      a[m + 1] = cmul(csub(x, y), b4);
+    }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) Z[pz(j0 + m * q)] = a[m];
     __syncthreads();
   }
 }
@@ -111,51 +135,50 @@ __device__ __forceinline__ void dif(double2* Z, const double2* __restrict__ T) {
 // inverse DIT (unscaled), bit-reversed -> natural: radix-8 passes from span
 // 1, then LOGM % 3 radix-2 stages (the exact mirror of dif)
 template <int LOGM, int NT>
-__device__ __forceinline__ void dit(double2* Z, const double2* __restrict__ T) {
+__device__ __forceinline__ void dit(double2* Z, const Tw<LOGM, NT>& W) {
   constexpr int M = 1 << LOGM;
   const int t = threadIdx.x;
   int h = 1;
 #pragma unroll
-  for (int pass = 0; pass < LOGM / 3; ++pass, h <<= 3) {
+  for (int pass = LOGM / 3 - 1; pass >= 0; --pass, h <<= 3) {
+    const int g = t;
+    const int r0 = g % h, j0 = (g / h) * 8 * h + r0;
+    double2 a[8];
 #pragma unroll
-    for (int g = t; g < M / 8; g += NT) {
-      const int r0 = g % h, j0 = (g / h) * 8 * h + r0;
-      double2 a[8];
+    for (int m = 0; m < 8; ++m) a[m] = Z[pz(j0 + m * h)];
+    const double2 c1 = cconj(W.w8[pass]);
+    const double2 c2 = cmul(c1, c1), c4 = cmul(c2, c2);
 #pragma unroll
-      for (int m = 0; m < 8; ++m) a[m] = Z[pz(j0 + m * h)];
-      const double2 c1 = cconj(tw<M>(T, r0 * (M / (8 * h))));
-      const double2 c2 = cmul(c1, c1), c4 = cmul(c2, c2);
-#pragma unroll
-      for (int m = 0; m < 8; m += 2) {
-        const double2 x = a[m], y = cmul(a[m + 1], c4);
-        a[m] = cadd(x, y);
-        a[m + 1] = csub(x, y);
-      }
-#pragma unroll
-      for (int mm = 0; mm < 4; ++mm) {
-        const int m = (mm & 1) + 4 * (mm >> 1);
-        const double2 d = cmul(a[m + 2], c2);
-        const double2 x = a[m], y = (m & 1) ? cmul_pi(d) : d;
-        a[m] = cadd(x, y);
-        a[m + 2] = csub(x, y);
-      }
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const double2 x = a[m], y = w8<true>(cmul(a[m + 4], c1), m);
-        a[m] = cadd(x, y);
-        a[m + 4] = csub(x, y);
-      }
-#pragma unroll
-      for (int m = 0; m < 8; ++m) Z[pz(j0 + m * h)] = a[m];
+    for (int m = 0; m < 8; m += 2) {
+      const double2 x = a[m], y = cmul(a[m + 1], c4);
+      a[m] = cadd(x, y);
+      a[m + 1] = csub(x, y);
     }
+#pragma unroll
+    for (int mm = 0; mm < 4; ++mm) {
+      const int m = (mm & 1) + 4 * (mm >> 1);
+      const double2 d = cmul(a[m + 2], c2);
+      const double2 x = a[m], y = (m & 1) ? cmul_pi(d) : d;
+      a[m] = cadd(x, y);
+      a[m + 2] = csub(x, y);
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const double2 x = a[m], y = w8<true>(cmul(a[m + 4], c1), m);
+      a[m] = cadd(x, y);
+      a[m + 4] = csub(x, y);
+    }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) Z[pz(j0 + m * h)] = a[m];
     __syncthreads();
   }
 #pragma unroll
-  for (int r = 0; r < LOGM % 3; ++r, h <<= 1) {
+  for (int r = LOGM % 3 - 1; r >= 0; --r, h <<= 1) {
 #pragma unroll
-    for (int p = t; p < M / 2; p += NT) {
+    for (int k = 0; k < M / 2 / NT; ++k) {
+      const int p = t + k * NT;
       const int j = (p / h) * 2 * h + p % h;
-      const double2 x = Z[pz(j)], y = cmul(Z[pz(j + h)], cconj(tw<M>(T, (p % h) * (M / (2 * h)))));
+      const double2 x = Z[pz(j)], y = cmul(Z[pz(j + h)], cconj(W.w2[r][k]));
       Z[pz(j)] = cadd(x, y);
       Z[pz(j + h)] = csub(x, y);
     }
@@ -183,22 +206,26 @@ __global__ void __launch_bounds__(NT) k_circ_os(int n, int L, int V, int ncols, 
   const int i0 = blk * V;
   const double* A = in + (size_t)ca * n;
   const double* B = in + (size_t)(hb ? cb : ca) * n;
-  int g = i0 - L + t;
-  g = g < 0 ? g + n : g;
-  while (g >= n) g -= n;
-  const int step = NT % n;
-#pragma unroll 4
-  for (int q = t; q < M; q += NT) {
-    Z[pz(q)] = make_double2(__ldg(A + g), hb ? __ldg(B + g) : 0.0);
-    g += step;
-    if (g >= n) g -= n;
+  // window [i0 - L, i0 - L + M) of the ring: n > M (os_logm_for), so one
+  // conditional wrap per index; every load is issued before the first store
+  double ra[M / NT], rb[M / NT];
+#pragma unroll
+  for (int k = 0; k < M / NT; ++k) {
+    int g = i0 - L + t + k * NT;
+    g = g < 0 ? g + n : (g >= n ? g - n : g);
+    ra[k] = __ldg(A + g);
+    rb[k] = hb ? __ldg(B + g) : 0.0;
   }
+  Tw<LOGM, NT> W;
+  W.load(T);
+#pragma unroll
+  for (int k = 0; k < M / NT; ++k) Z[pz(t + k * NT)] = make_double2(ra[k], rb[k]);
   __syncthreads();
-  dif<LOGM, NT>(Z, T);
+  dif<LOGM, NT>(Z, W);
 #pragma unroll
   for (int j = t; j < M; j += NT) Z[pz(j)] = cmul(Z[pz(j)], __ldg(H + j));
   __syncthreads();
-  dit<LOGM, NT>(Z, T);
+  dit<LOGM, NT>(Z, W);
   // epilogue: outputs i0 + j, j < V, at block position L + j
   double da = 0.0, db = 0.0;
   const int nv = min(V, n - i0);
@@ -253,7 +280,7 @@ int launch_circ_os(const edak_problem* P, const double* in, double* out, int nco
   const int logm = P->os_logm, K = P->ntaps, n = P->n;
   if (!P->os_spec || !P->os_tw || (logm != 10 && logm != 11)) return EDAK_EUNSUPPORTED;
   const int M = 1 << logm, V = M - K + 1, L = K - 1 - P->tap_w;
-  if (V < M / 2 || L < 0 || P->tap_w < 0) return EDAK_EUNSUPPORTED;
+  if (V < M / 2 || L < 0 || P->tap_w < 0 || n <= M) return EDAK_EUNSUPPORTED;
   const int nb = (n + V - 1) / V;
   if (dotp && nb > dtiles) return EDAK_EUNSUPPORTED;
   dim3 grid(nb, (ncols + 1) / 2);
