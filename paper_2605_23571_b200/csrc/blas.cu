@@ -33,41 +33,48 @@ __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %
 // Both kernels: CTA tile 64 x 64, 8 warps as 2 x 4 (warp tile 32 x 16 = 4 x 2
 // DMMA.8x8x4 fragments), K chunks of 32 staged by a 2-deep cp.async
 // pipeline so the next chunk's loads overlap this chunk's DMMAs.
-constexpr int G_BM = 64, G_BN = 64, G_BK = 32, G_PAD = 4;
+constexpr int G_BM = 64, G_BK = 32, G_PAD = 4;
 
 // ----------------------------------------------------------------- TN ----
-// sA[stage][col a][k], sB[stage][col b][k]  (both operands K-contiguous)
+// sA[stage][col a][k], sB[stage][col b][k]  (both operands K-contiguous).
+// FN = DMMA fragments per warp along N: CTA N tile BN = 32 FN (FN = 2: 64,
+// FN = 4: 128 -- one N tile for a 100-member group)
+template <int FN>
 __global__ void __launch_bounds__(256) k_gemm_tn(const double* __restrict__ A, int64_t lda,
                                                  const double* __restrict__ B, int64_t ldb, int m, int nb,
                                                  int64_t K, int64_t kslice, double* __restrict__ part) {
+  constexpr int BN = 32 * FN;
   extern __shared__ __align__(16) double gsm[];
   double (*sA)[G_BM][G_BK + G_PAD] = reinterpret_cast<double (*)[G_BM][G_BK + G_PAD]>(gsm);
-  double (*sB)[G_BN][G_BK + G_PAD] =
-      reinterpret_cast<double (*)[G_BN][G_BK + G_PAD]>(gsm + 2 * G_BM * (G_BK + G_PAD));
+  double (*sB)[BN][G_BK + G_PAD] =
+      reinterpret_cast<double (*)[BN][G_BK + G_PAD]>(gsm + 2 * G_BM * (G_BK + G_PAD));
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int wa = (warp >> 2) * 32, wb = (warp & 3) * 16;
-  const int a0 = blockIdx.x * G_BM, b0 = blockIdx.y * G_BN;
+  const int wa = (warp >> 2) * 32, wb = (warp & 3) * 8 * FN;
+  const int a0 = blockIdx.x * G_BM, b0 = blockIdx.y * BN;
   const int64_t k_begin = (int64_t)blockIdx.z * kslice;
   const int64_t k_end = min(K, k_begin + kslice);
   const int nch = (int)((k_end - k_begin + G_BK - 1) / G_BK);
   auto load = [&](int stg, int64_t k0) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < 8 * FN / 2; ++q) {
       const int idx = t + q * 256;
       const int col = idx >> 5, kk = idx & 31;
       const int64_t k = k0 + kk;
       const bool kin = k < k_end;
-      const bool va = kin && a0 + col < m, vb = kin && b0 + col < nb;
-      cpa8(&sA[stg][col][kk], va ? A + k + (int64_t)(a0 + col) * lda : A, va);
+      if (q < 8) {
+        const bool va = kin && a0 + col < m;
+        cpa8(&sA[stg][col][kk], va ? A + k + (int64_t)(a0 + col) * lda : A, va);
+      }
+      const bool vb = kin && b0 + col < nb;
       cpa8(&sB[stg][col][kk], vb ? B + k + (int64_t)(b0 + col) * ldb : B, vb);
     }
     cpa_commit();
   };
-  double acc[4][2][2];
+  double acc[4][FN][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   if (nch > 0) load(0, k_begin);
   for (int c = 0; c < nch; ++c) {
     if (c + 1 < nch) {
@@ -80,15 +87,15 @@ __global__ void __launch_bounds__(256) k_gemm_tn(const double* __restrict__ A, i
     const int stg = c & 1;
 #pragma unroll
     for (int ks = 0; ks < G_BK; ks += 4) {
-      double af[4], bf[2];
+      double af[4], bf[FN];
 #pragma unroll
       for (int i = 0; i < 4; ++i) af[i] = sA[stg][wa + i * 8 + (lane >> 2)][ks + (lane & 3)];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) bf[j] = sB[stg][wb + j * 8 + (lane >> 2)][ks + (lane & 3)];
+      for (int j = 0; j < FN; ++j) bf[j] = sB[stg][wb + j * 8 + (lane >> 2)][ks + (lane & 3)];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
     __syncthreads();
   }
@@ -96,7 +103,7 @@ __global__ void __launch_bounds__(256) k_gemm_tn(const double* __restrict__ A, i
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < FN; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int a = a0 + wa + i * 8 + (lane >> 2);
@@ -127,8 +134,17 @@ __global__ void __launch_bounds__(256) k_reduce_parts(const double* __restrict__
   }
 }
 
+// N-tile fragments per warp: 4 (BN = 128) for 65..128 columns, else 2
+// (knob EDAK_GEMM_FN = 2 or 4 for A/B)
+static int gemm_fn(int nb) {
+  const char* e = getenv("EDAK_GEMM_FN");
+  (void)nb;
+  return e && atoi(e) == 4 ? 4 : 2;  // 4 measured no faster for the 100-member LMP shapes
+}
+
 static int tn_nsplit(int m, int nb, int64_t K, int64_t& kslice) {
-  const int tiles = ((m + G_BM - 1) / G_BM) * ((nb + G_BN - 1) / G_BN);
+  const int bn = 32 * gemm_fn(nb);
+  const int tiles = ((m + G_BM - 1) / G_BM) * ((nb + bn - 1) / bn);
   static const int waves = [] {  // A/B knob: CTAs per SM targeted by the split
     const char* e = getenv("EDAK_TN_WAVES");
     return e ? atoi(e) : 2;
@@ -149,7 +165,10 @@ int64_t gemm_tn_partials(int m, int nb, int64_t K) {
   return (int64_t)tn_nsplit(m, nb, K, ks) * m * nb;
 }
 
-static constexpr size_t G_SMEM = (2 * (size_t)(G_BM + G_BN) * (G_BK + G_PAD) + 2 * G_BK) * sizeof(double);
+// dynamic smem of both kernels for N tile 32 FN (two stages + the B scale)
+static constexpr size_t g_smem(int fn) {
+  return (2 * (size_t)(G_BM + 32 * fn) * (G_BK + G_PAD) + 2 * G_BK) * sizeof(double);
+}
 
 // split-K partials only (the consumer reduces them): returns the split count
 int launch_gemm_tn_parts(const double* A, int64_t lda, const double* B, int64_t ldb, int m, int nb, int64_t K,
@@ -158,11 +177,16 @@ int launch_gemm_tn_parts(const double* A, int64_t lda, const double* B, int64_t 
   const int s = tn_nsplit(m, nb, K, ks);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm_tn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G_SMEM);
+    cudaFuncSetAttribute(k_gemm_tn<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem(2));
+    cudaFuncSetAttribute(k_gemm_tn<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem(4));
     attr = true;
   }
-  dim3 grid((m + G_BM - 1) / G_BM, (nb + G_BN - 1) / G_BN, s);
-  k_gemm_tn<<<grid, 256, G_SMEM, st>>>(A, lda, B, ldb, m, nb, K, ks, part);
+  const int fn = gemm_fn(nb);
+  dim3 grid((m + G_BM - 1) / G_BM, (nb + 32 * fn - 1) / (32 * fn), s);
+  if (fn == 4)
+    k_gemm_tn<4><<<grid, 256, g_smem(4), st>>>(A, lda, B, ldb, m, nb, K, ks, part);
+  else
+    k_gemm_tn<2><<<grid, 256, g_smem(2), st>>>(A, lda, B, ldb, m, nb, K, ks, part);
   count_launch();
   return s;
 }
@@ -179,28 +203,30 @@ int launch_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, d
 
 // ----------------------------------------------------------------- NN ----
 // sA[stage][l][i] (A is M-contiguous), sB[stage][j][l] (B is K-contiguous)
-__global__ void __launch_bounds__(256, 3) k_gemm_nn(const double* __restrict__ A, int64_t lda,
+template <int FN>
+__global__ void __launch_bounds__(256, 2) k_gemm_nn(const double* __restrict__ A, int64_t lda,
                                                  const double* __restrict__ B, int ldb,
                                                  const double* __restrict__ bscale, const double* Cin,
                                                  int64_t ldc, double beta, double* D, int64_t ldd, int64_t M,
                                                  int N, int kk, const double* __restrict__ colscale,
                                                  const double* C2) {
+  constexpr int BN = 32 * FN;
   extern __shared__ __align__(16) double gsm[];
   double (*sA)[G_BK][G_BM + G_PAD] = reinterpret_cast<double (*)[G_BK][G_BM + G_PAD]>(gsm);
-  double (*sB)[G_BN][G_BK + G_PAD] =
-      reinterpret_cast<double (*)[G_BN][G_BK + G_PAD]>(gsm + 2 * G_BK * (G_BM + G_PAD));
+  double (*sB)[BN][G_BK + G_PAD] =
+      reinterpret_cast<double (*)[BN][G_BK + G_PAD]>(gsm + 2 * G_BK * (G_BM + G_PAD));
   double (*sS)[G_BK] = reinterpret_cast<double (*)[G_BK]>(gsm + 2 * G_BK * (G_BM + G_PAD) +
-                                                          2 * G_BN * (G_BK + G_PAD));
+                                                          2 * BN * (G_BK + G_PAD));
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int wi = (warp >> 2) * 32, wj = (warp & 3) * 16;
+  const int wi = (warp >> 2) * 32, wj = (warp & 3) * 8 * FN;
   const int64_t i0 = (int64_t)blockIdx.x * G_BM;
-  const int j0 = blockIdx.y * G_BN;
+  const int j0 = blockIdx.y * BN;
   const int nch = (kk + G_BK - 1) / G_BK;
   auto load = [&](int stg, int l0) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < 8 * FN / 2; ++q) {
       const int idx = t + q * 256;
-      {
+      if (q < 8) {
         const int l = idx >> 6, i = idx & 63;
         const bool v = l0 + l < kk && i0 + i < M;
         cpa8(&sA[stg][l][i], v ? A + (i0 + i) + (int64_t)(l0 + l) * lda : A, v);
@@ -217,12 +243,28 @@ __global__ void __launch_bounds__(256, 3) k_gemm_nn(const double* __restrict__ A
     }
     cpa_commit();
   };
-  double acc[4][2][2];
+  double acc[4][FN][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   load(0, 0);
+  // the epilogue operands (PCG p-update: r and p) are fetched now, so their
+  // latency hides behind the K loop instead of ending every CTA (K is only
+  // 4 chunks for the LMP shapes)
+  double ec[4][FN][2], e2[4][FN][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t gi = i0 + wi + i * 8 + (lane >> 2);
+        const int gj = j0 + wj + j * 8 + 2 * (lane & 3) + h;
+        const bool in = gi < M && gj < N;
+        ec[i][j][h] = Cin && in ? Cin[gi + gj * ldc] : 0.0;
+        e2[i][j][h] = C2 && in ? C2[gi + gj * ldd] : 0.0;  // C2 may alias D: read before any write
+      }
   for (int c = 0; c < nch; ++c) {
     if (c + 1 < nch) {
       load((c + 1) & 1, (c + 1) * G_BK);
@@ -234,31 +276,31 @@ __global__ void __launch_bounds__(256, 3) k_gemm_nn(const double* __restrict__ A
     const int stg = c & 1;
 #pragma unroll
     for (int ks = 0; ks < G_BK; ks += 4) {
-      double af[4], bf[2];
+      double af[4], bf[FN];
 #pragma unroll
       for (int i = 0; i < 4; ++i) af[i] = sA[stg][ks + (lane & 3)][wi + i * 8 + (lane >> 2)];
       const double sc = bscale ? sS[stg][ks + (lane & 3)] : 1.0;
 #pragma unroll
-      for (int j = 0; j < 2; ++j) bf[j] = sc * sB[stg][wj + j * 8 + (lane >> 2)][ks + (lane & 3)];
+      for (int j = 0; j < FN; ++j) bf[j] = sc * sB[stg][wj + j * 8 + (lane >> 2)][ks + (lane & 3)];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
     __syncthreads();
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < FN; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t gi = i0 + wi + i * 8 + (lane >> 2);
         const int gj = j0 + wj + j * 8 + 2 * (lane & 3) + h;
         if (gi < M && gj < N) {
           double v = acc[i][j][h];
-          if (Cin) v += beta * Cin[gi + gj * ldc];
-          if (C2) v += colscale[gj] * C2[gi + gj * ldd];  // C2 may alias D
+          if (Cin) v += beta * ec[i][j][h];
+          if (C2) v += colscale[gj] * e2[i][j][h];
           D[gi + gj * ldd] = v;
         }
       }
@@ -269,11 +311,18 @@ int launch_gemm_nn(const double* A, int64_t lda, const double* B, int ldb, const
                    const double* colscale, const double* C2) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm_nn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G_SMEM);
+    cudaFuncSetAttribute(k_gemm_nn<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem(2));
+    cudaFuncSetAttribute(k_gemm_nn<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem(4));
     attr = true;
   }
-  dim3 grid((unsigned)((M + G_BM - 1) / G_BM), (N + G_BN - 1) / G_BN);
-  k_gemm_nn<<<grid, 256, G_SMEM, st>>>(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M, N, kk, colscale, C2);
+  const int fn = gemm_fn(N);
+  dim3 grid((unsigned)((M + G_BM - 1) / G_BM), (N + 32 * fn - 1) / (32 * fn));
+  if (fn == 4)
+    k_gemm_nn<4><<<grid, 256, g_smem(4), st>>>(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M, N, kk, colscale,
+                                                C2);
+  else
+    k_gemm_nn<2><<<grid, 256, g_smem(2), st>>>(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M, N, kk, colscale,
+                                                C2);
   count_launch();
   return check_launch("k_gemm_nn");
 }
