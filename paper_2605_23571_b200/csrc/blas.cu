@@ -30,49 +30,66 @@ __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_gro
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// Both kernels: CTA tile 64 x 64, 8 warps as 2 x 4 (warp tile 32 x 16 = 4 x 2
-// DMMA.8x8x4 fragments), K chunks of 32 staged by a 2-deep cp.async
-// pipeline so the next chunk's loads overlap this chunk's DMMAs.
-constexpr int G_BM = 64, G_BK = 32, G_PAD = 4;
+// Both kernels: 8 warps as WM x (8 / WM), each warp FM x FN DMMA.8x8x4
+// fragments, so the CTA tile is BM = 8 WM FM rows by BN = 8 (8 / WM) FN
+// columns; K chunks of 32 staged by a 2-deep cp.async pipeline so the next
+// chunk's loads overlap this chunk's DMMAs.  Two tilings:
+//   <2, 4, 2>: 64 x 64 (general shapes)
+//   <4, 2, 7>: 64 x 112 -- one N tile for the 65..112-member groups of the
+//              batched PCG (100 at cfg4: 13 live fragments of 14, against
+//              128 columns for two 64-wide tiles), 14 DMMAs per 9 fragment
+//              loads; fragments wholly past N are skipped (warp-uniform).
+constexpr int G_BK = 32, G_PAD = 4;
+
+template <int WM, int FM, int FN>
+struct GTile {
+  static constexpr int WN = 8 / WM, BM = 8 * WM * FM, BN = 8 * WN * FN;
+  static constexpr size_t smem_tn = (2 * (size_t)(BM + BN) * (G_BK + G_PAD)) * sizeof(double);
+  static constexpr size_t smem_nn =
+      (2 * (size_t)G_BK * (BM + G_PAD) + 2 * (size_t)BN * (G_BK + G_PAD) + 2 * G_BK) * sizeof(double);
+};
 
 // ----------------------------------------------------------------- TN ----
-// sA[stage][col a][k], sB[stage][col b][k]  (both operands K-contiguous).
-// FN = DMMA fragments per warp along N: CTA N tile BN = 32 FN (FN = 2: 64,
-// FN = 4: 128 -- one N tile for a 100-member group)
-template <int FN>
+// sA[stage][col a][k], sB[stage][col b][k]  (both operands K-contiguous)
+template <int WM, int FM, int FN>
 __global__ void __launch_bounds__(256) k_gemm_tn(const double* __restrict__ A, int64_t lda,
                                                  const double* __restrict__ B, int64_t ldb, int m, int nb,
                                                  int64_t K, int64_t kslice, double* __restrict__ part) {
-  constexpr int BN = 32 * FN;
+  using GT = GTile<WM, FM, FN>;
+  constexpr int BM = GT::BM, BN = GT::BN;
   extern __shared__ __align__(16) double gsm[];
-  double (*sA)[G_BM][G_BK + G_PAD] = reinterpret_cast<double (*)[G_BM][G_BK + G_PAD]>(gsm);
-  double (*sB)[BN][G_BK + G_PAD] =
-      reinterpret_cast<double (*)[BN][G_BK + G_PAD]>(gsm + 2 * G_BM * (G_BK + G_PAD));
+  double (*sA)[BM][G_BK + G_PAD] = reinterpret_cast<double (*)[BM][G_BK + G_PAD]>(gsm);
+  double (*sB)[BN][G_BK + G_PAD] = reinterpret_cast<double (*)[BN][G_BK + G_PAD]>(gsm + 2 * BM * (G_BK + G_PAD));
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int wa = (warp >> 2) * 32, wb = (warp & 3) * 8 * FN;
-  const int a0 = blockIdx.x * G_BM, b0 = blockIdx.y * BN;
+  const int wa = (warp % WM) * 8 * FM, wb = (warp / WM) * 8 * FN;
+  const int a0 = blockIdx.x * BM, b0 = blockIdx.y * BN;
   const int64_t k_begin = (int64_t)blockIdx.z * kslice;
   const int64_t k_end = min(K, k_begin + kslice);
   const int nch = (int)((k_end - k_begin + G_BK - 1) / G_BK);
   auto load = [&](int stg, int64_t k0) {
 #pragma unroll
-    for (int q = 0; q < 8 * FN / 2; ++q) {
+    for (int q = 0; q < (BM + BN) * G_BK / 256; ++q) {
       const int idx = t + q * 256;
       const int col = idx >> 5, kk = idx & 31;
       const int64_t k = k0 + kk;
       const bool kin = k < k_end;
-      if (q < 8) {
+      if (col < BM) {
         const bool va = kin && a0 + col < m;
         cpa8(&sA[stg][col][kk], va ? A + k + (int64_t)(a0 + col) * lda : A, va);
+      } else {
+        const int c = col - BM;
+        const bool vb = kin && b0 + c < nb;
+        cpa8(&sB[stg][c][kk], vb ? B + k + (int64_t)(b0 + c) * ldb : B, vb);
       }
-      const bool vb = kin && b0 + col < nb;
-      cpa8(&sB[stg][col][kk], vb ? B + k + (int64_t)(b0 + col) * ldb : B, vb);
     }
     cpa_commit();
   };
-  double acc[4][FN][2];
+  // fragments wholly past nb are skipped (warp-uniform)
+  int nfr = (nb - b0 - wb + 7) / 8;
+  nfr = nfr < 0 ? 0 : (nfr > FN ? FN : nfr);
+  double acc[FM][FN][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
     for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   if (nch > 0) load(0, k_begin);
@@ -87,21 +104,23 @@ __global__ void __launch_bounds__(256) k_gemm_tn(const double* __restrict__ A, i
     const int stg = c & 1;
 #pragma unroll
     for (int ks = 0; ks < G_BK; ks += 4) {
-      double af[4], bf[FN];
+      double af[FM], bf[FN];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = sA[stg][wa + i * 8 + (lane >> 2)][ks + (lane & 3)];
+      for (int i = 0; i < FM; ++i) af[i] = sA[stg][wa + i * 8 + (lane >> 2)][ks + (lane & 3)];
 #pragma unroll
-      for (int j = 0; j < FN; ++j) bf[j] = sB[stg][wb + j * 8 + (lane >> 2)][ks + (lane & 3)];
+      for (int j = 0; j < FN; ++j)
+        if (j < nfr) bf[j] = sB[stg][wb + j * 8 + (lane >> 2)][ks + (lane & 3)];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < FN; ++j)
+          if (j < nfr) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
     __syncthreads();
   }
   double* P = part + (size_t)blockIdx.z * m * nb;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
     for (int j = 0; j < FN; ++j)
 #pragma unroll
@@ -134,23 +153,22 @@ __global__ void __launch_bounds__(256) k_reduce_parts(const double* __restrict__
   }
 }
 
-// N-tile fragments per warp: 4 (BN = 128) for 65..128 columns, else 2
-// (knob EDAK_GEMM_FN = 2 or 4 for A/B)
-static int gemm_fn(int nb) {
-  const char* e = getenv("EDAK_GEMM_FN");
-  (void)nb;
-  return e && atoi(e) == 4 ? 4 : 2;  // 4 measured no faster for the 100-member LMP shapes
+// tiling for N columns: 64 x 112 for 65..112 (EDAK_GEMM_WIDE=0: always 64 x 64)
+static bool gemm_wide(int nb) {
+  const char* e = getenv("EDAK_GEMM_WIDE");
+  if (e && atoi(e) == 0) return false;
+  return nb > 64 && nb <= 112;
 }
 
 static int tn_nsplit(int m, int nb, int64_t K, int64_t& kslice) {
-  const int bn = 32 * gemm_fn(nb);
-  const int tiles = ((m + G_BM - 1) / G_BM) * ((nb + bn - 1) / bn);
+  const int bn = gemm_wide(nb) ? GTile<4, 2, 7>::BN : GTile<2, 4, 2>::BN;
+  const int tiles = ((m + 63) / 64) * ((nb + bn - 1) / bn);
   static const int waves = [] {  // A/B knob: CTAs per SM targeted by the split
     const char* e = getenv("EDAK_TN_WAVES");
     return e ? atoi(e) : 2;
   }();
   int64_t want = (waves * 148 + tiles - 1) / tiles;
-  int64_t maxs = (K + 255) / 256;                // slices of >= 256 rows
+  int64_t maxs = (K + 127) / 128;                // slices of >= 128 rows
   int64_t s = want < maxs ? want : maxs;
   if (s < 1) s = 1;
   kslice = (K + s - 1) / s;
@@ -165,28 +183,26 @@ int64_t gemm_tn_partials(int m, int nb, int64_t K) {
   return (int64_t)tn_nsplit(m, nb, K, ks) * m * nb;
 }
 
-// dynamic smem of both kernels for N tile 32 FN (two stages + the B scale)
-static constexpr size_t g_smem(int fn) {
-  return (2 * (size_t)(G_BM + 32 * fn) * (G_BK + G_PAD) + 2 * G_BK) * sizeof(double);
-}
-
 // split-K partials only (the consumer reduces them): returns the split count
 int launch_gemm_tn_parts(const double* A, int64_t lda, const double* B, int64_t ldb, int m, int nb, int64_t K,
                          double* part, cudaStream_t st) {
+  using G0 = GTile<2, 4, 2>;
+  using G1 = GTile<4, 2, 7>;
   int64_t ks;
   const int s = tn_nsplit(m, nb, K, ks);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm_tn<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem(2));
-    cudaFuncSetAttribute(k_gemm_tn<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem(4));
+    cudaFuncSetAttribute(k_gemm_tn<2, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G0::smem_tn);
+    cudaFuncSetAttribute(k_gemm_tn<4, 2, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G1::smem_tn);
     attr = true;
   }
-  const int fn = gemm_fn(nb);
-  dim3 grid((m + G_BM - 1) / G_BM, (nb + 32 * fn - 1) / (32 * fn), s);
-  if (fn == 4)
-    k_gemm_tn<4><<<grid, 256, g_smem(4), st>>>(A, lda, B, ldb, m, nb, K, ks, part);
-  else
-    k_gemm_tn<2><<<grid, 256, g_smem(2), st>>>(A, lda, B, ldb, m, nb, K, ks, part);
+  if (gemm_wide(nb)) {
+    dim3 grid((m + G1::BM - 1) / G1::BM, (nb + G1::BN - 1) / G1::BN, s);
+    k_gemm_tn<4, 2, 7><<<grid, 256, G1::smem_tn, st>>>(A, lda, B, ldb, m, nb, K, ks, part);
+  } else {
+    dim3 grid((m + G0::BM - 1) / G0::BM, (nb + G0::BN - 1) / G0::BN, s);
+    k_gemm_tn<2, 4, 2><<<grid, 256, G0::smem_tn, st>>>(A, lda, B, ldb, m, nb, K, ks, part);
+  }
   count_launch();
   return s;
 }
@@ -203,39 +219,39 @@ int launch_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, d
 
 // ----------------------------------------------------------------- NN ----
 // sA[stage][l][i] (A is M-contiguous), sB[stage][j][l] (B is K-contiguous)
-template <int FN>
+template <int WM, int FM, int FN>
 __global__ void __launch_bounds__(256, 2) k_gemm_nn(const double* __restrict__ A, int64_t lda,
                                                  const double* __restrict__ B, int ldb,
                                                  const double* __restrict__ bscale, const double* Cin,
                                                  int64_t ldc, double beta, double* D, int64_t ldd, int64_t M,
                                                  int N, int kk, const double* __restrict__ colscale,
                                                  const double* C2) {
-  constexpr int BN = 32 * FN;
+  using GT = GTile<WM, FM, FN>;
+  constexpr int BM = GT::BM, BN = GT::BN;
   extern __shared__ __align__(16) double gsm[];
-  double (*sA)[G_BK][G_BM + G_PAD] = reinterpret_cast<double (*)[G_BK][G_BM + G_PAD]>(gsm);
-  double (*sB)[BN][G_BK + G_PAD] =
-      reinterpret_cast<double (*)[BN][G_BK + G_PAD]>(gsm + 2 * G_BK * (G_BM + G_PAD));
-  double (*sS)[G_BK] = reinterpret_cast<double (*)[G_BK]>(gsm + 2 * G_BK * (G_BM + G_PAD) +
-                                                          2 * BN * (G_BK + G_PAD));
+  double (*sA)[G_BK][BM + G_PAD] = reinterpret_cast<double (*)[G_BK][BM + G_PAD]>(gsm);
+  double (*sB)[BN][G_BK + G_PAD] = reinterpret_cast<double (*)[BN][G_BK + G_PAD]>(gsm + 2 * G_BK * (BM + G_PAD));
+  double (*sS)[G_BK] =
+      reinterpret_cast<double (*)[G_BK]>(gsm + 2 * G_BK * (BM + G_PAD) + 2 * BN * (G_BK + G_PAD));
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int wi = (warp >> 2) * 32, wj = (warp & 3) * 8 * FN;
-  const int64_t i0 = (int64_t)blockIdx.x * G_BM;
+  const int wi = (warp % WM) * 8 * FM, wj = (warp / WM) * 8 * FN;
+  const int64_t i0 = (int64_t)blockIdx.x * BM;
   const int j0 = blockIdx.y * BN;
   const int nch = (kk + G_BK - 1) / G_BK;
   auto load = [&](int stg, int l0) {
 #pragma unroll
-    for (int q = 0; q < 8 * FN / 2; ++q) {
+    for (int q = 0; q < BM * G_BK / 256; ++q) {
       const int idx = t + q * 256;
-      if (q < 8) {
-        const int l = idx >> 6, i = idx & 63;
-        const bool v = l0 + l < kk && i0 + i < M;
-        cpa8(&sA[stg][l][i], v ? A + (i0 + i) + (int64_t)(l0 + l) * lda : A, v);
-      }
-      {
-        const int j = idx >> 5, l = idx & 31;
-        const bool v = l0 + l < kk && j0 + j < N;
-        cpa8(&sB[stg][j][l], v ? B + (l0 + l) + (int64_t)(j0 + j) * ldb : B, v);
-      }
+      const int l = idx / BM, i = idx % BM;
+      const bool v = l0 + l < kk && i0 + i < M;
+      cpa8(&sA[stg][l][i], v ? A + (i0 + i) + (int64_t)(l0 + l) * lda : A, v);
+    }
+#pragma unroll
+    for (int q = 0; q < BN * G_BK / 256; ++q) {
+      const int idx = t + q * 256;
+      const int j = idx >> 5, l = idx & 31;
+      const bool v = l0 + l < kk && j0 + j < N;
+      cpa8(&sB[stg][j][l], v ? B + (l0 + l) + (int64_t)(j0 + j) * ldb : B, v);
     }
     if (bscale && t < G_BK) {
       const bool v = l0 + t < kk;
@@ -243,18 +259,21 @@ __global__ void __launch_bounds__(256, 2) k_gemm_nn(const double* __restrict__ A
     }
     cpa_commit();
   };
-  double acc[4][FN][2];
+  int nfr = (N - j0 - wj + 7) / 8;  // live fragments of this warp (warp-uniform)
+  nfr = nfr < 0 ? 0 : (nfr > FN ? FN : nfr);
+  double acc[FM][FN][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
     for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   load(0, 0);
   // the epilogue operands (PCG p-update: r and p) are fetched now, so their
   // latency hides behind the K loop instead of ending every CTA (K is only
-  // 4 chunks for the LMP shapes)
-  double ec[4][FN][2], e2[4][FN][2];
+  // 4 chunks for the LMP shapes); the wide tiling has no registers to spare
+  constexpr bool PRE = FM * FN <= 8;
+  double ec[FM][FN][2], e2[FM][FN][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < (PRE ? FM : 0); ++i)
 #pragma unroll
     for (int j = 0; j < FN; ++j)
 #pragma unroll
@@ -276,21 +295,23 @@ __global__ void __launch_bounds__(256, 2) k_gemm_nn(const double* __restrict__ A
     const int stg = c & 1;
 #pragma unroll
     for (int ks = 0; ks < G_BK; ks += 4) {
-      double af[4], bf[FN];
+      double af[FM], bf[FN];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = sA[stg][ks + (lane & 3)][wi + i * 8 + (lane >> 2)];
+      for (int i = 0; i < FM; ++i) af[i] = sA[stg][ks + (lane & 3)][wi + i * 8 + (lane >> 2)];
       const double sc = bscale ? sS[stg][ks + (lane & 3)] : 1.0;
 #pragma unroll
-      for (int j = 0; j < FN; ++j) bf[j] = sc * sB[stg][wj + j * 8 + (lane >> 2)][ks + (lane & 3)];
+      for (int j = 0; j < FN; ++j)
+        if (j < nfr) bf[j] = sc * sB[stg][wj + j * 8 + (lane >> 2)][ks + (lane & 3)];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < FN; ++j)
+          if (j < nfr) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
     for (int j = 0; j < FN; ++j)
 #pragma unroll
@@ -299,8 +320,8 @@ __global__ void __launch_bounds__(256, 2) k_gemm_nn(const double* __restrict__ A
         const int gj = j0 + wj + j * 8 + 2 * (lane & 3) + h;
         if (gi < M && gj < N) {
           double v = acc[i][j][h];
-          if (Cin) v += beta * ec[i][j][h];
-          if (C2) v += colscale[gj] * e2[i][j][h];
+          if (Cin) v += beta * (PRE ? ec[i][j][h] : Cin[gi + gj * ldc]);
+          if (C2) v += colscale[gj] * (PRE ? e2[i][j][h] : C2[gi + gj * ldd]);  // C2 may alias D
           D[gi + gj * ldd] = v;
         }
       }
@@ -309,20 +330,27 @@ __global__ void __launch_bounds__(256, 2) k_gemm_nn(const double* __restrict__ A
 int launch_gemm_nn(const double* A, int64_t lda, const double* B, int ldb, const double* bscale, const double* Cin,
                    int64_t ldc, double beta, double* D, int64_t ldd, int64_t M, int N, int kk, cudaStream_t st,
                    const double* colscale, const double* C2) {
+  using G0 = GTile<2, 4, 2>;
+  using G1 = GTile<4, 2, 7>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm_nn<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem(2));
-    cudaFuncSetAttribute(k_gemm_nn<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem(4));
+    cudaFuncSetAttribute(k_gemm_nn<2, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G0::smem_nn);
+    cudaFuncSetAttribute(k_gemm_nn<4, 2, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G1::smem_nn);
     attr = true;
   }
-  const int fn = gemm_fn(N);
-  dim3 grid((unsigned)((M + G_BM - 1) / G_BM), (N + 32 * fn - 1) / (32 * fn));
-  if (fn == 4)
-    k_gemm_nn<4><<<grid, 256, g_smem(4), st>>>(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M, N, kk, colscale,
-                                                C2);
-  else
-    k_gemm_nn<2><<<grid, 256, g_smem(2), st>>>(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M, N, kk, colscale,
-                                                C2);
+  // the p-update (K = 128) keeps the 64 x 64 tiling: its epilogue-operand
+  // prefetch needs the registers the wide tiling spends on accumulators
+  // (measured: 35.5 us narrow vs 35.8 us wide per 100-member group)
+  const char* ew = getenv("EDAK_GEMM_WIDE_NN");
+  if (ew && atoi(ew) != 0 && gemm_wide(N)) {
+    dim3 grid((unsigned)((M + G1::BM - 1) / G1::BM), (N + G1::BN - 1) / G1::BN);
+    k_gemm_nn<4, 2, 7><<<grid, 256, G1::smem_nn, st>>>(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M, N, kk,
+                                                       colscale, C2);
+  } else {
+    dim3 grid((unsigned)((M + G0::BM - 1) / G0::BM), (N + G0::BN - 1) / G0::BN);
+    k_gemm_nn<2, 4, 2><<<grid, 256, G0::smem_nn, st>>>(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M, N, kk,
+                                                       colscale, C2);
+  }
   count_launch();
   return check_launch("k_gemm_nn");
 }

@@ -275,12 +275,21 @@ int edak_pcg_lmp_beta(int n, int k, int ncols, const double* S, const double* co
   int rc;
   // W = S^T r (lmp.py:63) as split-K partials; their reduction, rz_new =
   // |r|^2 + W^T diag(coef) W and beta in one kernel
+#ifdef EDAK_EXP_NOGEMM  // timing experiment only (wrong results): the pass without its LMP GEMMs
+  int64_t ks_;
+  const int nsplit = 1;
+  (void)ks_;
+#else
   const int nsplit = launch_gemm_tn_parts(S, n, r, n, k, ncols, n, part, st);
+#endif
   if ((rc = check_launch("k_gemm_tn"))) return rc;
   if ((rc = launch_pcg_reduce_rz(n, ncols, k, part, nsplit, W, coef, work, rtol, hist_rz, hist_J, hist_ld, status,
                                  iters, it, st)))
     return rc;
   // p = r + beta p + S (coef o W)  (= z + beta p, krylov.py:95 with z = P r)
+#ifdef EDAK_EXP_NOGEMM
+  return EDAK_OK;
+#endif
   return launch_gemm_nn(S, n, W, k, coef, r, n, 1.0, p, n, n, ncols, k, st, pcg_beta_ptr(n, ncols, work), p);
 }
 
