@@ -151,6 +151,9 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
     gw[j] = (R.t < R.nact && e >= wlo && e < whi) ? __ldg(P.gpos + R.gidx(j)) : -1;
   }
   auto capture_tp = [&](int tp) {
+#ifdef EDAK_EXP_NOCAPTURE  // timing ablation (wrong results): no observation capture / forcing
+    return;
+#endif
     if (tp < 0) return;
 #pragma unroll
     for (int j = 0; j < C; ++j)
@@ -339,6 +342,9 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
   // its end, so its global latency hides behind the step instead of stalling
   // every warp of the CTA at once (long_scoreboard in the ncu profile)
   auto fetch_force = [&](int tp, int sbuf) {
+#ifdef EDAK_EXP_NOCAPTURE
+    return;
+#endif
     if (tp < 0) return;
     const double* f = fc + (size_t)tp * G;
     double* d = FS + (size_t)sbuf * C * NT + threadIdx.x;
@@ -347,6 +353,9 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
       if (is_obs(j)) cp_async8(d + j * NT, f + gpos_of(j));
   };
   auto add_fetched = [&](int tp, int sbuf, double (&gg)[C + 4]) {
+#ifdef EDAK_EXP_NOCAPTURE
+    return;
+#endif
     if (tp < 0) return;
     const double* d = FS + (size_t)sbuf * C * NT + threadIdx.x;
 #pragma unroll

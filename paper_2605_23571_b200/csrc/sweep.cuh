@@ -76,34 +76,41 @@ struct Ring {
     }
   }
 
-  // publish first two / last two own values into sh[4][NT + 2] (slot t + 1);
-  // slots 0 and NT + 1 are zero pads, so a tile's edge threads read zeros
-  // without a branch (their halo is in the budgeted garbage zone anyway)
+  // publish the first two / last two own values as two 16-byte pairs into
+  // the planes sh2[0][NT + 2] (first pair) and sh2[1][NT + 2] (last pair),
+  // slot t + 1: one STS.128 / LDS.128 per pair instead of two 8-byte
+  // accesses (the halo traffic was ~28% of the TL sweep, ablation in
+  // profiles/r1_sweep_knobs_ab.txt).  Slots 0 and NT + 1 are zero pads, so a
+  // tile's edge threads read zeros without a branch (their halo is in the
+  // budgeted garbage zone anyway).
   static constexpr int S = NT + 2;
   __device__ __forceinline__ void put(double* sh, const double (&a)[C + 4]) const {
-    sh[0 * S + t + 1] = a[2];
-    sh[1 * S + t + 1] = a[3];
-    sh[2 * S + t + 1] = a[C];
-    sh[3 * S + t + 1] = a[C + 1];
+    double2* p = reinterpret_cast<double2*>(sh);
+    p[t + 1] = make_double2(a[2], a[3]);
+    p[S + t + 1] = make_double2(a[C], a[C + 1]);
   }
   __device__ __forceinline__ void get(const double* sh, double (&a)[C + 4]) const {
-    a[0] = sh[2 * S + prev + 1];
-    a[1] = sh[3 * S + prev + 1];
-    a[C + 2] = sh[0 * S + next + 1];
-    a[C + 3] = sh[1 * S + next + 1];
+    const double2* p = reinterpret_cast<const double2*>(sh);
+    const double2 l = p[S + prev + 1], r = p[next + 1];
+    a[0] = l.x;
+    a[1] = l.y;
+    a[C + 2] = r.x;
+    a[C + 3] = r.y;
   }
 };
 
-// shared-memory exchange buffers: [2 bufs][2 arrays][4 slots][NT]
+// shared-memory exchange buffers: [2 bufs][2 arrays][2 planes of NT + 2
+// 16-byte pairs] (stored as [4][NT + 2] doubles: the same bytes)
 template <int NT>
 struct XBuf {
   double v[2][2][4][NT + 2];
   // zero the pad slots (call once before the first exchange's barrier)
   __device__ __forceinline__ void init_pads() {
     const int i = threadIdx.x;
-    if (i < 32) {
-      const int b = i >> 4, a = (i >> 3) & 1, k = (i >> 1) & 3, side = i & 1;
-      v[b][a][k][side ? NT + 1 : 0] = 0.0;
+    if (i < 16) {
+      const int b = i >> 3, a = (i >> 2) & 1, plane = (i >> 1) & 1, side = i & 1;
+      double2* p = reinterpret_cast<double2*>(&v[b][a][0][0]);
+      p[plane * (NT + 2) + (side ? NT + 1 : 0)] = make_double2(0.0, 0.0);
     }
   }
 };
@@ -115,8 +122,13 @@ struct XBuf {
 #define EDAK_XSYNC() __syncthreads()
 #endif
 
+// EDAK_EXP_NOXCHG: timing ablation (wrong results): barriers without the halo traffic
 template <int C, int NT>
 __device__ __forceinline__ void xchg1(const Ring<C, NT>& R, XBuf<NT>& X, int& buf, double (&a)[C + 4]) {
+#ifdef EDAK_EXP_NOXCHG
+  EDAK_XSYNC();
+  return;
+#endif
   R.put(&X.v[buf][0][0][0], a);
   EDAK_XSYNC();
   R.get(&X.v[buf][0][0][0], a);
@@ -126,6 +138,10 @@ __device__ __forceinline__ void xchg1(const Ring<C, NT>& R, XBuf<NT>& X, int& bu
 template <int C, int NT>
 __device__ __forceinline__ void xchg2(const Ring<C, NT>& R, XBuf<NT>& X, int& buf, double (&a)[C + 4],
                                       double (&b)[C + 4]) {
+#ifdef EDAK_EXP_NOXCHG
+  EDAK_XSYNC();
+  return;
+#endif
   R.put(&X.v[buf][0][0][0], a);
   R.put(&X.v[buf][1][0][0], b);
   EDAK_XSYNC();
@@ -220,6 +236,10 @@ struct Stage2 {
   // pairs m < (used + 4) / 2 are copied
   __device__ static __forceinline__ void stage(double* buf, const double* __restrict__ src, int gm2, int n,
                                                int used) {
+#ifdef EDAK_EXP_NOSTAGE  // timing ablation (wrong results): no state staging
+    cp_commit();
+    return;
+#endif
     const int t = threadIdx.x;
     const int np = (used + 4) >> 1;
     double* d = buf + 2 * t + 2 * (t / (C / 2));
