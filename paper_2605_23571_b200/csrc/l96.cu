@@ -748,7 +748,7 @@ v1:
       else
         go<64, 16>(k_tl<16, 64, false, 4, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
     } else if (C == 16 && NT == 128 && !stream && pair_ok(P, geo)) {
-      go<128, 16>(k_tl<16, 128, false, 2, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
+      go<128, 16, 0, 3>(k_tl<16, 128, false, 2, true, 2>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
     } else if (C == 12 && NT == 96 && !stream && pair_ok(P, geo)) {
       go<96, 12>(k_tl<12, 96, false, 4, true>, grid, st, *P, vin, obs, col_traj, geo, s0, s1, vout);
     } else if (C == 8 && NT == 256 && !stream && pair_ok(P, geo)) {
@@ -858,7 +858,7 @@ v1:
         go<64, 16, 2 * 16 * 64>(k_ad<16, 64, false, 3, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1,
                                 gin);
     } else if (C == 16 && NT == 128 && !stream && pair_ok(P, geo)) {
-      go<128, 16, 2 * 16 * 128>(k_ad<16, 128, false, 1, true>, grid, st, *P, forcing, gout, col_traj, geo, s0,
+      go<128, 16, 2 * 16 * 128>(k_ad<16, 128, false, 2, true>, grid, st, *P, forcing, gout, col_traj, geo, s0,
                                 s1, gin);
     } else if (C == 12 && NT == 96 && !stream && pair_ok(P, geo)) {
       go<96, 12, 2 * 12 * 96>(k_ad<12, 96, false, 2, true>, grid, st, *P, forcing, gout, col_traj, geo, s0, s1,

@@ -1,8 +1,8 @@
 """A/B timing of sweep knobs on a config's PCG block (CFG env, default 4).
 
-    python tools/ab_knobs.py "EDAK_SWEEP_DEPTH=1" "EDAK_SWEEP_DEPTH=2,EDAK_AD_GPS=1" ...
+    python tools/ab_knobs.py "EDAK_SWEEP_DEPTH=1" "EDAK_TL_DEPTH=1+EDAK_AD_DEPTH=2" ...
 
-Each argument is a comma-separated set of environment assignments applied
+Each argument is a "+"-separated set of environment assignments applied
 before the launches (the library reads its knobs at launch time).  Prints TL,
 AD and full Hessian-block times and whether the results are bit-identical to
 the first variant's."""
@@ -41,12 +41,12 @@ def timeit(fn, reps=20):
 
 ref = None
 variants = sys.argv[1:] or [""]
-keys = {kv.split("=")[0] for v in variants for kv in v.split(",") if kv}
+keys = {kv.split("=")[0] for v in variants for kv in v.split("+") if kv}
 for rnd in range(2):
     for v in variants:
         for k in keys:
             os.environ.pop(k, None)
-        for kv in v.split(","):
+        for kv in v.split("+"):
             if kv:
                 k, val = kv.split("=")
                 os.environ[k] = val
