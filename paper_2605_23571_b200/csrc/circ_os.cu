@@ -16,6 +16,7 @@
 // (M / V) redundancy, against K FMAs per column for the tap convolution
 // (cfg4: M = 1024, K = 189, V = 836).
 #include "common.cuh"
+#include <cstdlib>
 
 namespace edak {
 
@@ -190,8 +191,8 @@ __device__ __forceinline__ void dit(double2* Z, const Tw<LOGM, NT>& W) {
 
 // grid (blocks of V outputs, column pairs); L = left reach of u (taps k <
 // K act on in[i + tap_w - k]: reach K - 1 - tap_w to the left, tap_w right)
-template <int LOGM, int NT>
-__global__ void __launch_bounds__(NT) k_circ_os(int n, int L, int V, int ncols, const double2* __restrict__ T,
+template <int LOGM, int NT, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) k_circ_os(int n, int L, int V, int ncols, const double2* __restrict__ T,
                                                 const double2* __restrict__ H, const double* __restrict__ in,
                                                 double* __restrict__ out, double ident,
                                                 const double* __restrict__ zadd, double* __restrict__ dotp,
@@ -286,7 +287,15 @@ int launch_circ_os(const edak_problem* P, const double* in, double* out, int nco
   dim3 grid(nb, (ncols + 1) / 2);
   const double2* T = reinterpret_cast<const double2*>(P->os_tw);
   const double2* H = reinterpret_cast<const double2*>(P->os_spec);
-  if (logm == 10)
+  // resident CTAs per SM the M = 1024 kernel is built for (A/B knob; 6 =
+  // 80 registers measured best: cfg4 U_B pair 3% faster than 1 (126 regs))
+  const char* eb = getenv("EDAK_CIRC_OS_MINB");
+  const int mb = eb ? atoi(eb) : 6;
+  if (logm == 10 && mb == 8)
+    k_circ_os<10, 128, 8><<<grid, 128, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
+  else if (logm == 10 && mb == 6)
+    k_circ_os<10, 128, 6><<<grid, 128, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
+  else if (logm == 10)
     k_circ_os<10, 128><<<grid, 128, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
   else
     k_circ_os<11, 256><<<grid, 256, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
