@@ -253,7 +253,7 @@ def pcg(apply_h, b, cfg, precond=None, cost_fn=None):
 
 
 _SIDE_STREAMS = {}
-GRAPH_MAX_ELEMS = 1 << 20  # members x n up to which pcg_members replays a CUDA graph
+GRAPH_MAX_ELEMS = 1 << 22  # members x n up to which pcg_members replays a CUDA graph
 
 
 def _side_streams(count):
@@ -327,7 +327,7 @@ def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fu
     HBM-bound vector updates and the DMMA GEMMs).  Default: 2 for >= 64
     members (EDAK_PCG_GROUPS overrides).
 
-    ``graph`` (default: for members x n <= 2^20, when the iteration count is
+    ``graph`` (default: for members x n <= 2^22, when the iteration count is
     fixed -- no residual_rtol -- and the LMP is single-pass or absent) records the whole
     solve (init + every iteration on every group stream) as ONE CUDA graph
     the first time an ensemble sees this shape, and replays it afterwards
@@ -348,7 +348,8 @@ def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fu
     if graph is None:
         env = os.environ.get("EDAK_PCG_GRAPH")
         # measured: graphs pay off where launches dominate (cfg1-3: -10..-25%
-        # per pass) and cost ~2% at cfg4 scale (two streams of long kernels)
+        # per pass) and, with the staggered member groups, still -1% at cfg4
+        # (75.5 -> 74.7 ms); no change at cfg5 (20 long iterations)
         graph = (env != "0") if env is not None else (B.numel() <= GRAPH_MAX_ELEMS)
     graph = (graph and snapshots is None and cfg.residual_rtol is None and fused
              and (precond is None or lmp is not None) and cost in ("recurrence", None))
