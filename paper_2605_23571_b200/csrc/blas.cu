@@ -105,11 +105,18 @@ __global__ void __launch_bounds__(256) k_gemm_tn(const double* __restrict__ A, i
 #pragma unroll
     for (int ks = 0; ks < G_BK; ks += 4) {
       double af[FM], bf[FN];
+#ifdef EDAK_EXP_NOFRAG  // timing ablation (wrong results): DMMAs without their fragment loads
+#pragma unroll
+      for (int i = 0; i < FM; ++i) af[i] = 1.0 + i * 1e-3 + ks;
+#pragma unroll
+      for (int j = 0; j < FN; ++j) bf[j] = 1.0 + j * 1e-3 + ks;
+#else
 #pragma unroll
       for (int i = 0; i < FM; ++i) af[i] = sA[stg][wa + i * 8 + (lane >> 2)][ks + (lane & 3)];
 #pragma unroll
       for (int j = 0; j < FN; ++j)
         if (j < nfr) bf[j] = sB[stg][wb + j * 8 + (lane >> 2)][ks + (lane & 3)];
+#endif
 #pragma unroll
       for (int i = 0; i < FM; ++i)
 #pragma unroll
@@ -296,12 +303,19 @@ __global__ void __launch_bounds__(256, 2) k_gemm_nn(const double* __restrict__ A
 #pragma unroll
     for (int ks = 0; ks < G_BK; ks += 4) {
       double af[FM], bf[FN];
+#ifdef EDAK_EXP_NOFRAG
+#pragma unroll
+      for (int i = 0; i < FM; ++i) af[i] = 1.0 + i * 1e-3 + ks;
+#pragma unroll
+      for (int j = 0; j < FN; ++j) bf[j] = 1.0 + j * 1e-3 + ks;
+#else
 #pragma unroll
       for (int i = 0; i < FM; ++i) af[i] = sA[stg][ks + (lane & 3)][wi + i * 8 + (lane >> 2)];
       const double sc = bscale ? sS[stg][ks + (lane & 3)] : 1.0;
 #pragma unroll
       for (int j = 0; j < FN; ++j)
         if (j < nfr) bf[j] = sc * sB[stg][wj + j * 8 + (lane >> 2)][ks + (lane & 3)];
+#endif
 #pragma unroll
       for (int i = 0; i < FM; ++i)
 #pragma unroll
