@@ -26,6 +26,12 @@ __device__ __forceinline__ void cpa8(double* dst, const double* src, bool valid)
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 8 : 0));
 }
+// 16-byte variant (cp.async.cg, L2 only): nbytes of 0, 8 or 16 valid source
+// bytes, the rest zero-filled
+__device__ __forceinline__ void cpa16(double* dst, const double* src, int nbytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(nbytes));
+}
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n"); }
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -51,7 +57,7 @@ struct GTile {
 
 // ----------------------------------------------------------------- TN ----
 // sA[stage][col a][k], sB[stage][col b][k]  (both operands K-contiguous)
-template <int WM, int FM, int FN>
+template <int WM, int FM, int FN, bool V16 = false>
 __global__ void __launch_bounds__(256) k_gemm_tn(const double* __restrict__ A, int64_t lda,
                                                  const double* __restrict__ B, int64_t ldb, int m, int nb,
                                                  int64_t K, int64_t kslice, double* __restrict__ part) {
@@ -67,19 +73,37 @@ __global__ void __launch_bounds__(256) k_gemm_tn(const double* __restrict__ A, i
   const int64_t k_end = min(K, k_begin + kslice);
   const int nch = (int)((k_end - k_begin + G_BK - 1) / G_BK);
   auto load = [&](int stg, int64_t k0) {
+    if constexpr (V16) {  // 16-byte pairs along K (even lda/ldb/k0, 16-byte aligned operands)
 #pragma unroll
-    for (int q = 0; q < (BM + BN) * G_BK / 256; ++q) {
-      const int idx = t + q * 256;
-      const int col = idx >> 5, kk = idx & 31;
-      const int64_t k = k0 + kk;
-      const bool kin = k < k_end;
-      if (col < BM) {
-        const bool va = kin && a0 + col < m;
-        cpa8(&sA[stg][col][kk], va ? A + k + (int64_t)(a0 + col) * lda : A, va);
-      } else {
-        const int c = col - BM;
-        const bool vb = kin && b0 + c < nb;
-        cpa8(&sB[stg][c][kk], vb ? B + k + (int64_t)(b0 + c) * ldb : B, vb);
+      for (int q = 0; q < (BM + BN) * G_BK / 512; ++q) {
+        const int idx = t + q * 256;
+        const int col = idx >> 4, kk = 2 * (idx & 15);
+        const int64_t k = k0 + kk;
+        const int nbytes = k < k_end ? (k + 1 < k_end ? 16 : 8) : 0;
+        if (col < BM) {
+          const bool va = a0 + col < m;
+          cpa16(&sA[stg][col][kk], va ? A + k + (int64_t)(a0 + col) * lda : A, va ? nbytes : 0);
+        } else {
+          const int c = col - BM;
+          const bool vb = b0 + c < nb;
+          cpa16(&sB[stg][c][kk], vb ? B + k + (int64_t)(b0 + c) * ldb : B, vb ? nbytes : 0);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < (BM + BN) * G_BK / 256; ++q) {
+        const int idx = t + q * 256;
+        const int col = idx >> 5, kk = idx & 31;
+        const int64_t k = k0 + kk;
+        const bool kin = k < k_end;
+        if (col < BM) {
+          const bool va = kin && a0 + col < m;
+          cpa8(&sA[stg][col][kk], va ? A + k + (int64_t)(a0 + col) * lda : A, va);
+        } else {
+          const int c = col - BM;
+          const bool vb = kin && b0 + c < nb;
+          cpa8(&sB[stg][c][kk], vb ? B + k + (int64_t)(b0 + c) * ldb : B, vb);
+        }
       }
     }
     cpa_commit();
@@ -201,11 +225,22 @@ int launch_gemm_tn_parts(const double* A, int64_t lda, const double* B, int64_t 
   if (!attr) {
     cudaFuncSetAttribute(k_gemm_tn<2, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G0::smem_tn);
     cudaFuncSetAttribute(k_gemm_tn<4, 2, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G1::smem_tn);
+    cudaFuncSetAttribute(k_gemm_tn<2, 4, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G0::smem_tn);
+    cudaFuncSetAttribute(k_gemm_tn<4, 2, 7, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G1::smem_tn);
     attr = true;
   }
-  if (gemm_wide(nb)) {
+  const char* ev = getenv("EDAK_GEMM_V16");
+  const bool v16 = !(ev && atoi(ev) == 0) && lda % 2 == 0 && ldb % 2 == 0 && ks % 2 == 0 &&
+                   ((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0;
+  if (gemm_wide(nb) && v16) {
+    dim3 grid((m + G1::BM - 1) / G1::BM, (nb + G1::BN - 1) / G1::BN, s);
+    k_gemm_tn<4, 2, 7, true><<<grid, 256, G1::smem_tn, st>>>(A, lda, B, ldb, m, nb, K, ks, part);
+  } else if (gemm_wide(nb)) {
     dim3 grid((m + G1::BM - 1) / G1::BM, (nb + G1::BN - 1) / G1::BN, s);
     k_gemm_tn<4, 2, 7><<<grid, 256, G1::smem_tn, st>>>(A, lda, B, ldb, m, nb, K, ks, part);
+  } else if (v16) {
+    dim3 grid((m + G0::BM - 1) / G0::BM, (nb + G0::BN - 1) / G0::BN, s);
+    k_gemm_tn<2, 4, 2, true><<<grid, 256, G0::smem_tn, st>>>(A, lda, B, ldb, m, nb, K, ks, part);
   } else {
     dim3 grid((m + G0::BM - 1) / G0::BM, (nb + G0::BN - 1) / G0::BN, s);
     k_gemm_tn<2, 4, 2><<<grid, 256, G0::smem_tn, st>>>(A, lda, B, ldb, m, nb, K, ks, part);
@@ -226,7 +261,7 @@ int launch_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, d
 
 // ----------------------------------------------------------------- NN ----
 // sA[stage][l][i] (A is M-contiguous), sB[stage][j][l] (B is K-contiguous)
-template <int WM, int FM, int FN>
+template <int WM, int FM, int FN, bool V16 = false>
 __global__ void __launch_bounds__(256, 2) k_gemm_nn(const double* __restrict__ A, int64_t lda,
                                                  const double* __restrict__ B, int ldb,
                                                  const double* __restrict__ bscale, const double* Cin,
@@ -246,19 +281,36 @@ __global__ void __launch_bounds__(256, 2) k_gemm_nn(const double* __restrict__ A
   const int j0 = blockIdx.y * BN;
   const int nch = (kk + G_BK - 1) / G_BK;
   auto load = [&](int stg, int l0) {
+    if constexpr (V16) {  // 16-byte pairs (even M offsets / lda / ldb, 16-byte aligned operands)
 #pragma unroll
-    for (int q = 0; q < BM * G_BK / 256; ++q) {
-      const int idx = t + q * 256;
-      const int l = idx / BM, i = idx % BM;
-      const bool v = l0 + l < kk && i0 + i < M;
-      cpa8(&sA[stg][l][i], v ? A + (i0 + i) + (int64_t)(l0 + l) * lda : A, v);
-    }
+      for (int q = 0; q < BM * G_BK / 512; ++q) {
+        const int idx = t + q * 256;
+        const int l = idx / (BM / 2), i = 2 * (idx % (BM / 2));
+        const int nb_ = l0 + l < kk ? (i0 + i + 1 < M ? 16 : (i0 + i < M ? 8 : 0)) : 0;
+        cpa16(&sA[stg][l][i], nb_ ? A + (i0 + i) + (int64_t)(l0 + l) * lda : A, nb_);
+      }
 #pragma unroll
-    for (int q = 0; q < BN * G_BK / 256; ++q) {
-      const int idx = t + q * 256;
-      const int j = idx >> 5, l = idx & 31;
-      const bool v = l0 + l < kk && j0 + j < N;
-      cpa8(&sB[stg][j][l], v ? B + (l0 + l) + (int64_t)(j0 + j) * ldb : B, v);
+      for (int q = 0; q < BN * G_BK / 512; ++q) {
+        const int idx = t + q * 256;
+        const int j = idx >> 4, l = 2 * (idx & 15);
+        const int nb_ = j0 + j < N ? (l0 + l + 1 < kk ? 16 : (l0 + l < kk ? 8 : 0)) : 0;
+        cpa16(&sB[stg][j][l], nb_ ? B + (l0 + l) + (int64_t)(j0 + j) * ldb : B, nb_);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < BM * G_BK / 256; ++q) {
+        const int idx = t + q * 256;
+        const int l = idx / BM, i = idx % BM;
+        const bool v = l0 + l < kk && i0 + i < M;
+        cpa8(&sA[stg][l][i], v ? A + (i0 + i) + (int64_t)(l0 + l) * lda : A, v);
+      }
+#pragma unroll
+      for (int q = 0; q < BN * G_BK / 256; ++q) {
+        const int idx = t + q * 256;
+        const int j = idx >> 5, l = idx & 31;
+        const bool v = l0 + l < kk && j0 + j < N;
+        cpa8(&sB[stg][j][l], v ? B + (l0 + l) + (int64_t)(j0 + j) * ldb : B, v);
+      }
     }
     if (bscale && t < G_BK) {
       const bool v = l0 + t < kk;
@@ -350,6 +402,7 @@ int launch_gemm_nn(const double* A, int64_t lda, const double* B, int ldb, const
   if (!attr) {
     cudaFuncSetAttribute(k_gemm_nn<2, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G0::smem_nn);
     cudaFuncSetAttribute(k_gemm_nn<4, 2, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G1::smem_nn);
+    cudaFuncSetAttribute(k_gemm_nn<2, 4, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G0::smem_nn);
     attr = true;
   }
   // the p-update (K = 128) keeps the 64 x 64 tiling: its epilogue-operand
@@ -361,9 +414,16 @@ int launch_gemm_nn(const double* A, int64_t lda, const double* B, int ldb, const
     k_gemm_nn<4, 2, 7><<<grid, 256, G1::smem_nn, st>>>(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M, N, kk,
                                                        colscale, C2);
   } else {
+    const char* ev = getenv("EDAK_GEMM_V16");
+    const bool v16 = !(ev && atoi(ev) == 0) && lda % 2 == 0 && ldb % 2 == 0 && ((uintptr_t)A & 15) == 0 &&
+                     ((uintptr_t)B & 15) == 0;
     dim3 grid((unsigned)((M + G0::BM - 1) / G0::BM), (N + G0::BN - 1) / G0::BN);
-    k_gemm_nn<2, 4, 2><<<grid, 256, G0::smem_nn, st>>>(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M, N, kk,
-                                                       colscale, C2);
+    if (v16)
+      k_gemm_nn<2, 4, 2, true><<<grid, 256, G0::smem_nn, st>>>(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M,
+                                                               N, kk, colscale, C2);
+    else
+      k_gemm_nn<2, 4, 2><<<grid, 256, G0::smem_nn, st>>>(A, lda, B, ldb, bscale, Cin, ldc, beta, D, ldd, M, N, kk,
+                                                         colscale, C2);
   }
   count_launch();
   return check_launch("k_gemm_nn");
