@@ -503,3 +503,46 @@ def test_pcg_small_breakdown_statuses(gpu):
     coef = torch.full((S.shape[0],), -3.0, dtype=torch.float64, device=B.device)
     with pytest.raises(PcgBreakdown, match="preconditioner is not positive definite"):
         pcg_members_small(ens, B, SolverConfig(max_iters=5), (S, coef))
+
+
+def test_gemm_16byte_staging_edges(gpu):
+    """The 16-byte cp.async staging of the DMMA GEMMs (even leading
+    dimensions, 16-byte aligned operands) at odd K / odd M / odd inner
+    dimension: the last pair of a row is half valid and half zero-filled.
+    Leading dimensions are padded to even sizes so the 16-byte path runs, and
+    the result equals the 8-byte path (EDAK_GEMM_V16=0) and torch."""
+    import os
+    from paper_2605_23571_b200 import _lib
+    lib = _lib.lib()
+    dev = "cuda"
+    m, nb, K, ld = 37, 5, 999, 1000                      # TN: C = A^T B over K (odd), lda = ldb = 1000
+    A = torch.randn(m, ld, dtype=torch.float64, device=dev)
+    B = torch.randn(nb, ld, dtype=torch.float64, device=dev)
+    outs = []
+    for v in ("1", "0"):
+        os.environ["EDAK_GEMM_V16"] = v
+        C = torch.empty(nb, m, dtype=torch.float64, device=dev)
+        part = torch.empty(int(lib.edak_gemm_tn_partials(m, nb, K)), dtype=torch.float64, device=dev)
+        _lib.call("edak_gemm_tn", A.data_ptr(), ld, B.data_ptr(), ld, C.data_ptr(), m, m, nb, K,
+                  part.data_ptr(), _lib.stream())
+        outs.append(C)
+    os.environ.pop("EDAK_GEMM_V16")
+    ref = B[:, :K] @ A[:, :K].t()
+    assert torch.allclose(outs[0], ref, rtol=1e-12, atol=1e-11 * K ** 0.5)
+    assert torch.equal(outs[0], outs[1])
+    M, N, kk, lda, ldb = 999, 7, 33, 1000, 34            # NN: odd M and inner dim, even lds
+    A = torch.randn(kk, lda, dtype=torch.float64, device=dev)
+    B = torch.randn(N, ldb, dtype=torch.float64, device=dev)
+    s = torch.rand(kk, dtype=torch.float64, device=dev)
+    Cin = torch.randn(N, M, dtype=torch.float64, device=dev)
+    outs = []
+    for v in ("1", "0"):
+        os.environ["EDAK_GEMM_V16"] = v
+        D = torch.empty(N, M, dtype=torch.float64, device=dev)
+        _lib.call("edak_gemm_nn", A.data_ptr(), lda, B.data_ptr(), ldb, s.data_ptr(), Cin.data_ptr(), M, 1.0,
+                  D.data_ptr(), M, M, N, kk, _lib.stream())
+        outs.append(D)
+    os.environ.pop("EDAK_GEMM_V16")
+    ref = Cin + (B[:, :kk] * s) @ A[:, :M]
+    assert torch.allclose(outs[0], ref, rtol=1e-12, atol=1e-12 * kk)
+    assert torch.equal(outs[0], outs[1])
