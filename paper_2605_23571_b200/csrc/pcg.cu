@@ -248,7 +248,13 @@ int launch_pcg_alpha(int n, int M, const double* p, const double* hp, double* x,
 // k_pcg_rz with the split-K reduction of W = S^T r folded in: one CTA per
 // column reduces its k entries (2 lanes per entry, fixed order) from the
 // GEMM's partials, writes W for the p-update GEMM, and runs the rz step.
-__global__ void __launch_bounds__(256) k_pcg_reduce_rz(int T, int M, int k, const double* __restrict__ part,
+// 1024 threads: entry i = t % 128 of a 128-entry slab (a warp reads 32
+// consecutive entries of one split row: coalesced), split group q = t / 128
+// sums splits q, q + 8, ... in order; the 8 group sums are then combined in
+// a fixed tree (deterministic).  The split-K GEMM for the 100-member groups
+// writes 128 splits, which the former 2-lanes-per-entry form summed as 64
+// dependent strided loads per thread (14 us per launch, latency-bound).
+__global__ void __launch_bounds__(1024) k_pcg_reduce_rz(int T, int M, int k, const double* __restrict__ part,
                                                        int nsplit, double* __restrict__ W,
                                                        const double* __restrict__ coef,
                                                        const double* __restrict__ part_rr,
@@ -258,21 +264,30 @@ __global__ void __launch_bounds__(256) k_pcg_reduce_rz(int T, int M, int k, cons
                                                        int hist_ld, int32_t* __restrict__ status,
                                                        int32_t* __restrict__ iters, int it) {
   __shared__ double sh[32];
+  __shared__ double gs[8][128];
   const int c = blockIdx.x, t = threadIdx.x;
+  const int e = t & 127, g = t >> 7;
   const int64_t tot = (int64_t)k * M;
   double q = 0.0;
   for (int i0 = 0; i0 < k; i0 += 128) {
-    const int i = i0 + (t >> 1), hh = t & 1;
+    const int i = i0 + e;
     double s = 0.0;
-    if (i < k)
-      for (int z = hh; z < nsplit; z += 2) s += part[(size_t)z * tot + i + (size_t)c * k];
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    if (i < k && hh == 0) {
-      W[i + (size_t)c * k] = s;
-      q += coef[i] * (s * s);
+    if (i < k) {
+      const double* pp = part + i + (size_t)c * k;
+#pragma unroll 4
+      for (int z = g; z < nsplit; z += 8) s += pp[(size_t)z * tot];
     }
+    gs[g][e] = s;
+    __syncthreads();
+    if (g == 0 && i < k) {
+      const double w = ((gs[0][e] + gs[1][e]) + (gs[2][e] + gs[3][e])) +
+                       ((gs[4][e] + gs[5][e]) + (gs[6][e] + gs[7][e]));
+      W[i + (size_t)c * k] = w;
+      q += coef[i] * (w * w);
+    }
+    __syncthreads();
   }
-  q = block_sum<256>(q, sh);
+  q = block_sum<1024>(q, sh);
   if (threadIdx.x < 32) {
     const double rr = sum_parts(part_rr + (size_t)c * T, T);
     const double xbr = hist_J ? sum_parts(part_x + (size_t)c * T, T) : 0.0;
@@ -303,7 +318,7 @@ int launch_pcg_reduce_rz(int n, int M, int k, const double* part, int nsplit, do
   double* part_rr = work + 2 * (size_t)M * T;
   double* rzb = work + 4 * (size_t)M * T;
   double* beta = rzb + 2 * (size_t)M;
-  k_pcg_reduce_rz<<<M, 256, 0, st>>>(T, M, k, part, nsplit, W, coef, part_rr, part_x, rzb, beta, rtol, hist_rz,
+  k_pcg_reduce_rz<<<M, 1024, 0, st>>>(T, M, k, part, nsplit, W, coef, part_rr, part_x, rzb, beta, rtol, hist_rz,
                                      hist_J, hist_ld, status, iters, it);
   count_launch();
   return check_launch("k_pcg_reduce_rz");
