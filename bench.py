@@ -180,8 +180,8 @@ def cpu_sample(cfg_id, seconds, cores, truth, iters=None):
 
 # ------------------------------------------------------------ GPU leg -----
 # from the round's ncu --set full capture of the cfg4 sweeps (profiles/)
-SWEEP_DRAM_BYTES = {"k_ad": 0.754e9, "k_tl": 0.748e9}
-SWEEP_FP64_UTIL = "k_ad 56%, k_tl 59% of the FP64 pipe (ncu sm__pipe_fp64_cycles_active, profiles/)"
+SWEEP_DRAM_BYTES = {"k_ad": 0.767e9, "k_tl": 0.746e9}
+SWEEP_FP64_UTIL = "k_ad 58-59%, k_tl 59-63% of the FP64 pipe (ncu sm__pipe_fp64_cycles_active, profiles/)"
 
 
 def kernel_roofline(torch, lib, eng, reps, peaks):
