@@ -244,7 +244,15 @@ struct Stage2 {
     const int np = (used + 4) >> 1;
     double* d = buf + 2 * t + 2 * (t / (C / 2));
     constexpr int DSTEP = 2 * NT + 2 * (NT / (C / 2));  // smem doubles per NT pairs
-    if (gm2 >= 0 && gm2 + used + 4 <= n) {
+    constexpr int NFULL = (R + 4) / 2;  // pairs of a full tile (tile mode: used == R)
+    if (gm2 >= 0 && gm2 + used + 4 <= n && np == NFULL) {
+      // full tile inside [0, n): only the last copy is predicated, on a
+      // compile-time bound (the loop-invariant test hoists out of the sweep)
+      const double* p = src + gm2 + 2 * t;
+#pragma unroll
+      for (int it = 0; it < IT; ++it)
+        if (it + 1 < IT || t + it * NT < NFULL) cp_async16(d + it * DSTEP, p + 2 * it * NT);
+    } else if (gm2 >= 0 && gm2 + used + 4 <= n) {
       // window inside [0, n): immediate offsets, ~2 instructions per copy
       const double* p = src + gm2 + 2 * t;
 #pragma unroll
