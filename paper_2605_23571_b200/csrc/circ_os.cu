@@ -189,39 +189,18 @@ __device__ __forceinline__ void dit(double2* Z, const Tw<LOGM, NT>& W) {
 
 }  // namespace os
 
-// grid (blocks of V outputs, column pairs); L = left reach of u (taps k <
-// K act on in[i + tap_w - k]: reach K - 1 - tap_w to the left, tap_w right)
-template <int LOGM, int NT, int MINB = 1>
-__global__ void __launch_bounds__(NT, MINB) k_circ_os(int n, int L, int V, int ncols, const double2* __restrict__ T,
-                                                const double2* __restrict__ H, const double* __restrict__ in,
-                                                double* __restrict__ out, double ident,
-                                                const double* __restrict__ zadd, double* __restrict__ dotp,
-                                                int dtiles) {
+// transform + epilogue of one item (block blk of the column pair (ca, ca+1))
+// whose input window already sits in Z
+template <int LOGM, int NT>
+__device__ __forceinline__ void os_item(double2* Z, double (*red)[NT / 32], const os::Tw<LOGM, NT>& W,
+                                        const double2* __restrict__ H, int n, int L, int V, int ncols, int blk,
+                                        int ca, double* __restrict__ out, double ident,
+                                        const double* __restrict__ zadd, double* __restrict__ dotp, int dtiles) {
   using namespace os;
   constexpr int M = 1 << LOGM;
-  __shared__ __align__(16) double2 Z[M + M / 8];
-  __shared__ double red[2][NT / 32];
-  const int t = threadIdx.x, blk = blockIdx.x;
-  const int ca = 2 * blockIdx.y, cb = ca + 1;
+  const int t = threadIdx.x, cb = ca + 1;
   const bool hb = cb < ncols;
   const int i0 = blk * V;
-  const double* A = in + (size_t)ca * n;
-  const double* B = in + (size_t)(hb ? cb : ca) * n;
-  // window [i0 - L, i0 - L + M) of the ring: n > M (os_logm_for), so one
-  // conditional wrap per index; every load is issued before the first store
-  double ra[M / NT], rb[M / NT];
-#pragma unroll
-  for (int k = 0; k < M / NT; ++k) {
-    int g = i0 - L + t + k * NT;
-    g = g < 0 ? g + n : (g >= n ? g - n : g);
-    ra[k] = __ldg(A + g);
-    rb[k] = hb ? __ldg(B + g) : 0.0;
-  }
-  Tw<LOGM, NT> W;
-  W.load(T);
-#pragma unroll
-  for (int k = 0; k < M / NT; ++k) Z[pz(t + k * NT)] = make_double2(ra[k], rb[k]);
-  __syncthreads();
   dif<LOGM, NT>(Z, W);
 #pragma unroll
   for (int j = t; j < M; j += NT) Z[pz(j)] = cmul(Z[pz(j)], __ldg(H + j));
@@ -270,7 +249,44 @@ __global__ void __launch_bounds__(NT, MINB) k_circ_os(int n, int L, int V, int n
         if (hb) dotp[(size_t)cb * dtiles + q] = 0.0;
       }
     }
+    __syncthreads();  // red is reused by the next item
   }
+}
+
+// grid (blocks of V outputs, column pairs); L = left reach of u (taps k <
+// K act on in[i + tap_w - k]: reach K - 1 - tap_w to the left, tap_w right)
+template <int LOGM, int NT, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) k_circ_os(int n, int L, int V, int ncols, const double2* __restrict__ T,
+                                                const double2* __restrict__ H, const double* __restrict__ in,
+                                                double* __restrict__ out, double ident,
+                                                const double* __restrict__ zadd, double* __restrict__ dotp,
+                                                int dtiles) {
+  using namespace os;
+  constexpr int M = 1 << LOGM;
+  __shared__ __align__(16) double2 Z[M + M / 8];
+  __shared__ double red[2][NT / 32];
+  const int t = threadIdx.x, blk = blockIdx.x;
+  const int ca = 2 * blockIdx.y, cb = ca + 1;
+  const bool hb = cb < ncols;
+  const int i0 = blk * V;
+  const double* A = in + (size_t)ca * n;
+  const double* B = in + (size_t)(hb ? cb : ca) * n;
+  // window [i0 - L, i0 - L + M) of the ring: n > M (os_logm_for), so one
+  // conditional wrap per index; every load is issued before the first store
+  double ra[M / NT], rb[M / NT];
+#pragma unroll
+  for (int k = 0; k < M / NT; ++k) {
+    int g = i0 - L + t + k * NT;
+    g = g < 0 ? g + n : (g >= n ? g - n : g);
+    ra[k] = __ldg(A + g);
+    rb[k] = hb ? __ldg(B + g) : 0.0;
+  }
+  Tw<LOGM, NT> W;
+  W.load(T);
+#pragma unroll
+  for (int k = 0; k < M / NT; ++k) Z[pz(t + k * NT)] = make_double2(ra[k], rb[k]);
+  __syncthreads();
+  os_item<LOGM, NT>(Z, red, W, H, n, L, V, ncols, blk, ca, out, ident, zadd, dotp, dtiles);
 }
 
 // U_B by overlap-save when the problem carries the block spectrum
