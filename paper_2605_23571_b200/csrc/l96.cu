@@ -155,9 +155,11 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
     return;
 #endif
     if (tp < 0) return;
+    double* ot = ob + (size_t)tp * G;  // one base per level, 32-bit grid offsets
+    asm("" : "+l"(ot));  // opaque: keeps ptxas from re-expanding a 64-bit index per element
 #pragma unroll
     for (int j = 0; j < C; ++j)
-      if (gw[j] >= 0) ob[(size_t)tp * G + gw[j]] = v[j + 2];
+      if (gw[j] >= 0) ot[gw[j]] = v[j + 2];
   };
   auto capture = [&](int level) {
     const int tp = __ldg(P.tpos + level);
@@ -194,10 +196,16 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
       else cp_commit();
     }
   }
+  // running pointers / buffer indices (no per-step 64-bit index math or
+  // modulo; the asm keeps ptxas from re-deriving them from s)
+  const double* nsrc = tr + (size_t)(s0 + DEPTH) * n;
+  const int32_t* tpp = P.tpos + s0 + 1;
+  int bcur = s0 % NB, bnext = (s0 + DEPTH) % NB;
 #pragma unroll 1
   for (int s = s0; s < s1; ++s) {
     const double* Xs = tr + (size_t)s * sstride;
-    const int tp_next = __ldg(P.tpos + s + 1);  // consumed at the end of the step
+    asm("" : "+l"(nsrc), "+l"(tpp));
+    const int tp_next = __ldg(tpp);  // consumed at the end of the step
     double X[C + 4];
     if (!STREAM) cp_wait_group<DEPTH - 1>();
     if constexpr (WT) __syncwarp();  // staged X_s visible, X_{s-1}'s buffer free
@@ -205,10 +213,14 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
     if (STREAM) {
       R.load_halo(Xs, X);
     } else {
-      if (s + DEPTH < s1) SS::stage(sbuf(s + DEPTH), Xs + (size_t)DEPTH * n, gst, n, used);
+      if (s + DEPTH < s1) SS::stage(XB0 + (size_t)bnext * SS::PLEN, nsrc, gst, n, used);
       else if (DEPTH > 1) cp_commit();
-      SS::win(sbuf(s), R.t, X);
+      SS::win(XB0 + (size_t)bcur * SS::PLEN, R.t, X);
     }
+    nsrc += n;
+    ++tpp;
+    bcur = bcur + 1 == NB ? 0 : bcur + 1;
+    bnext = bnext + 1 == NB ? 0 : bnext + 1;
     double acc[C], a[C], kk[C], dd[C];
     double x2[C + 4], u2[C + 4];
 #pragma unroll
@@ -347,6 +359,7 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
 #endif
     if (tp < 0) return;
     const double* f = fc + (size_t)tp * G;
+    asm("" : "+l"(f));  // opaque base: 32-bit grid offsets per element (see k_tl capture)
     double* d = FS + (size_t)sbuf * C * NT + threadIdx.x;
 #pragma unroll
     for (int j = 0; j < C; ++j)
@@ -404,9 +417,12 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
     if constexpr (WT) __syncwarp(); else __syncthreads();
   }
 #pragma unroll 1
+  const double* psrc = tr + (size_t)(s1 - 2) * n;  // X_{s-1}: running pointer (see k_tl)
+  const int32_t* tpp = P.tpos + s1 - 2;
   for (int s = s1 - 1; s >= s0; --s) {
     const double* Xs = tr + (size_t)s * sstride;
-    const int tp_next = (PAIR && s > s0) ? __ldg(P.tpos + s - 1) : -1;
+    asm("" : "+l"(psrc), "+l"(tpp));
+    const int tp_next = (PAIR && s > s0) ? __ldg(tpp) : -1;
     double X[C + 4], x2[C + 4], x3[C + 4], x4[C + 4];
     if (STREAM) R.load_halo(Xs, X);
     else SS::win(sbuf(s), R.t, X);  // staged, published by the last barrier
@@ -429,7 +445,7 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
         // X_{s-1} goes to the buffer X_{s+1} used: every thread read it last step
         if (s > s0) {
           if (PAIR) fetch_force(tp_next, (s - 1) & 1);  // same commit group as X_{s-1}
-          SS::stage(sbuf(s - 1), Xs - n, gst, n, used);
+          SS::stage(sbuf(s - 1), STREAM ? Xs - n : psrc, gst, n, used);
         }
       } else {
         // X_{s-2} goes to the buffer X_{s+1} used (every thread is past this
@@ -494,6 +510,8 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
     } else {
       add_force(s, g);
     }
+    psrc -= n;
+    --tpp;
   }
   if (R.t < R.nact) {
     double* go = gout + (size_t)col * n;

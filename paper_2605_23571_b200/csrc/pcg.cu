@@ -246,9 +246,8 @@ int launch_pcg_alpha(int n, int M, const double* p, const double* hp, double* x,
 }
 
 // k_pcg_rz with the split-K reduction of W = S^T r folded in: one CTA per
-// column reduces its k entries (2 lanes per entry, fixed order) from the
-// GEMM's partials, writes W for the p-update GEMM, and runs the rz step.
-// 1024 threads: entry i = t % 128 of a 128-entry slab (a warp reads 32
+// column reduces its k entries from the GEMM's partials, writes W for the
+// p-update GEMM, and runs the rz step.  1024 threads: entry i = t % 128 of a 128-entry slab (a warp reads 32
 // consecutive entries of one split row: coalesced), split group q = t / 128
 // sums splits q, q + 8, ... in order; the 8 group sums are then combined in
 // a fixed tree (deterministic).  The split-K GEMM for the 100-member groups
