@@ -175,6 +175,7 @@ def cpu_sample(cfg_id, seconds, cores, truth, iters=None):
         wall = time.perf_counter() - t0
     busy = max(r[0] for r in res)
     applies = sum(r[1] for r in res)
+    cpu_sample.per_core = sum(r[1] / r[0] for r in res) / len(res)  # one process = one core
     return applies / busy, busy, iters, wall
 
 
@@ -410,9 +411,11 @@ def run_ours(args):
         truth = dens_truth(dens)
         v, busy, iters, wall = cpu_sample(args.config, args.cpu_seconds, cores, truth)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+               "value_1core": cpu_sample.per_core,
                "sample": f"{cores} members x {iters} LMP-PCG iterations (J traced) of "
                          f"{cfg.name}, one member per process, oracle port of edasketch "
-                         f"(krylov.pcg/assim.MemberProblem); busy {busy:.1f} s"}
+                         f"(krylov.pcg/assim.MemberProblem); busy {busy:.1f} s; value_1core = "
+                         f"the mean single-process rate (SURVEY 8d '1 core')"}
     if rank == 0:
         tr0 = res.traces[0]
         line = {
