@@ -371,6 +371,9 @@ def run_ours(args):
             x_ready.record(main)
             with torch.cuda.stream(cs):
                 cs.wait_event(x_ready)
+                # r.x was allocated on the main stream and r dies with this
+                # step: keep its block out of the allocator until the copy ran
+                r.x.record_stream(cs)
                 h_x.copy_(r.x, non_blocking=True)
             return r
 

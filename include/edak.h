@@ -47,8 +47,7 @@ typedef struct edak_problem {
   const double* stages;
   int64_t traj_stride;   /* doubles between consecutive trajectories        */
   int32_t stage_mode;    /* 0 = recompute stages from states, 1 = stream all
-                          * four stored stages, 2 = hybrid: stream x1..x3
-                          * and recompute x4 (stages buffer required)       */
+                          * four stored stages                              */
   int32_t pad0;
   /* observation network (ObsNetwork, obs.py:23-41) as position maps */
   const int32_t* gpos;   /* [n]: position of grid point i in net.grid, or -1 */
@@ -61,14 +60,6 @@ typedef struct edak_problem {
   const double* taps;
   int32_t ntaps;
   int32_t tap_w;
-  /* optional spectral form of the same factor (covariance.py:41-45: U_B v =
-   * irfft(symbol * rfft(v))): sym = the n/2+1 real symbol entries, fft_tw =
-   * exp(-2 pi i k / n) for k < n/2 as interleaved (re, im) doubles.  When
-   * both are set, n is a power of two in [1024, 16384] and EDAK_CIRC_FFT is
-   * set, U_B runs as a shared-memory FFT (one CTA, or a 2-CTA cluster, per
-   * column) instead of the tap convolution. */
-  const double* sym;
-  const double* fft_tw;
   /* optional overlap-save form of the same factor (circ_os.cu): with
    * M = 2^os_logm (10 or 11) and K = ntaps <= M/2 + 1, os_spec holds the M
    * complex values fft(h)/M of the block kernel h[m mod M] = taps[m + tap_w]

@@ -25,7 +25,6 @@ class Problem(C.Structure):
         ("stage_mode", i32), ("pad0", i32),
         ("gpos", vp), ("tpos", vp), ("G", i32), ("T", i32), ("sigma2", f64),
         ("taps", vp), ("ntaps", i32), ("tap_w", i32),
-        ("sym", vp), ("fft_tw", vp),
         ("os_spec", vp), ("os_tw", vp), ("os_logm", i32), ("pad1", i32),
     ]
 

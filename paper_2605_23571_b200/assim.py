@@ -23,8 +23,8 @@ from . import _dev, _lib
 from .covariance import device_factor
 from .obs import DeviceNetwork
 
-STAGE_MODES = ("auto", "recompute", "stream", "hybrid")
-_MODE_CODE = {"recompute": 0, "stream": 1, "hybrid": 2}
+STAGE_MODES = ("auto", "recompute", "stream")
+_MODE_CODE = {"recompute": 0, "stream": 1}
 
 
 def _prob_struct(n, n_steps, dt, forcing, states, stages, traj_stride, stage_mode,
@@ -39,7 +39,6 @@ def _prob_struct(n, n_steps, dt, forcing, states, stages, traj_stride, stage_mod
     P.G, P.T = dnet.G, dnet.T
     P.sigma2 = float(sigma2)
     P.taps, P.ntaps, P.tap_w = dfac.taps.data_ptr(), dfac.ntaps, dfac.tap_w
-    P.sym, P.fft_tw = _lib.ptr(dfac.sym), _lib.ptr(dfac.fft_tw)
     P.os_spec, P.os_tw, P.os_logm = _lib.ptr(dfac.os_spec), _lib.ptr(dfac.os_tw), dfac.os_logm
     return P
 
@@ -87,11 +86,11 @@ class Linearization:
             else:
                 stage_mode = ("recompute" if stages_recomputable(states, stages, dt, forcing)
                               else "stream")
-        if stage_mode in ("stream", "hybrid") and stages is None:
+        if stage_mode == "stream" and stages is None:
             raise ValueError(f"stage_mode={stage_mode!r} needs the stored stages")
         self.stage_mode = stage_mode
         self.states = states
-        self.stages = stages if stage_mode in ("stream", "hybrid") else None
+        self.stages = stages if stage_mode == "stream" else None
         self.dt, self.forcing = float(dt), float(forcing)
         self.net, self.ub, self.rn = net, ub, rn
         self.dnet = DeviceNetwork(net, self.n, self.n_steps)

@@ -109,21 +109,6 @@ def factor_taps(ub):
     return np.ascontiguousarray(taps), w
 
 
-def fft_tables(n):
-    """(symbol-length check aside) the twiddle table exp(-2 pi i k / n),
-    k < n/2, as interleaved (re, im) float64 -- for the spectral U_B kernel
-    (circ_fft.cu), used when n is a power of two in [1024, 16384]."""
-    k = np.arange(n // 2, dtype=float)
-    ang = np.pi * (2.0 * k / n)  # 2k/n exact for power-of-two n
-    tw = np.empty(n, dtype=float)
-    tw[0::2] = np.cos(ang)
-    tw[1::2] = -np.sin(ang)
-    return tw
-
-
-FFT_MIN_N, FFT_MAX_N = 1024, 16384
-
-
 def os_tables(taps, w, logm):
     """Overlap-save tables for circ_os.cu: the block kernel
     h[m mod M] = taps[m + w] (m = k - w, k < K), its spectrum fft(h) / M in
@@ -158,9 +143,9 @@ def os_logm_for(n, ntaps):
 
 
 class DeviceFactor:
-    """Device-resident taps (and, for power-of-two rings in [1024, 16384],
-    the rfft symbol + twiddles) of a circulant factor, plus a minimal
-    edak_problem that the U_B kernels read."""
+    """Device-resident taps (and, on long rings, the overlap-save block
+    spectrum + twiddles) of a circulant factor, plus a minimal edak_problem
+    that the U_B kernels read."""
 
     def __init__(self, ub):
         self.n = int(ub.n)
@@ -169,10 +154,6 @@ class DeviceFactor:
         self.tap_w = w
         self.ntaps = taps.size
         n = self.n
-        self.sym = self.fft_tw = None
-        if FFT_MIN_N <= n <= FFT_MAX_N and n & (n - 1) == 0:
-            self.sym = _dev.f64(np.asarray(ub.symbol, dtype=float))
-            self.fft_tw = _dev.f64(fft_tables(n))
         self.os_spec = self.os_tw = None
         self.os_logm = os_logm_for(n, self.ntaps)
         if self.os_logm:
@@ -183,8 +164,6 @@ class DeviceFactor:
         self._prob.taps = self.taps.data_ptr()
         self._prob.ntaps = self.ntaps
         self._prob.tap_w = w
-        self._prob.sym = _lib.ptr(self.sym)
-        self._prob.fft_tw = _lib.ptr(self.fft_tw)
         self._prob.os_spec, self._prob.os_tw = _lib.ptr(self.os_spec), _lib.ptr(self.os_tw)
         self._prob.os_logm = self.os_logm
 

@@ -106,19 +106,11 @@ __global__ void __launch_bounds__(NT) k_circ(int n, const double* __restrict__ t
 // tiles of the tap convolution and the >= 512-output blocks of circ_os.cu
 int circ_tiles(int n) { return (n + 511) / 512; }
 
-bool circ_fft_ok(const edak_problem* P);
-int launch_circ_fft(const edak_problem* P, const double* in, double* out, int ncols, double ident,
-                    const double* zadd, cudaStream_t st, double* dotp, int dtiles);
-
 int launch_circ_os(const edak_problem* P, const double* in, double* out, int ncols, double ident,
                    const double* zadd, cudaStream_t st, double* dotp, int dtiles);
 
 int launch_circ(const edak_problem* P, const double* in, double* out, int ncols, double ident,
                 const double* zadd, cudaStream_t st, double* dotp) {
-  // spectral form (circ_fft.cu): exact to 1e-15 but measured no faster than
-  // the tap convolution at cfg4 (70.6 vs 68.9 us per 200 columns), so opt-in
-  if (circ_fft_ok(P) && getenv("EDAK_CIRC_FFT"))
-    return launch_circ_fft(P, in, out, ncols, ident, zadd, st, dotp, circ_tiles(P->n));
   // overlap-save block FFTs (circ_os.cu) when the factor carries their
   // tables; EDAK_CIRC_OS=0 forces the tap convolution
   const char* eo = getenv("EDAK_CIRC_OS");

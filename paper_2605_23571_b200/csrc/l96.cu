@@ -416,9 +416,9 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
     }
     if constexpr (WT) __syncwarp(); else __syncthreads();
   }
-#pragma unroll 1
   const double* psrc = tr + (size_t)(s1 - 2) * n;  // X_{s-1}: running pointer (see k_tl)
   const int32_t* tpp = P.tpos + s1 - 2;
+#pragma unroll 1
   for (int s = s1 - 1; s >= s0; --s) {
     const double* Xs = tr + (size_t)s * sstride;
     asm("" : "+l"(psrc), "+l"(tpp));
@@ -647,15 +647,6 @@ static void widen_pairs(const edak_problem* P, bool stream, int& C, int& NT, Swe
   geo.nact = NT;
 }
 
-int sweep2_mode(const edak_problem* P, int K);
-int sweep3_mode(const edak_problem* P, int K);
-int launch_tl3(const edak_problem*, const double*, double*, int, const int32_t*, int, int, double*, cudaStream_t);
-int launch_ad3(const edak_problem*, const double*, double*, int, const int32_t*, int, int, const double*,
-               cudaStream_t);
-int launch_tl2(const edak_problem*, const double*, double*, int, const int32_t*, int, int, double*, cudaStream_t);
-int launch_ad2(const edak_problem*, const double*, double*, int, const int32_t*, int, int, const double*,
-               cudaStream_t);
-
 // warp-tile sweeps (EDAK_SWEEP_WARP): one warp per tile of 16 x 32 = 512
 // ring elements, halos by shuffles, no CTA barrier.  Window chunks of K steps
 // (EDAK_WARP_CHUNK) keep the redundant halo (12K + 8) a small share of the
@@ -683,37 +674,6 @@ int launch_tl(const edak_problem* P, const double* v0, double* obs, int ncols, c
   int C, NT, nt;
   SweepGeom geo;
   const int N = P->n_steps;
-  if (const int m3 = sweep3_mode(P, SWEEP_CHUNK)) {  // hybrid storage: stream x1..x3
-    const int nch = (m3 == 1 || !work2 || N <= SWEEP_CHUNK) ? 1 : (N + SWEEP_CHUNK - 1) / SWEEP_CHUNK;
-    if (!(m3 == 2 && nch == 1 && N > SWEEP_CHUNK && sweep3_mode(P, N) == 0)) {
-      const size_t blk = (size_t)ncols * P->n;
-      for (int c = 0; c < nch; ++c) {
-        const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch);
-        const double* vin = c == 0 ? v0 : work2 + (size_t)((c - 1) & 1) * blk;
-        double* vout = c + 1 < nch ? work2 + (size_t)(c & 1) * blk : nullptr;
-        int rc = launch_tl3(P, vin, obs, ncols, col_traj, s0, s1, vout, st);
-        if (rc) return rc;
-      }
-      return EDAK_OK;
-    }
-  }
-  if (const int m2 = sweep2_mode(P, SWEEP_CHUNK)) {  // shared-memory-staged kernels
-    const int nch = (m2 == 1 || !work2 || N <= SWEEP_CHUNK || getenv("EDAK_SWEEP_NOCHUNK"))
-                        ? 1 : (N + SWEEP_CHUNK - 1) / SWEEP_CHUNK;
-    if (m2 == 2 && nch == 1 && N > SWEEP_CHUNK && sweep2_mode(P, N) == 0) goto v1;
-    {
-      const size_t blk = (size_t)ncols * P->n;
-      for (int c = 0; c < nch; ++c) {
-        const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch);
-        const double* vin = c == 0 ? v0 : work2 + (size_t)((c - 1) & 1) * blk;
-        double* vout = c + 1 < nch ? work2 + (size_t)(c & 1) * blk : nullptr;
-        int rc = launch_tl2(P, vin, obs, ncols, col_traj, s0, s1, vout, st);
-        if (rc) return rc;
-      }
-      return EDAK_OK;
-    }
-  }
-v1:
   if (warp_mode(P, work2)) {
     const int K = warp_chunk();
     const int nch = (N + K - 1) / K;
@@ -793,37 +753,6 @@ int launch_ad(const edak_problem* P, const double* forcing, double* g, int ncols
   int C, NT, nt;
   SweepGeom geo;
   const int N = P->n_steps;
-  if (const int m3 = sweep3_mode(P, SWEEP_CHUNK)) {  // hybrid storage: stream x1..x3
-    const int nch = (m3 == 1 || !work2 || N <= SWEEP_CHUNK) ? 1 : (N + SWEEP_CHUNK - 1) / SWEEP_CHUNK;
-    if (!(m3 == 2 && nch == 1 && N > SWEEP_CHUNK && sweep3_mode(P, N) == 0)) {
-      const size_t blk = (size_t)ncols * P->n;
-      for (int c = nch - 1, k = 0; c >= 0; --c, ++k) {
-        const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch);
-        const double* gin = k == 0 ? nullptr : work2 + (size_t)((k - 1) & 1) * blk;
-        double* gout = c == 0 ? g : work2 + (size_t)(k & 1) * blk;
-        int rc = launch_ad3(P, forcing, gout, ncols, col_traj, s0, s1, gin, st);
-        if (rc) return rc;
-      }
-      return EDAK_OK;
-    }
-  }
-  if (const int m2 = sweep2_mode(P, SWEEP_CHUNK)) {
-    const int nch = (m2 == 1 || !work2 || N <= SWEEP_CHUNK || getenv("EDAK_SWEEP_NOCHUNK"))
-                        ? 1 : (N + SWEEP_CHUNK - 1) / SWEEP_CHUNK;
-    if (m2 == 2 && nch == 1 && N > SWEEP_CHUNK && sweep2_mode(P, N) == 0) goto v1;
-    {
-      const size_t blk = (size_t)ncols * P->n;
-      for (int c = nch - 1, k = 0; c >= 0; --c, ++k) {
-        const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch);
-        const double* gin = k == 0 ? nullptr : work2 + (size_t)((k - 1) & 1) * blk;
-        double* gout = c == 0 ? g : work2 + (size_t)(k & 1) * blk;
-        int rc = launch_ad2(P, forcing, gout, ncols, col_traj, s0, s1, gin, st);
-        if (rc) return rc;
-      }
-      return EDAK_OK;
-    }
-  }
-v1:
   if (warp_mode(P, work2)) {
     const int K = warp_chunk();
     const int nch = (N + K - 1) / K;

@@ -89,12 +89,17 @@ class SpectralLmp:
         return (self._S, self._c_full) if self.fused else None
 
     def work_cols(self, ncols, device):
-        key = (ncols, str(device))
-        if getattr(self, "_work_key", None) != key:
-            self._work = torch.empty(int(_lib.lib().edak_lmp_work_doubles(self.n, self.k, ncols)),
-                                     dtype=torch.float64, device=device)
-            self._work_key = key
-        return self._work
+        """Split-K workspace of edak_lmp_apply, one per (ncols, device, stream):
+        member groups of the batched PCG apply P on their own streams at the
+        same time, so a workspace shared across streams would race."""
+        key = (ncols, str(device), torch.cuda.current_stream(device).cuda_stream)
+        cache = self.__dict__.setdefault("_work", {})
+        w = cache.get(key)
+        if w is None:
+            w = torch.empty(int(_lib.lib().edak_lmp_work_doubles(self.n, self.k, ncols)),
+                            dtype=torch.float64, device=device)
+            cache[key] = w
+        return w
 
     def _project_cols(self, coef, R, out=None):
         n, ncols = R.shape[1], R.shape[0]

@@ -87,7 +87,6 @@ class DeviceEnsemble:
     innovations: torch.Tensor  # (M+1, p)
     traj_of: np.ndarray        # row -> trajectory index
     lin: Linearization = None
-    stages: torch.Tensor = None  # (trajectories, N, 4, n) when stage_mode == "hybrid"
     x0: torch.Tensor = None    # (M+1, n) initial states: x_b and the member x_j
     y: torch.Tensor = None     # (M+1, p) (perturbed) observations y, y_j
     grid_t: torch.Tensor = None
@@ -111,19 +110,14 @@ class DeviceEnsemble:
         n, N = cfg.n, cfg.n_steps
         rows = self.x0.shape[0]
         full = self.states if self.states.shape[0] == rows else self._scratch
-        stg = self.stages if (self.stages is not None and self.stages.shape[0] == rows) else None
         _lib.call("edak_integrate", n, N, float(cfg.dt), float(cfg.forcing), self.x0.data_ptr(), rows,
-                  full.data_ptr(), (N + 1) * n, _lib.ptr(stg), 4 * N * n, _lib.stream())
+                  full.data_ptr(), (N + 1) * n, None, 4 * N * n, _lib.stream())
         _lib.call("edak_observe", full.data_ptr(), (N + 1) * n, n, self.grid_t.data_ptr(),
                   self.net.grid.size, self.times_t.data_ptr(), self.net.times.size, rows,
                   self._gx.data_ptr(), _lib.stream())
         torch.sub(self.y, self._gx, out=self.innovations)
         if full is not self.states:
             self.states.copy_(full[: self.states.shape[0]])
-        if self.stages is not None and stg is None:  # shared control trajectory
-            _lib.call("edak_integrate", n, N, float(cfg.dt), float(cfg.forcing), self.x0.data_ptr(),
-                      self.stages.shape[0], self._scratch2.data_ptr(), (N + 1) * n,
-                      self.stages.data_ptr(), 4 * N * n, _lib.stream())
 
 
 def _normal_block(seed, path_fn, rows, size):
@@ -133,15 +127,14 @@ def _normal_block(seed, path_fn, rows, size):
     return out
 
 
-def build_ensemble(cfg, members=None, member_offset=0, truth=None, stage_mode="recompute"):
+def build_ensemble(cfg, members=None, member_offset=0, truth=None):
     """Device twin experiment for a BASELINE config.
 
     members / member_offset select member ids member_offset+1 ..
     member_offset+members (multi-GPU sharding keeps the reference stream ids).
     Returns a DeviceEnsemble whose Linearization holds the control
-    trajectory and each member's own (or, shared mode, only the control).
-    stage_mode "hybrid" also keeps the stored RK4 stages (the sweeps then
-    stream x1..x3 and recompute x4); "recompute" keeps the states only."""
+    trajectory and each member's own (or, shared mode, only the control);
+    only the states are kept (the sweeps recompute the RK4 stages)."""
     members = cfg.members if members is None else members
     dev = _dev.device()
     n, N = cfg.n, cfg.n_steps
@@ -165,8 +158,7 @@ def build_ensemble(cfg, members=None, member_offset=0, truth=None, stage_mode="r
     pert = df.apply_cols(_dev.f64(eta))
     x_bg = x_true[None] + pert[:1]
     x0 = torch.cat([x_bg, x_bg + pert[1:]], 0).contiguous()
-    hybrid = stage_mode == "hybrid"
-    states, stages = integrate_device(x0, cfg.dt, N, cfg.forcing, want_stages=hybrid)
+    states, _ = integrate_device(x0, cfg.dt, N, cfg.forcing)
     # innovations d_j = y_j - G(x_j) against each member's own run (eda.py:103-105)
     gx = torch.empty((members + 1, p), dtype=torch.float64, device=dev)
     _lib.call("edak_observe", states.data_ptr(), (N + 1) * n, n, grid_t.data_ptr(),
@@ -177,20 +169,15 @@ def build_ensemble(cfg, members=None, member_offset=0, truth=None, stage_mode="r
     innov = (yj - gx).contiguous()
     if cfg.shared_linearization:
         states = states[:1].contiguous()
-        stages = stages[:1].contiguous() if hybrid else None
         traj_of = np.zeros(members + 1, dtype=np.int64)
     else:
         traj_of = np.arange(members + 1)
     ens = DeviceEnsemble(cfg, net, ub, rn, states, innov, traj_of)
-    ens.stages = stages
-    ens.lin = Linearization(states, cfg.dt, cfg.forcing, net, ub, rn, stages,
-                            "hybrid" if hybrid else "recompute")
+    ens.lin = Linearization(states, cfg.dt, cfg.forcing, net, ub, rn)
     ens.x0, ens.y, ens.grid_t, ens.times_t = x0, yj.contiguous(), grid_t, times_t
     ens._gx = gx
     ens._scratch = (None if not cfg.shared_linearization else
                     torch.empty((members + 1, N + 1, n), dtype=torch.float64, device=dev))
-    ens._scratch2 = (torch.empty((1, N + 1, n), dtype=torch.float64, device=dev)
-                     if (cfg.shared_linearization and hybrid) else None)
     return ens
 
 

@@ -193,25 +193,6 @@ def test_ensemble_per_member_trajectories(gpu):
         assert rel(AZ[j], o.a_apply(Z[j].cpu().numpy())) < 1e-12
 
 
-def test_hybrid_equals_recompute(gpu):
-    """stage_mode "hybrid" (stream x1..x3, recompute x4; sweep3.cu) gives the
-    same bits as recomputing every stage, in tile mode (n=16384, chunked
-    window) and periodic mode (n=1024)."""
-    from paper_2605_23571_b200.assim import Linearization
-    from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
-    for n, N, L in [(16384, 24, 16.0), (1024, 16, 8.0)]:
-        op = _oracle_problem(n, N, 4, 3, L, 9)
-        ub = CirculantFactor(n, op.ub.symbol)
-        a = Linearization(op.traj.states[None], 0.025, 8.0, op.net, ub, DiagonalNoise(1.0),
-                          op.traj.stages[None], "recompute")
-        b = Linearization(op.traj.states[None], 0.025, 8.0, op.net, ub, DiagonalNoise(1.0),
-                          op.traj.stages[None], "hybrid")
-        z = torch.randn(3, n, dtype=torch.float64, device="cuda")
-        assert torch.equal(a.hessian_cols(z), b.hessian_cols(z))
-        d = torch.randn(3, op.net.p, dtype=torch.float64, device="cuda")
-        assert torch.equal(a.rhs_cols(d), b.rhs_cols(d))
-
-
 def test_pair_staging_equals_generic(gpu, monkeypatch):
     """16-byte pair staging (even n, sweep.cuh Stage2) and the generic 8-byte
     staging give the same bits: tile mode with wrapping edge tiles
@@ -229,14 +210,6 @@ def test_pair_staging_equals_generic(gpu, monkeypatch):
         assert torch.equal(hz, a.hessian_cols(z))
         assert torch.equal(rd, a.rhs_cols(d))
         monkeypatch.delenv("EDAK_NO_PAIR")
-        # warp tiles (shuffled halos, no CTA barrier) at several window chunks
-        monkeypatch.setenv("EDAK_SWEEP_WARP", "1")
-        for k in ("3", "6", "8"):
-            monkeypatch.setenv("EDAK_WARP_CHUNK", k)
-            assert torch.equal(hz, a.hessian_cols(z)), (n, "warp", k)
-            assert torch.equal(rd, a.rhs_cols(d)), (n, "warp", k)
-        monkeypatch.delenv("EDAK_WARP_CHUNK")
-        monkeypatch.delenv("EDAK_SWEEP_WARP")
         # U_B register blocking 8 vs 16 outputs per thread: same tap order, same bits
         for r in ("8", "16"):
             monkeypatch.setenv("EDAK_CIRC_R", r)
@@ -341,33 +314,6 @@ def test_randomized_window_operators(gpu, seed):
     assert rel(hz, z[:, 0] + ref[:, 0]) < 1e-12
     assert rel(prob.rhs(), op.rhs()) < 1e-12
     assert prob.quadratic_cost(z[:, 1]) == pytest.approx(op.quadratic_cost(z[:, 1]), rel=1e-12)
-
-
-def test_spectral_factor_equals_taps(gpu, monkeypatch):
-    """The opt-in spectral U_B (circ_fft.cu: one-CTA n = 1024, 2-CTA cluster
-    n = 16384) against the tap convolution and numpy's irfft(symbol rfft),
-    including the I + A epilogue and its p.Hp tile partials."""
-    from paper_2605_23571_b200.assim import Linearization
-    from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
-    for n, N, L in [(1024, 8, 8.0), (16384, 6, 16.0)]:
-        op = _oracle_problem(n, N, 4, 2, L, 21)
-        ub = CirculantFactor(n, op.ub.symbol)
-        lin = Linearization(op.traj.states[None], 0.025, 8.0, op.net, ub, DiagonalNoise(1.0))
-        z = torch.randn(5, n, dtype=torch.float64, device="cuda")
-        direct = lin.dfac.apply_cols(z)
-        monkeypatch.setenv("EDAK_CIRC_FFT", "1")
-        spec = lin.dfac.apply_cols(z)
-        ref = np.fft.irfft(np.fft.rfft(z.cpu().numpy(), axis=1) * op.ub.symbol, n=n, axis=1)
-        assert float((spec - direct).abs().max()) <= 1e-14 * float(direct.abs().max())
-        assert np.abs(spec.cpu().numpy() - ref).max() <= 1e-14 * np.abs(ref).max()
-        tiles = lin.dot_tiles()
-        dp = torch.empty((5, tiles), dtype=torch.float64, device="cuda")
-        hz = lin.hessian_cols(z, None, 1.0, None, None, None, dp)
-        monkeypatch.delenv("EDAK_CIRC_FFT")
-        dp2 = torch.empty_like(dp)
-        hz2 = lin.hessian_cols(z, None, 1.0, None, None, None, dp2)
-        assert float((hz - hz2).abs().max()) <= 1e-13 * float(hz2.abs().max())
-        assert torch.allclose(dp.sum(1), (z * hz).sum(1), rtol=1e-13)
 
 
 def test_overlap_save_factor_equals_taps(gpu, monkeypatch):
