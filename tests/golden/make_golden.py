@@ -89,7 +89,9 @@ def pack_problem(prefix, prob, out):
     out[prefix + "sigma_obs"] = np.array(prob.rn.sigma)
 
 
-def trace_arrays(prefix, tr, out):
+def trace_arrays(prefix, tr, out, x=None):
+    if x is not None:  # the final increment krylov.pcg returns (krylov.py:97)
+        out[prefix + "x"] = np.asarray(x)
     out[prefix + "cost"] = np.array(tr.cost)
     out[prefix + "resnorm"] = np.array(tr.resnorm)
     out[prefix + "iters"] = np.array(tr.iterations)
@@ -141,9 +143,9 @@ def make_problem_cases():
     out["tiny_rhs"] = prob.rhs()
     out["tiny_cost"] = np.array([prob.quadratic_cost(z[:, j]) for j in range(6)])
     out["tiny_dense_a"] = prob.a_apply(np.eye(40))
-    _, tr = pcg(prob.hessian_apply, prob.rhs(), SolverConfig(max_iters=8),
+    x, tr = pcg(prob.hessian_apply, prob.rhs(), SolverConfig(max_iters=8),
                 cost_fn=prob.quadratic_cost)
-    trace_arrays("tiny_pcg_", tr, out)
+    trace_arrays("tiny_pcg_", tr, out, x)
     sk = make_sketch("rhsdiff", setup, 10, substream(0, "sketch"))
     out["tiny_gamma"] = sk.columns
     out["tiny_member_rhs"] = np.column_stack([m.rhs() for m in setup.members])
@@ -152,9 +154,9 @@ def make_problem_cases():
     out["tiny_nys_shift"] = np.array(approx.shift)
     lmp = make_lmp(approx, "halfsum")
     out["tiny_theta"] = np.array(lmp.theta)
-    _, tr = pcg(prob.hessian_apply, prob.rhs(), SolverConfig(max_iters=8),
+    x, tr = pcg(prob.hessian_apply, prob.rhs(), SolverConfig(max_iters=8),
                 precond=lmp, cost_fn=prob.quadratic_cost)
-    trace_arrays("tiny_lmp_", tr, out)
+    trace_arrays("tiny_lmp_", tr, out, x)
 
     # (2) BASELINE cfg1-like: n=40, N=8, every 2nd var every step, shared
     x, control, mems = baseline_like(40, 8, 2, 1, 2.0, 10, True)
@@ -172,9 +174,9 @@ def make_problem_cases():
     out["cfg1_nys_shift"] = np.array(approx.shift)
     lmp = make_lmp(approx, "halfsum")
     for j in (0, 4, 9):
-        _, tr = pcg(mems[j].hessian_apply, mems[j].rhs(), SolverConfig(max_iters=30),
+        x, tr = pcg(mems[j].hessian_apply, mems[j].rhs(), SolverConfig(max_iters=30),
                     precond=lmp, cost_fn=mems[j].quadratic_cost)
-        trace_arrays(f"cfg1_m{j}_", tr, out)
+        trace_arrays(f"cfg1_m{j}_", tr, out, x)
 
     # (3) BASELINE cfg2-like: 50 own trajectories, ell=50 > n (shift path)
     x, control, mems = baseline_like(40, 8, 2, 1, 2.0, 50, False)
@@ -190,9 +192,9 @@ def make_problem_cases():
         m = mems[j]
         pack_problem(f"cfg2_m{j}_", m, out)
         approx = nystrom_evd(control.a_apply, gam, NystromConfig(ell=50, k=20, shift_mode="trace"))
-        _, tr = pcg(m.hessian_apply, m.rhs(), SolverConfig(max_iters=50),
+        x, tr = pcg(m.hessian_apply, m.rhs(), SolverConfig(max_iters=50),
                     precond=make_lmp(approx, "halfsum"), cost_fn=m.quadratic_cost)
-        trace_arrays(f"cfg2_m{j}_", tr, out)
+        trace_arrays(f"cfg2_m{j}_", tr, out, x)
 
     # (4) n=120 mirror (test_nystrom.py:21-24) with a gaussian sketch
     tw = TwinConfig(n=120, obs_grid_count=10, members=0, seed=21)

@@ -20,12 +20,13 @@ JITTER = 2e-16
 PCG_JITTER = 1e-15
 
 
-def pcg_envelope(apply_h, b, cfg, precond=None, cost_fn=None, trials=6, seed=7):
-    """(reference trace, envelope of |dJ|, envelope of |d resnorm|)."""
-    _, ref = oalg.pcg(apply_h, b, cfg, precond=precond, cost_fn=cost_fn)
+def pcg_envelope(apply_h, b, cfg, precond=None, cost_fn=None, trials=6, seed=7, with_x=False):
+    """(reference trace, envelope of |dJ|, envelope of |d resnorm|); with
+    ``with_x`` also (reference x, envelope of ||dx||)."""
+    x_ref, ref = oalg.pcg(apply_h, b, cfg, precond=precond, cost_fn=cost_fn)
     rng = np.random.default_rng(seed)
     n = len(ref.cost)
-    e_j, e_r = np.zeros(n), np.zeros(n)
+    e_j, e_r, e_x = np.zeros(n), np.zeros(n), 0.0
     papply = None if precond is None else (precond if callable(precond) else precond.apply)
     for _ in range(trials):
         def h(v):
@@ -34,11 +35,24 @@ def pcg_envelope(apply_h, b, cfg, precond=None, cost_fn=None, trials=6, seed=7):
         def pc(v):
             w = v if papply is None else papply(v)
             return w * (1 + PCG_JITTER * rng.standard_normal(np.shape(v)))
-        _, tr = oalg.pcg(h, b, cfg, precond=pc, cost_fn=cost_fn)
+        x, tr = oalg.pcg(h, b, cfg, precond=pc, cost_fn=cost_fn)
         m = min(n, len(tr.cost))
         e_j[:m] = np.maximum(e_j[:m], np.abs(np.array(tr.cost[:m]) - ref.cost[:m]))
         e_r[:m] = np.maximum(e_r[:m], np.abs(np.array(tr.resnorm[:m]) - ref.resnorm[:m]))
+        e_x = max(e_x, float(np.linalg.norm(x - x_ref)))
+    if with_x:
+        return ref, e_j, e_r, x_ref, e_x
     return ref, e_j, e_r
+
+
+def assert_increment(x, x_ref, env_x, rtol=1e-10):
+    """Final increment (krylov.py:97): ||x - x_ref|| <= max(rtol ||x_ref||,
+    10 x the CPU-vs-CPU spread of x)."""
+    x, x_ref = np.asarray(x), np.asarray(x_ref)
+    err = float(np.linalg.norm(x - x_ref))
+    tol = max(rtol * float(np.linalg.norm(x_ref)), 10.0 * env_x)
+    assert err <= tol, ("x", err, tol, float(np.linalg.norm(x_ref)))
+    return err / float(np.linalg.norm(x_ref))
 
 
 def assert_trace(ours, ref, env_j, env_r, rtol=1e-10):
@@ -75,26 +89,43 @@ def nystrom_envelope(op, phi, cfg, trials=4):
     return env
 
 
-def lmp_pcg_envelope(op, phi, ncfg, rule, member, cfg, trials=4, seed=321):
-    """CPU-vs-CPU spread of a member's LMP-PCG trace (J, resnorm) when the
-    LMP itself is built from Y = A Phi perturbed at the 1e-16 level -- two
-    legitimate fp64 Nystrom/Cholesky/SVD implementations differ that way
-    (LAPACK-stage results are not bit-pinned)."""
+def lmp_pcg_envelope(op, phi, ncfg, rule, member, cfg, trials=4, seed=321, with_x=False):
+    """CPU-vs-CPU spread of a member's LMP-PCG trace (J, resnorm; with
+    ``with_x`` also the final increment) when the LMP itself is built from
+    Y = A Phi perturbed at the 1e-16 level -- two legitimate fp64
+    Nystrom/Cholesky/SVD implementations differ that way (SURVEY.md §8c:
+    LAPACK-stage results are not bit-pinned)."""
     y = op.a_apply(phi)
     lmp = oalg.make_lmp(oalg.nystrom_evd(lambda v: y, phi, ncfg), rule)
     b = member.rhs()
-    _, ref = oalg.pcg(member.hessian_apply, b, cfg, precond=lmp, cost_fn=member.quadratic_cost)
+    x_ref, ref = oalg.pcg(member.hessian_apply, b, cfg, precond=lmp, cost_fn=member.quadratic_cost)
     rng = np.random.default_rng(seed)
     n = len(ref.cost)
-    e_j, e_r = np.zeros(n), np.zeros(n)
+    e_j, e_r, e_x = np.zeros(n), np.zeros(n), 0.0
     for _ in range(trials):
         yp = y * (1 + JITTER * rng.standard_normal(y.shape))
         lp = oalg.make_lmp(oalg.nystrom_evd(lambda v: yp, phi, ncfg), rule)
-        _, tr = oalg.pcg(member.hessian_apply, b, cfg, precond=lp, cost_fn=member.quadratic_cost)
+        x, tr = oalg.pcg(member.hessian_apply, b, cfg, precond=lp, cost_fn=member.quadratic_cost)
         m = min(n, len(tr.cost))
         e_j[:m] = np.maximum(e_j[:m], np.abs(np.array(tr.cost[:m]) - ref.cost[:m]))
         e_r[:m] = np.maximum(e_r[:m], np.abs(np.array(tr.resnorm[:m]) - ref.resnorm[:m]))
+        e_x = max(e_x, float(np.linalg.norm(x - x_ref)))
+    if with_x:
+        return ref, e_j, e_r, x_ref, e_x
     return ref, e_j, e_r
+
+
+def nystrom_envelope_y(y, phi, cfg, trials=4):
+    """nystrom_envelope for a given Y = A Phi (e.g. the GPU's own Y, so that
+    only the dense Nystrom stage is compared): (reference approximation,
+    per-value CPU-vs-CPU spread)."""
+    base = oalg.nystrom_evd(lambda v: y, phi, cfg)
+    rng = np.random.default_rng(123)
+    env = np.zeros_like(base.values)
+    for _ in range(trials):
+        yp = y * (1 + JITTER * rng.standard_normal(y.shape))
+        env = np.maximum(env, np.abs(oalg.nystrom_evd(lambda v: yp, phi, cfg).values - base.values))
+    return base, env
 
 
 def assert_values(ours, ref, env):
@@ -116,3 +147,27 @@ def teacher_forced_step(apply_h, apply_p, x, r, p, rz):
     z1 = apply_p(r1) if apply_p is not None else r1
     rz1 = r1 @ z1
     return x1, r1, z1 + (rz1 / rz) * p, rz1
+
+
+def oracle_rows(dens, rows):
+    """Oracle MemberProblems for ensemble rows (0 = control) on the device
+    ensemble's own trajectories and innovations (only the needed
+    trajectories are copied to the host: cfg5's full set is 7 GB)."""
+    from oracle import l96 as ol96
+    from oracle.cov import CirculantFactor as OFactor, DiagonalNoise as ONoise
+    from oracle.obs import ObsNetwork as OObs
+    from oracle.problem import MemberProblem as OProblem
+    cfg = dens.cfg
+    net = OObs(dens.net.grid, dens.net.times)
+    ub = OFactor(cfg.n, dens.ub.symbol)
+    out, cache = [], {}
+    for r in rows:
+        t = int(dens.traj_of[r])
+        if t not in cache:
+            st = dens.states[t].cpu().numpy()
+            stg = np.stack([np.stack(ol96.rk4_stages(st[s], cfg.dt, cfg.forcing)[1])
+                            for s in range(cfg.n_steps)])
+            cache[t] = ol96.Trajectory(st, stg, cfg.dt, cfg.forcing)
+        out.append(OProblem(cache[t], net, ub, ONoise(cfg.sigma_obs),
+                            dens.innovations[r].cpu().numpy()))
+    return out

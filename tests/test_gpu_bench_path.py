@@ -1,0 +1,187 @@
+"""Parity of the EXACT code path bench.py times, at the BASELINE configs'
+own sizes, against the CPU oracle on the same device-built inputs.
+
+bench.py's step is ``EdaPass.run()``: batched rhs -> Gamma -> Y = A Gamma ->
+Nystrom -> halfsum LMP -> batched LMP-PCG.  At cfg4 the solve runs as a
+replayed CUDA graph over two member groups on two streams, one group-
+iteration apart, with the single-pass LMP folded into the beta step and J
+traced by the quadratic identity; at cfg5 (no graph: members x n > 2^22) the
+same two staggered groups run eagerly.  Nothing here passes ``snapshots`` or
+otherwise changes that path.
+
+Checked (SURVEY.md §8c protocol; nystrom.py:96-133, lmp.py:62-74,
+krylov.py:49-97):
+  (i)   every Ritz value against the oracle's nystrom_evd on the GPU's own
+        Y = A Gamma (only the dense stage is compared), rel 1e-10 or 10x the
+        CPU-vs-CPU envelope; the LMP action likewise;
+  (ii)  full J traces (rel 1e-10 or 10x envelope) and residual histories (to
+        the divergence onset) for members in BOTH groups, oracle PCG with the
+        LMP built from our eigenpairs;
+  (iii) final increments x (rel 1e-10 or 10x the CPU-vs-CPU envelope);
+  (iv)  J from the identity J(0) - x.(b + r)/2 against the oracle's exact
+        quadratic_cost(x) at iterations 0, 40 and the last;
+  plus graph == eager and replay == replay bit identity.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import algorithms as oalg
+from parity import (JITTER, assert_increment, assert_trace, assert_values, nystrom_envelope_y,
+                    oracle_rows, pcg_envelope)
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(cfg_id, members=None):
+    from paper_2605_23571_b200 import build
+    build.build()
+    from paper_2605_23571_b200.engine import EdaPass
+    from paper_2605_23571_b200.twin import BASELINE_CONFIGS, build_ensemble
+    dens = build_ensemble(BASELINE_CONFIGS[cfg_id], members=members)
+    eng = EdaPass(dens)
+    res = eng.run()
+    torch.cuda.synchronize()
+    return dens, eng, res
+
+
+@pytest.fixture(scope="module")
+def cfg4():
+    dens, eng, res = _run(4)
+    res2 = eng.run()  # a second pass: graph replay with reloaded inputs
+    return dens, eng, res, res2
+
+
+def _y_of(eng, G):
+    return eng.control.a_apply_cols(G).cpu().numpy().T  # (n, ell), numpy layout
+
+
+def _check_nystrom(eng, res, ncfg, trials):
+    phi = res.gamma.cpu().numpy().T
+    y = _y_of(eng, res.gamma)
+    base, env = nystrom_envelope_y(y, phi, ncfg, trials=trials)
+    assert res.approx.values.size == base.values.size == ncfg.k
+    assert_values(res.approx.values, base.values, env)
+    assert res.approx.shift == base.shift
+    # LMP action (sign-invariant), against the spread of oracle LMPs built
+    # from Y jittered at 1e-16
+    rule = "halfsum"
+    ref = oalg.make_lmp(base, rule)
+    v = np.random.default_rng(5).standard_normal((phi.shape[0], 3))
+    pv = ref.apply(v)
+    rng = np.random.default_rng(77)
+    env_p = 0.0
+    for _ in range(trials):
+        yp = y * (1 + JITTER * rng.standard_normal(y.shape))
+        lp = oalg.make_lmp(oalg.nystrom_evd(lambda z: yp, phi, ncfg), rule)
+        env_p = max(env_p, float(np.linalg.norm(lp.apply(v) - pv)))
+    err = float(np.linalg.norm(res.lmp.apply(v) - pv))
+    assert err <= max(1e-10 * np.linalg.norm(pv), 10 * env_p), (err, env_p)
+    assert res.lmp.theta == pytest.approx(ref.theta, rel=1e-10, abs=10 * env[-1])
+
+
+def _check_members(dens, res, members, iters, trials):
+    """(ii) + (iii) + (iv at the last iteration) for the given member ids."""
+    ops = oracle_rows(dens, [m + 1 for m in members])
+    olmp = oalg.SpectralLmp(res.approx.vectors, res.approx.values, res.lmp.theta)
+    X = res.x
+    worst = {}
+    for m, op in zip(members, ops):
+        tr = res.traces[m]
+        ref, ej, er, xr, ex = pcg_envelope(op.hessian_apply, op.rhs(),
+                                           oalg.SolverConfig(max_iters=iters), precond=olmp,
+                                           cost_fn=op.quadratic_cost, trials=trials, with_x=True)
+        assert len(tr.cost) == iters + 1
+        assert_trace(tr, ref, ej, er)
+        x = X[m].cpu().numpy()
+        worst[m] = assert_increment(x, xr, ex)
+        # (iv) the identity-traced J of our x against its exact cost
+        exact = op.quadratic_cost(x)
+        assert abs(tr.cost[-1] - exact) <= 1e-10 * abs(exact), (m, tr.cost[-1], exact)
+        assert abs(tr.cost[0] - op.quadratic_cost(np.zeros_like(x))) <= 1e-12 * abs(tr.cost[0])
+    return worst
+
+
+# ------------------------------------------------------------------ cfg4 --
+
+def test_cfg4_benched_path_shape(cfg4):
+    """The pass really is the benched configuration: a replayed CUDA graph
+    over two member groups, single-pass LMP, recurrence J; and a second
+    replay reproduces the first bit for bit."""
+    dens, eng, res, res2 = cfg4
+    graphs = eng.members.__dict__.get("_pcg_graphs", {})
+    assert len(graphs) == 1
+    entry = next(iter(graphs.values()))
+    assert entry.G == 2 and [r.M for r in entry.runs] == [100, 100]
+    assert res.lmp.single_pass() is not None
+    assert torch.equal(res.x, res2.x)
+    for a, b in zip(res.traces, res2.traces):
+        assert a.cost == b.cost and a.resnorm == b.resnorm
+
+
+def test_cfg4_graph_equals_eager(cfg4):
+    """Graph replay == eager launches of the same two staggered groups, bit
+    for bit, at the full cfg4 size (members and traces)."""
+    from paper_2605_23571_b200.krylov import pcg_members
+    dens, eng, res, _ = cfg4
+    B = eng.all_rows.rhs_all()
+    X, trs = pcg_members(eng.members, B[1:].contiguous(), eng.scfg, res.lmp, graph=False)
+    assert torch.equal(X, res.x)
+    for a, b in zip(trs, res.traces):
+        assert a.cost == b.cost and a.resnorm == b.resnorm
+    # one group (different GEMM tiling of the LMP step): equal to rounding
+    X1, trs1 = pcg_members(eng.members, B[1:].contiguous(), eng.scfg, res.lmp, graph=False,
+                           groups=1)
+    assert float((X1 - res.x).norm() / res.x.norm()) < 1e-9
+    for a, b in zip(trs1, res.traces):
+        np.testing.assert_allclose(a.cost, b.cost, rtol=1e-11)
+
+
+def test_cfg4_ritz_values_and_lmp(cfg4):
+    """(i): all 128 Ritz values of the benched pass vs the oracle Nystrom on
+    the GPU's own Y (cfg4: l = k = 128)."""
+    dens, eng, res, _ = cfg4
+    _check_nystrom(eng, res, oalg.NystromConfig(128, 128, shift_mode="trace"), trials=3)
+
+
+def test_cfg4_member_traces_increments_and_cost(cfg4):
+    """(ii)-(iv) for members 0 and 99 (group 1) and 100 and 199 (group 2):
+    the full 81-entry J and residual traces and the final increments of the
+    benched pass against the oracle PCG."""
+    dens, eng, res, _ = cfg4
+    worst = _check_members(dens, res, [0, 99, 100, 199], 80, trials=2)
+    print("cfg4 rel x error per member:", worst)
+
+
+def test_cfg4_cost_identity_midway(cfg4):
+    """(iv) at iteration 40: a 40-iteration solve through the same graph
+    path; its trace is the 80-iteration pass's prefix bit for bit, and its
+    identity J equals the oracle's exact quadratic_cost of its x."""
+    from paper_2605_23571_b200.krylov import SolverConfig, pcg_members
+    dens, eng, res, _ = cfg4
+    B = eng.all_rows.rhs_all()
+    X40, tr40 = pcg_members(eng.members, B[1:].contiguous(), SolverConfig(max_iters=40),
+                            res.lmp)
+    for m in (0, 150):
+        assert tr40[m].cost == res.traces[m].cost[:41]
+        assert tr40[m].resnorm == res.traces[m].resnorm[:41]
+    ops = oracle_rows(dens, [1, 151])
+    for m, op in zip((0, 150), ops):
+        exact = op.quadratic_cost(X40[m].cpu().numpy())
+        assert abs(tr40[m].cost[40] - exact) <= 1e-10 * abs(exact), (m, tr40[m].cost[40], exact)
+
+
+# ------------------------------------------------------------------ cfg5 --
+
+def test_cfg5_pass_ritz_traces_increments():
+    """cfg5 (n = 262144, 12-step window, 256 members with their own
+    trajectories, l = 256, rank-128 LMP, 20 PCG iterations): Ritz values on
+    the GPU's own Y (the cluster Jacobi route), and J / residual traces and
+    final increments of members 0 (group 1) and 255 (group 2)."""
+    dens, eng, res = _run(5)
+    from paper_2605_23571_b200.krylov import _default_groups
+    assert _default_groups(eng.members.M) == 2
+    _check_nystrom(eng, res, oalg.NystromConfig(256, 128, shift_mode="trace"), trials=2)
+    worst = _check_members(dens, res, [0, 255], 20, trials=1)
+    print("cfg5 rel x error per member:", worst)

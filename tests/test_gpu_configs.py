@@ -14,38 +14,14 @@ import pytest
 import torch
 
 from oracle import algorithms as oalg
-from oracle import l96 as ol96
-from oracle.obs import ObsNetwork as OObs
-from oracle.problem import MemberProblem as OProblem
-from oracle.cov import CirculantFactor as OFactor, DiagonalNoise as ONoise
-from parity import assert_trace, assert_values, nystrom_envelope, pcg_envelope, teacher_forced_step
+from parity import (assert_trace, assert_values, nystrom_envelope, oracle_rows, pcg_envelope,
+                    teacher_forced_step)
 
 pytestmark = pytest.mark.gpu
 
 
 def rel(a, b):
     return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300)
-
-
-def oracle_rows(dens, rows):
-    """Oracle MemberProblems for ensemble rows (0 = control) on the device
-    ensemble's own trajectories and innovations."""
-    cfg = dens.cfg
-    states = dens.states.cpu().numpy()
-    innov = dens.innovations.cpu().numpy()
-    net = OObs(dens.net.grid, dens.net.times)
-    ub = OFactor(cfg.n, dens.ub.symbol)
-    out = []
-    cache = {}
-    for r in rows:
-        t = int(dens.traj_of[r])
-        if t not in cache:
-            st = states[t]
-            stg = np.stack([np.stack(ol96.rk4_stages(st[s], cfg.dt, cfg.forcing)[1])
-                            for s in range(cfg.n_steps)])
-            cache[t] = ol96.Trajectory(st, stg, cfg.dt, cfg.forcing)
-        out.append(OProblem(cache[t], net, ub, ONoise(cfg.sigma_obs), innov[r]))
-    return out
 
 
 @pytest.fixture(scope="module")

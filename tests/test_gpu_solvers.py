@@ -11,7 +11,8 @@ import pytest
 import torch
 
 from conftest import GOLDEN, unpack_problem
-from parity import lmp_pcg_envelope, assert_trace, assert_values, nystrom_envelope, pcg_envelope
+from parity import (assert_increment, assert_trace, assert_values, lmp_pcg_envelope, nystrom_envelope,
+                    pcg_envelope)
 from oracle import algorithms as oalg
 from oracle.twin import TwinConfig, build_setup
 from paper_2605_23571_b200 import _lib
@@ -101,6 +102,28 @@ def test_svd_jacobi(gpu, rows, cols, kind, monkeypatch):
     npt.assert_allclose(u * sig.cpu().numpy(), m @ v, atol=1e-12 * s_ref[0])
     npt.assert_allclose(u.T @ u, np.eye(cols), atol=1e-12)
     npt.assert_allclose(v.T @ v, np.eye(cols), atol=1e-12)
+
+
+@pytest.mark.parametrize("kind", ["auto", "cluster"])
+def test_svd_jacobi_256_no_v(gpu, kind, monkeypatch):
+    """The cfg5 route of the Nystrom stage: l = 256, T = R_Y C^-1 square,
+    left vectors only (8-CTA cluster kernel, jacobi_cluster.cu): singular
+    values vs LAPACK, U orthonormal, U^T T has orthogonal rows of norm sig."""
+    from paper_2605_23571_b200.linalg import svd_jacobi
+    if kind == "cluster":
+        monkeypatch.setenv("EDAK_JACOBI_CLUSTER", "1")
+    rng = np.random.default_rng(256)
+    q1, _ = np.linalg.qr(rng.standard_normal((256, 256)))
+    q2, _ = np.linalg.qr(rng.standard_normal((256, 256)))
+    m = (q1 * np.logspace(3, -5, 256)) @ q2.T
+    U, sig, _ = svd_jacobi(torch.tensor(m.T.copy(), device="cuda"))
+    s_ref = np.linalg.svd(m, compute_uv=False)
+    s = sig.cpu().numpy()
+    npt.assert_allclose(s, s_ref, rtol=1e-11, atol=1e-13 * s_ref[0])
+    u = U.cpu().numpy().T
+    npt.assert_allclose(u.T @ u, np.eye(256), atol=1e-12)
+    b = u.T @ m
+    npt.assert_allclose(b @ b.T, np.diag(s ** 2), atol=1e-11 * s_ref[0] ** 2)
 
 
 def _lmp_action_close(ours, ref_vecs, ref_vals, theta, n, tol):
@@ -222,15 +245,16 @@ def test_cfg1_lmp_pcg_golden(gpu, ref_problem):
     lmp = make_lmp(approx, "halfsum")
     for j in (0, 4, 9):
         m = _gpu_problem(st.members[j])
-        _, tr = pcg(m.hessian_apply, m.rhs(), SolverConfig(max_iters=30), precond=lmp,
+        x, tr = pcg(m.hessian_apply, m.rhs(), SolverConfig(max_iters=30), precond=lmp,
                     cost_fn=m.quadratic_cost)
         npt.assert_allclose(tr.cost, g[f"cfg1_m{j}_cost"], rtol=1e-10)
         ref = np.asarray(g[f"cfg1_m{j}_resnorm"])
-        _, _, env_r = lmp_pcg_envelope(st.control, g["cfg1_gamma"],
-                                       oalg.NystromConfig(10, 10, shift_mode="trace"), "halfsum",
-                                       st.members[j], oalg.SolverConfig(max_iters=30))
+        _, _, env_r, _, env_x = lmp_pcg_envelope(
+            st.control, g["cfg1_gamma"], oalg.NystromConfig(10, 10, shift_mode="trace"), "halfsum",
+            st.members[j], oalg.SolverConfig(max_iters=30), with_x=True)
         tol = np.maximum(1e-10 * ref[0], 10 * env_r)
         assert np.all(np.abs(np.array(tr.resnorm) - ref) <= tol)
+        assert_increment(x, g[f"cfg1_m{j}_x"], env_x)
 
 
 def test_pcg_members_batched_equals_single(gpu):
@@ -478,15 +502,60 @@ def test_pcg_small_cfg1_golden(gpu, ref_problem):
     approx = nystrom_evd(ctl.a_apply, g["cfg1_gamma"], NystromConfig(10, 10, shift_mode="trace"))
     lmp = make_lmp(approx, "halfsum")
     ens = Ensemble.from_members([_gpu_problem(m) for m in st.members])
-    _, trs = pcg_members(ens, ens.rhs_all(), SolverConfig(max_iters=30), precond=lmp, small=True)
+    X, trs = pcg_members(ens, ens.rhs_all(), SolverConfig(max_iters=30), precond=lmp, small=True)
+    X = X.cpu().numpy()
     for j in (0, 4, 9):
         npt.assert_allclose(trs[j].cost, g[f"cfg1_m{j}_cost"], rtol=1e-10)
         ref = np.asarray(g[f"cfg1_m{j}_resnorm"])
-        _, _, env_r = lmp_pcg_envelope(st.control, g["cfg1_gamma"],
-                                       oalg.NystromConfig(10, 10, shift_mode="trace"), "halfsum",
-                                       st.members[j], oalg.SolverConfig(max_iters=30))
+        _, _, env_r, _, env_x = lmp_pcg_envelope(
+            st.control, g["cfg1_gamma"], oalg.NystromConfig(10, 10, shift_mode="trace"), "halfsum",
+            st.members[j], oalg.SolverConfig(max_iters=30), with_x=True)
         tol = np.maximum(1e-10 * ref[0], 10 * env_r)
         assert np.all(np.abs(np.array(trs[j].resnorm) - ref) <= tol)
+        assert_increment(X[j], g[f"cfg1_m{j}_x"], env_x)
+
+
+@pytest.mark.parametrize("path", ["dropin", "batched", "persistent"])
+def test_cfg2_member_pcg_golden(gpu, ref_problem, path):
+    """cfg2 (n = 40, 50 members with their OWN trajectories, l = 50 > n, the
+    eps*trace(W) shift path, k = 20): the GPU Nystrom LMP of the control and
+    the 50-iteration member solves of members 0 and 17 (harness.py:256-266
+    per-member solves through krylov.py:49-97) against the reference's golden
+    J traces, residual histories and final increments -- through the drop-in
+    pcg, the batched per-iteration engine and the persistent one-launch
+    solve (the path bench cfg2 takes)."""
+    from paper_2605_23571_b200.assim import Ensemble
+    from paper_2605_23571_b200.krylov import SolverConfig, pcg, pcg_members
+    from paper_2605_23571_b200.lmp import make_lmp
+    from paper_2605_23571_b200.nystrom import NystromConfig, nystrom_evd
+    g = ref_problem
+    octl = unpack_problem(g, "cfg2_")
+    ctl = _gpu_problem(octl)
+    approx = nystrom_evd(ctl.a_apply, g["cfg2_gamma"], NystromConfig(50, 20, shift_mode="trace"))
+    assert approx.shift == pytest.approx(float(g["cfg2_k20_shift"]), rel=1e-12)
+    lmp = make_lmp(approx, "halfsum")
+    ops = [unpack_problem(g, f"cfg2_m{j}_") for j in (0, 17)]
+    mems = [_gpu_problem(o) for o in ops]
+    cfg = SolverConfig(max_iters=50)
+    if path == "dropin":
+        res = [pcg(m.hessian_apply, m.rhs(), cfg, precond=lmp, cost_fn=m.quadratic_cost)
+               for m in mems]
+    else:
+        ens = Ensemble.from_members(mems)
+        X, trs = pcg_members(ens, ens.rhs_all(), cfg, precond=lmp, small=(path == "persistent"))
+        res = list(zip(X.cpu().numpy(), trs))
+    for (x, tr), j, om in zip(res, (0, 17), ops):
+        ref_j = np.asarray(g[f"cfg2_m{j}_cost"])
+        ref_r = np.asarray(g[f"cfg2_m{j}_resnorm"])
+        ref, env_j, env_r, _, env_x = lmp_pcg_envelope(
+            octl, g["cfg2_gamma"], oalg.NystromConfig(50, 20, shift_mode="trace"), "halfsum", om,
+            oalg.SolverConfig(max_iters=50), with_x=True)
+        assert len(tr.cost) == ref_j.size == 51
+        assert np.all(np.abs(np.asarray(tr.cost) - ref_j) <= np.maximum(1e-10 * np.abs(ref_j),
+                                                                          10 * env_j))
+        assert np.all(np.abs(np.asarray(tr.resnorm) - ref_r) <= np.maximum(1e-10 * ref_r[0],
+                                                                            10 * env_r))
+        assert_increment(x, g[f"cfg2_m{j}_x"], env_x)
 
 
 def test_pcg_small_breakdown_statuses(gpu):

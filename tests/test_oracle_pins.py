@@ -64,10 +64,11 @@ def test_member_problem_bit_exact(ref_problem):
 def test_pcg_trace_bit_exact(ref_problem):
     g = ref_problem
     prob = unpack_problem(g, "tiny_")
-    _, tr = pcg(prob.hessian_apply, prob.rhs(), SolverConfig(max_iters=8),
+    x, tr = pcg(prob.hessian_apply, prob.rhs(), SolverConfig(max_iters=8),
                 cost_fn=prob.quadratic_cost)
     npt.assert_array_equal(tr.cost, g["tiny_pcg_cost"])
     npt.assert_array_equal(tr.resnorm, g["tiny_pcg_resnorm"])
+    npt.assert_array_equal(x, g["tiny_pcg_x"])  # final increment (krylov.py:97)
 
 
 def test_nystrom_lmp_pcg_match_reference(ref_problem):
@@ -79,9 +80,31 @@ def test_nystrom_lmp_pcg_match_reference(ref_problem):
     assert approx.shift == float(g["tiny_nys_shift"])
     lmp = make_lmp(approx, "halfsum")
     assert lmp.theta == pytest.approx(float(g["tiny_theta"]), rel=1e-12)
-    _, tr = pcg(prob.hessian_apply, prob.rhs(), SolverConfig(max_iters=8),
+    x, tr = pcg(prob.hessian_apply, prob.rhs(), SolverConfig(max_iters=8),
                 precond=lmp, cost_fn=prob.quadratic_cost)
     npt.assert_allclose(tr.cost, g["tiny_lmp_cost"], rtol=1e-10)
+    assert np.linalg.norm(x - g["tiny_lmp_x"]) <= 1e-10 * np.linalg.norm(g["tiny_lmp_x"])
+
+
+@pytest.mark.parametrize("cfg_id,members,iters,k", [(1, (0, 4, 9), 30, 10), (2, (0, 17), 50, 20)])
+def test_member_lmp_pcg_increments_match_reference(ref_problem, cfg_id, members, iters, k):
+    """cfg1 / cfg2 member solves (Nystrom LMP from the control, own or shared
+    trajectories) by the oracle against the reference's golden J traces and
+    final increments x (rel 1e-10 at cfg1/2)."""
+    g = ref_problem
+    ctl = unpack_problem(g, f"cfg{cfg_id}_")
+    gam = g[f"cfg{cfg_id}_gamma"]
+    ell = gam.shape[1]
+    lmp = make_lmp(nystrom_evd(ctl.a_apply, gam, NystromConfig(ell=ell, k=k, shift_mode="trace")),
+                   "halfsum")
+    st = baseline_setup(BASELINE_CONFIGS[1]) if cfg_id == 1 else None
+    for j in members:
+        m = st.members[j] if cfg_id == 1 else unpack_problem(g, f"cfg2_m{j}_")
+        x, tr = pcg(m.hessian_apply, m.rhs(), SolverConfig(max_iters=iters), precond=lmp,
+                    cost_fn=m.quadratic_cost)
+        npt.assert_allclose(tr.cost, g[f"cfg{cfg_id}_m{j}_cost"], rtol=1e-10)
+        xr = g[f"cfg{cfg_id}_m{j}_x"]
+        assert np.linalg.norm(x - xr) <= 1e-10 * np.linalg.norm(xr), (j, np.linalg.norm(x - xr))
 
 
 def test_reference_harness_fixtures_regenerate():
