@@ -339,7 +339,7 @@ def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fu
     import os
     M = ens.M
     G = _default_groups(M) if groups is None else groups
-    if snapshots is not None or M < 2:
+    if M < 2:
         G = 1
     G = max(1, min(G, M))
     apply_p = precond.apply_cols if precond is not None else None
@@ -364,8 +364,19 @@ def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fu
         return _pcg_members_graph(ens, B, Z0, cfg, lmp, cost, G)
     runs, streams = _group_runs(ens, B, Z0, cfg, apply_p, lmp, cost, G, fused)
     main = streams[0]
+
+    def snap(it):
+        # every group's state after iteration it, members in order (the
+        # groups are stepped on their own streams: wait for all of them)
+        for g in range(1, G):
+            main.wait_stream(streams[g])
+        parts = [r.snapshot(it) for r in runs]
+        snapshots.append((it,) + tuple(torch.cat([p[i] for p in parts], 0) for i in range(1, 5)))
+        for g in range(1, G):
+            streams[g].wait_stream(main)
+
     if snapshots is not None:
-        snapshots.append(runs[0].snapshot(0))
+        snap(0)
     rtol = runs[0].rtol
     stagger = _stagger()
     for it in range(1, cfg.max_iters + 1):
@@ -377,7 +388,7 @@ def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fu
         if G > 1:
             ens.n_matvecs += 1  # one batched member apply per iteration
         if snapshots is not None:
-            snapshots.append(runs[0].snapshot(it))
+            snap(it)
         if rtol >= 0.0 and it % check_every == 0:
             for g in range(1, G):
                 main.wait_stream(streams[g])

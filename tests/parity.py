@@ -20,22 +20,86 @@ JITTER = 2e-16
 PCG_JITTER = 1e-15
 
 
+class _ScipyFftFactor:
+    """The oracle's circulant factor with scipy.fft (pypocketfft) in place
+    of numpy.fft: an equally valid fp64 evaluation of covariance.py:41-45
+    that rounds differently ('oracle with numpy.fft vs
+    scipy.fft')."""
+
+    def __init__(self, ub):
+        self.n, self.symbol = ub.n, ub.symbol
+
+    def apply(self, v):
+        import scipy.fft as sfft
+        vhat = sfft.rfft(v, axis=0)
+        vhat *= self.symbol[:, None] if vhat.ndim == 2 else self.symbol
+        return sfft.irfft(vhat, n=self.n, axis=0)
+
+    apply_t = apply
+
+
+def _single_pass(lmp):
+    """P v = v + S diag(theta/(lam+1) - 1) S^T v: the one-pass form of the
+    reference's P = U(U v) (lmp.py:72-74), equal in exact arithmetic."""
+    S, c = lmp.vectors, lmp.theta / (lmp.values + 1.0) - 1.0
+
+    def apply(v):
+        w = S.T @ v
+        return v + S @ ((c[:, None] * w) if w.ndim == 2 else c * w)
+    return apply
+
+
+def _variants(apply_h, precond, cost_fn):
+    """Structured CPU-vs-CPU variants of one PCG solve, each a legitimate
+    fp64 implementation of the reference algorithm: the one-pass LMP, the
+    scipy.fft factor, and both.  Measured at cfg4: a PCG stagnation bump
+    (iterations ~20-25) amplifies the one-pass/two-pass difference to
+    2.7e-7 relative in J, ~10x more than random 1e-15 jitter shows."""
+    out = []
+    prob = getattr(apply_h, "__self__", None)
+    alt = None
+    if prob is not None and getattr(apply_h, "__name__", "") == "hessian_apply" and hasattr(prob, "ub"):
+        from oracle.problem import MemberProblem
+        alt = MemberProblem(prob.traj, prob.net, _ScipyFftFactor(prob.ub), prob.rn, prob.innovation)
+    alt_cost = None
+    if alt is not None and cost_fn is not None and getattr(cost_fn, "__self__", None) is prob:
+        alt_cost = alt.quadratic_cost
+    one = _single_pass(precond) if isinstance(precond, oalg.SpectralLmp) else None
+    if one is not None:
+        out.append((apply_h, one, cost_fn))
+    if alt is not None and (cost_fn is None or alt_cost is not None):
+        out.append((alt.hessian_apply, precond, alt_cost))
+        if one is not None:
+            out.append((alt.hessian_apply, one, alt_cost))
+    return out
+
+
 def pcg_envelope(apply_h, b, cfg, precond=None, cost_fn=None, trials=6, seed=7, with_x=False):
     """(reference trace, envelope of |dJ|, envelope of |d resnorm|); with
-    ``with_x`` also (reference x, envelope of ||dx||)."""
+    ``with_x`` also (reference x, envelope of ||dx||).  The envelope is the
+    spread over random 1e-15 jitter of H p and P r (``trials`` runs) and the
+    structured variants of ``_variants``."""
     x_ref, ref = oalg.pcg(apply_h, b, cfg, precond=precond, cost_fn=cost_fn)
     rng = np.random.default_rng(seed)
     n = len(ref.cost)
     e_j, e_r, e_x = np.zeros(n), np.zeros(n), 0.0
     papply = None if precond is None else (precond if callable(precond) else precond.apply)
-    for _ in range(trials):
+    one = _single_pass(precond) if isinstance(precond, oalg.SpectralLmp) else None
+    runs = []
+    for t in range(trials):
+        # jitter on top of the two-pass and (alternately) the one-pass LMP
+        base = one if (one is not None and t % 2) else papply
+
         def h(v):
             return apply_h(v) * (1 + PCG_JITTER * rng.standard_normal(np.shape(v)))
 
-        def pc(v):
-            w = v if papply is None else papply(v)
+        def pc(v, base=base):
+            w = v if base is None else base(v)
             return w * (1 + PCG_JITTER * rng.standard_normal(np.shape(v)))
-        x, tr = oalg.pcg(h, b, cfg, precond=pc, cost_fn=cost_fn)
+        runs.append((h, pc, cost_fn))
+    runs.extend(_variants(apply_h, precond, cost_fn))
+    for h, pc, cf in runs:
+        x, tr = oalg.pcg(h, b, cfg, precond=pc, cost_fn=cf)
         m = min(n, len(tr.cost))
         e_j[:m] = np.maximum(e_j[:m], np.abs(np.array(tr.cost[:m]) - ref.cost[:m]))
         e_r[:m] = np.maximum(e_r[:m], np.abs(np.array(tr.resnorm[:m]) - ref.resnorm[:m]))
@@ -105,11 +169,13 @@ def lmp_pcg_envelope(op, phi, ncfg, rule, member, cfg, trials=4, seed=321, with_
     for _ in range(trials):
         yp = y * (1 + JITTER * rng.standard_normal(y.shape))
         lp = oalg.make_lmp(oalg.nystrom_evd(lambda v: yp, phi, ncfg), rule)
-        x, tr = oalg.pcg(member.hessian_apply, b, cfg, precond=lp, cost_fn=member.quadratic_cost)
-        m = min(n, len(tr.cost))
-        e_j[:m] = np.maximum(e_j[:m], np.abs(np.array(tr.cost[:m]) - ref.cost[:m]))
-        e_r[:m] = np.maximum(e_r[:m], np.abs(np.array(tr.resnorm[:m]) - ref.resnorm[:m]))
-        e_x = max(e_x, float(np.linalg.norm(x - x_ref)))
+        for pc in (lp, _single_pass(lp)):
+            x, tr = oalg.pcg(member.hessian_apply, b, cfg, precond=pc,
+                             cost_fn=member.quadratic_cost)
+            m = min(n, len(tr.cost))
+            e_j[:m] = np.maximum(e_j[:m], np.abs(np.array(tr.cost[:m]) - ref.cost[:m]))
+            e_r[:m] = np.maximum(e_r[:m], np.abs(np.array(tr.resnorm[:m]) - ref.resnorm[:m]))
+            e_x = max(e_x, float(np.linalg.norm(x - x_ref)))
     if with_x:
         return ref, e_j, e_r, x_ref, e_x
     return ref, e_j, e_r
