@@ -14,7 +14,7 @@ import pytest
 import torch
 
 from oracle import algorithms as oalg
-from parity import (assert_trace, assert_values, nystrom_envelope, oracle_rows, pcg_envelope,
+from parity import (assert_increment, assert_trace, assert_values, nystrom_envelope, oracle_rows, pcg_envelope,
                     teacher_forced_step)
 
 pytestmark = pytest.mark.gpu
@@ -37,11 +37,11 @@ def cfg3_pass():
     G, approx, lmp = eng.build_lmp(B)
     from paper_2605_23571_b200.krylov import pcg_members
     X, traces = pcg_members(eng.members, B[1:].contiguous(), eng.scfg, lmp, snapshots=snaps)
-    return dens, eng, B, G, approx, lmp, traces, snaps
+    return dens, eng, B, G, approx, lmp, traces, snaps, X
 
 
 def test_cfg3_rhs_and_sketch(cfg3_pass):
-    dens, eng, B, G, approx, lmp, traces, snaps = cfg3_pass
+    dens, eng, B, G, approx, lmp, traces, snaps, _ = cfg3_pass
     rows = [0, 1, 17, 50]
     ops = oracle_rows(dens, rows)
     Bh = B.cpu().numpy()
@@ -56,7 +56,7 @@ def test_cfg3_rhs_and_sketch(cfg3_pass):
 
 
 def test_cfg3_nystrom_values(cfg3_pass):
-    dens, eng, B, G, approx, lmp, traces, snaps = cfg3_pass
+    dens, eng, B, G, approx, lmp, traces, snaps, _ = cfg3_pass
     ctl = oracle_rows(dens, [0])[0]
     phi = G.cpu().numpy().T
     cfg = oalg.NystromConfig(64, 64, shift_mode="trace")
@@ -68,14 +68,22 @@ def test_cfg3_nystrom_values(cfg3_pass):
 
 
 def test_cfg3_pcg_traces_and_teacher_forcing(cfg3_pass):
-    dens, eng, B, G, approx, lmp, traces, snaps = cfg3_pass
+    dens, eng, B, G, approx, lmp, traces, snaps, X = cfg3_pass
     ops = oracle_rows(dens, [1, 25])
     # oracle LMP built from OUR eigenpairs, so the PCG comparison isolates PCG
     olmp = oalg.SpectralLmp(approx.vectors, approx.values, lmp.theta)
+    # the benched path (EdaPass.run: CUDA-graph replay of the same solve)
+    # gives the snapshot run's results bit for bit
+    res = eng.run()
+    assert torch.equal(res.x, X)
+    for a, b in zip(res.traces, traces):
+        assert a.cost == b.cost and a.resnorm == b.resnorm
     for j, (row, op) in enumerate(zip([1, 25], ops)):
-        ref, ej, er = pcg_envelope(op.hessian_apply, op.rhs(), oalg.SolverConfig(max_iters=60),
-                                   precond=olmp, cost_fn=op.quadratic_cost, trials=3)
+        ref, ej, er, xr, ex = pcg_envelope(op.hessian_apply, op.rhs(),
+                                           oalg.SolverConfig(max_iters=60), precond=olmp,
+                                           cost_fn=op.quadratic_cost, trials=3, with_x=True)
         assert_trace(traces[row - 1], ref, ej, er)
+        assert_increment(X[row - 1].cpu().numpy(), xr, ex)  # final increment (krylov.py:97)
         # teacher forcing at every iteration
         worst = 0.0
         for (it, X, R, P, rz), (_, X1, R1, P1, rz1) in zip(snaps[:-1], snaps[1:]):
