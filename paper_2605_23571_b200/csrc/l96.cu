@@ -18,12 +18,6 @@
 
 namespace edak {
 
-struct SweepGeom {
-  int W;         // output window per tile (ring elements)
-  int HL;        // left halo
-  int periodic;  // 1: one tile covers the ring, nact = n / C
-  int nact;
-};
 
 // ------------------------------------------------------------------ RK4 --
 
@@ -647,6 +641,9 @@ static void widen_pairs(const edak_problem* P, bool stream, int& C, int& NT, Swe
   geo.nact = NT;
 }
 
+int launch_tl_tile(const edak_problem* P, const double* vin, double* obs, int ncols, const int32_t* col_traj,
+                   const SweepGeom& geo, int nt, int s0, int s1, double* vout, cudaStream_t st);
+
 // warp-tile sweeps (EDAK_SWEEP_WARP): one warp per tile of 16 x 32 = 512
 // ring elements, halos by shuffles, no CTA barrier.  Window chunks of K steps
 // (EDAK_WARP_CHUNK) keep the redundant halo (12K + 8) a small share of the
@@ -716,6 +713,13 @@ int launch_tl(const edak_problem* P, const double* v0, double* obs, int ncols, c
     const double* vin = c == 0 ? v0 : work2 + (size_t)((c - 1) & 1) * blk;
     double* vout = c + 1 < nch ? work2 + (size_t)(c & 1) * blk : nullptr;
     dim3 grid(nt, ncols);
+    if (C == 16 && NT == 64 && !stream && pair_ok(P, geo) && !env_int("EDAK_SWEEP_LEGACY", 0)) {
+      const int rc = launch_tl_tile(P, vin, obs, ncols, col_traj, geo, nt, s0, s1, vout, st);
+      if (rc != EDAK_EUNSUPPORTED) {
+        if (rc) return rc;
+        continue;
+      }
+    }
     // measured best on B200: 4 resident CTAs (126 regs, no spills)
     const int mb = env_int("EDAK_TL_MINB", 4);
     if (C == 8 && NT == 128 && !stream && mb == 4 && pair_ok(P, geo)) {

@@ -19,6 +19,13 @@
 
 namespace edak {
 
+struct SweepGeom {
+  int W;         // output window per tile (ring elements)
+  int HL;        // left halo
+  int periodic;  // 1: one tile covers the ring, nact = n / C
+  int nact;
+};
+
 template <int C, int NT>
 struct Ring {
   int t, prev, next, nact;

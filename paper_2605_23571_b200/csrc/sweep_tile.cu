@@ -1,0 +1,334 @@
+// Tile-mode TL sweep (half of every Hessian apply on rings of n >= 4160):
+// the same arithmetic as k_tl in l96.cu -- RK4 stages recomputed
+// bit-exactly from the stored states (model.py:38-48), TL of model.py:56-63
+// with the time-major observation capture of obs.py:47-50 -- on 1024-element
+// tiles (16 elements x 64 threads) with redundant halos, with the state
+// window of each step staged by the Tensor Memory Accelerator:
+//
+//  * ONE cp.async.bulk.tensor (SASS UTMALDG) per step and CTA, issued by one
+//    thread, completing on an mbarrier ring (SYNCS) that every consumer
+//    waits on.  The window [gm2, gm2 + 1028) of a state row starts at any
+//    even element: the tensor map is 3-D, {16 elements, rows of 128 B,
+//    8 sub-row shifts of 16 B} -- overlapping strides, so coordinate
+//    (0, E >> 4, (E & 15) >> 1) addresses element E -- and the 65 x 128-B
+//    box lands 128-byte-swizzled, so thread t's 16-byte window reads (its
+//    row t and the first two chunks of row t + 1) are bank-conflict free
+//    with one XOR per read.  Replaces nine 16-byte cp.async per thread and
+//    step plus their address arithmetic (the staging ablation had cost the
+//    sweeps 12-15%, profiles/r1_sweep_knobs_ab.txt).
+//  * The two tiles per column whose window wraps the ring end stage it with
+//    per-thread cp.async into the same swizzled layout, completing on the
+//    same mbarrier (cp.async.mbarrier.arrive.noinc), so the loop is shared.
+//
+// EDAK_SWEEP_LEGACY=1 selects k_tl instead (A/B); the results are
+// bit-identical (every element's operation sequence is unchanged).
+// Measured at cfg4 / cfg5 (profiles/r2_sweep_tma_ab.txt): TL 0.3236 ->
+// 0.3213 ms / 2.927 -> 2.921 ms per sweep.  The same staging in the AD
+// sweep (two or three buffers, X_s re-read from its buffer instead of held
+// in registers) measured 10% SLOWER than k_ad (0.374 -> 0.411 ms at cfg4),
+// so the AD keeps its cp.async staging.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "sweep.cuh"
+
+namespace edak {
+
+// ------------------------------------------------- mbarrier / TMA / LDS --
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(m), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t m, unsigned parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(m), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ double2 lds2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+
+// State window [gm2, gm2 + R + 4) of one row, 128-byte swizzled: window
+// element w sits in row w >> 4, 16-byte chunk ((w >> 1) & 7) ^ (row & 7) of
+// a 1024-byte-aligned buffer of 65 rows (ROWS x 128 B; BUF bytes apart).
+template <int C, int NT>
+struct TmaStage {
+  static_assert(C == 16, "one 128-byte row per thread");
+  static constexpr int R = C * NT;
+  static constexpr int ROWS = NT + 1;
+  static constexpr unsigned BYTES = ROWS * 128;
+  static constexpr unsigned BUF = (BYTES + 1023) / 1024 * 1024;
+
+  // the common case: one TMA load of 65 rows at element offset E of the
+  // trajectory set (coordinates of the 3-D overlapping-stride map)
+  __device__ static __forceinline__ void tma(uint32_t buf, const CUtensorMap* tm, const double* src,
+                                             const double* states, uint32_t mbar) {
+    const int64_t E = src - states;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar), "r"(BYTES) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4}], [%5];\n" ::"r"(buf),
+        "l"((uint64_t)tm), "r"(0), "r"((int)(E >> 4)), "r"((int)((E & 15) >> 1)), "r"(mbar)
+        : "memory");
+  }
+  // wrapped windows (the tiles across the ring end): per-thread 16-byte
+  // cp.async into the same layout; each thread's copies arrive on the
+  // mbarrier (initialised with NT arrivals for these CTAs) when they land
+  __device__ static __forceinline__ void wrapped(uint32_t buf, const double* row, int gm2, int n, uint32_t mbar) {
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < (R + 4) / 2 / NT + 1; ++k) {
+      const int m = t + k * NT;  // pair m = window elements 2m, 2m + 1
+      if (m < (R + 4) / 2) {
+        int g = gm2 + 2 * m;
+        g = g < 0 ? g + n : (g >= n ? g - n : g);
+        const int r = m >> 3;
+        const uint32_t dst = buf + 128 * r + 16 * ((m & 7) ^ (r & 7));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(row + g) : "memory");
+      }
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(mbar) : "memory");
+  }
+  // thread t's window (own elements 16t .. 16t + 15 and the 2 + 2 halo):
+  // row t's chunks 0..7 and row t + 1's chunks 0, 1.  Chunk c of row r sits
+  // at byte 128 r + 16 (c ^ (r & 7)) = (128 r + 16 (r & 7)) ^ 16 c of the
+  // 1024-aligned buffer: one XOR per 16-byte load.
+  __device__ static __forceinline__ void win(uint32_t buf, int t, double (&a)[C + 4]) {
+    const uint32_t A = buf + 128u * t + 16u * (t & 7), A2 = buf + 128u * (t + 1) + 16u * ((t + 1) & 7);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double2 v = lds2(A ^ (16u * c));
+      a[2 * c] = v.x;
+      a[2 * c + 1] = v.y;
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const double2 v = lds2(A2 ^ (16u * c));
+      a[C + 2 * c] = v.x;
+      a[C + 2 * c + 1] = v.y;
+    }
+  }
+};
+
+// shared-memory carve-up of a tile kernel: exchange buffers, NB 1024-aligned
+// stage buffers, extra doubles, NB mbarriers
+template <int C, int NT, int NB>
+struct TileSmem {
+  using TS = TmaStage<C, NT>;
+  static constexpr size_t XB = (sizeof(XBuf<NT>) + 1023) / 1024 * 1024;
+  static constexpr size_t bytes(size_t extra_doubles) {
+    return 1024 /* alignment slack */ + XB + NB * (size_t)TS::BUF + extra_doubles * 8 + NB * 8;
+  }
+};
+
+// ------------------------------------------------------------------- TL --
+template <int C, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    k_tl_tile(const __grid_constant__ CUtensorMap tmap, edak_problem P, const double* __restrict__ vin,
+              double* __restrict__ obs, const int32_t* __restrict__ col_traj, SweepGeom geo, int s0, int s1,
+              double* __restrict__ vout) {
+  using TS = TmaStage<C, NT>;
+  using SM = TileSmem<C, NT, 3>;
+  constexpr int NB = 3;  // X_s, X_{s+1}, X_{s+2}: staged two steps ahead
+  extern __shared__ __align__(16) unsigned char dsm_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(((uintptr_t)dsm_raw + 1023) & ~(uintptr_t)1023);
+  XBuf<NT>& xb = *reinterpret_cast<XBuf<NT>*>(base);
+  const uint32_t sb0 = smem_u32(base + SM::XB);  // stage buffer 0
+  const uint32_t mb0 = sb0 + NB * TS::BUF;       // mbarrier 0
+  Ring<C, NT> R;
+  const int n = P.n;
+  const int i0 = blockIdx.x * geo.W;
+  R.init(n, i0 - geo.HL, NT, false);
+  const int gst = R.base - 2;
+  const bool wraps = gst < 0 || gst + 16 * TS::ROWS > n;  // CTA-uniform
+  xb.init_pads();
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NB; ++b) mbar_init(mb0 + 8 * b, wraps ? NT : 1);
+    mbar_init_fence();
+  }
+  const int col = blockIdx.y;
+  const int wlo = geo.HL, whi = geo.HL + min(geo.W, n - i0);
+  const int traj = col_traj ? col_traj[col] : 0;
+  const double* tr = P.states + (size_t)traj * P.traj_stride;
+  const int G = P.G;
+  double* ob = obs + (size_t)col * G * P.T;
+  const double dt = P.dt, h = 0.5 * dt, c6 = dt / 6.0, F = P.forcing;
+  __syncthreads();  // mbarriers initialised before any copy or wait
+
+  // window chunk [s0, s1): v enters at level s0 and leaves at level s1
+  double v[C + 4];
+  R.load_own(vin + (size_t)col * n, v);
+  int gw[C];  // observed own elements inside the output window: grid position or -1
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    const int e = R.t * C + j;
+    gw[j] = (e >= wlo && e < whi) ? __ldg(P.gpos + R.gidx(j)) : -1;
+  }
+  auto capture_tp = [&](int tp) {
+    if (tp < 0) return;
+    double* ot = ob + (size_t)tp * G;
+    asm("" : "+l"(ot));  // opaque per-level base: 32-bit grid offsets per element
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+      if (gw[j] >= 0) ot[gw[j]] = v[j + 2];
+  };
+  if (s0 == 0) capture_tp(__ldg(P.tpos));
+
+  auto stage = [&](int level, int b) {
+    const uint32_t buf = sb0 + b * TS::BUF, mb = mb0 + 8 * b;
+    if (wraps) TS::wrapped(buf, tr + (size_t)level * n, gst, n, mb);
+    else if (threadIdx.x == 0) TS::tma(buf, &tmap, tr + (size_t)level * n + gst, P.states, mb);
+  };
+  stage(s0, 0);  // prologue: X_{s0}, X_{s0+1}
+  if (s0 + 1 < s1) stage(s0 + 1, 1);
+
+  int xbi = 0;  // exchange buffer (double-buffered)
+  R.put(&xb.v[xbi][0][0][0], v);  // v's halos for the first step's exchange
+  auto xchg2 = [&](double (&a)[C + 4], double (&b)[C + 4]) {
+    R.put(&xb.v[xbi][0][0][0], a);
+    R.put(&xb.v[xbi][1][0][0], b);
+    __syncthreads();
+    R.get(&xb.v[xbi][0][0][0], a);
+    R.get(&xb.v[xbi][1][0][0], b);
+    xbi ^= 1;
+  };
+
+  const int32_t* tpp = P.tpos + s0 + 1;
+  int bcur = 0, bnext = 2;
+  unsigned ph = 0;  // mbarrier phase bit per buffer
+#pragma unroll 1
+  for (int s = s0; s < s1; ++s) {
+    asm("" : "+l"(tpp));
+    const int tp_next = __ldg(tpp);  // consumed at the end of the step
+    mbar_wait(mb0 + 8 * bcur, (ph >> bcur) & 1u);
+    ph ^= 1u << bcur;
+    __syncthreads();  // v's halos published; buffer (s + 2) % 3 no longer read
+    if (s + 2 < s1) stage(s + 2, bnext);
+    R.get(&xb.v[xbi][0][0][0], v);
+    xbi ^= 1;
+    double X[C + 4];
+    TS::win(sb0 + bcur * TS::BUF, R.t, X);
+    ++tpp;
+    bcur = bcur + 1 == NB ? 0 : bcur + 1;
+    bnext = bnext + 1 == NB ? 0 : bnext + 1;
+
+    double acc[C];
+    double x2[C + 4], u2[C + 4];
+#pragma unroll
+    for (int j = 0; j < C; ++j) {  // a1 = J(X) v; x2 = X + h f(X); u2 = v + h a1
+      const double d = __dsub_rn(X[j + 3], X[j]);
+      const double a = l96_tl_d(v[j + 3], v[j], v[j + 1], v[j + 2], d, X[j + 1]);
+      x2[j + 2] = axpy_rn(X[j + 2], h, l96_f_d(d, X[j + 1], X[j + 2], F));
+      acc[j] = a;
+      u2[j + 2] = fma(h, a, v[j + 2]);
+    }
+    xchg2(x2, u2);
+    double x3[C + 4], u3[C + 4];
+#pragma unroll
+    for (int j = 0; j < C; ++j) {  // a2 = J(x2) u2; x3 = X + h f(x2); u3 = v + h a2
+      const double d = __dsub_rn(x2[j + 3], x2[j]);
+      const double a = l96_tl_d(u2[j + 3], u2[j], u2[j + 1], u2[j + 2], d, x2[j + 1]);
+      x3[j + 2] = axpy_rn(X[j + 2], h, l96_f_d(d, x2[j + 1], x2[j + 2], F));
+      acc[j] = fma(2.0, a, acc[j]);
+      u3[j + 2] = fma(h, a, v[j + 2]);
+    }
+    xchg2(x3, u3);
+    double x4[C + 4], u4[C + 4];
+#pragma unroll
+    for (int j = 0; j < C; ++j) {  // a3 = J(x3) u3; x4 = X + dt f(x3); u4 = v + dt a3
+      const double d = __dsub_rn(x3[j + 3], x3[j]);
+      const double a = l96_tl_d(u3[j + 3], u3[j], u3[j + 1], u3[j + 2], d, x3[j + 1]);
+      x4[j + 2] = axpy_rn(X[j + 2], dt, l96_f_d(d, x3[j + 1], x3[j + 2], F));
+      acc[j] = fma(2.0, a, acc[j]);
+      u4[j + 2] = fma(dt, a, v[j + 2]);
+    }
+    xchg2(x4, u4);
+#pragma unroll
+    for (int j = 0; j < C; ++j) {  // a4 = J(x4) u4; v += (dt/6)(a1 + 2 a2 + 2 a3 + a4)
+      const double a = l96_tl(u4[j + 3], u4[j], u4[j + 1], u4[j + 2], x4[j + 3], x4[j], x4[j + 1]);
+      v[j + 2] = fma(c6, acc[j] + a, v[j + 2]);
+    }
+    R.put(&xb.v[xbi][0][0][0], v);  // halos for the next step's exchange
+    capture_tp(tp_next);
+  }
+  if (vout) {
+    double* vo = vout + (size_t)col * n;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int e = R.t * C + j;
+      if (e >= wlo && e < whi) vo[R.gidx(j)] = v[j + 2];
+    }
+  }
+}
+
+// ------------------------------------------------------------ launchers --
+// The 3-D overlapping-stride tensor map of a trajectory set (see the file
+// comment), cached per states pointer.
+static bool tile_map(const edak_problem* P, CUtensorMap* out) {
+  static PFN_cuTensorMapEncodeTiled enc = nullptr;
+  static const void* last = nullptr;
+  static CUtensorMap cached;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) != cudaSuccess ||
+        !enc) {
+      enc = nullptr;
+      return false;
+    }
+  }
+  if (last != P->states) {
+    // rows: TMA checks coordinates only; every box the kernels request lies
+    // inside the allocation (states hold N + 1 levels, the sweeps read
+    // levels 0..N-1, a box ends at most 12 elements past its window)
+    cuuint64_t dims[3] = {16, (cuuint64_t)1 << 31, 8};
+    cuuint64_t strides[2] = {128, 16};
+    cuuint32_t box[3] = {16, 65, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&cached, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(P->states), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+    last = P->states;
+  }
+  *out = cached;
+  return true;
+}
+
+static bool tile_ok(const edak_problem* P) {
+  // 16-byte aligned rows (pair_ok in l96.cu), a ring long enough that only
+  // two tiles wrap, and an (N + 1)-th level behind the last swept one
+  return P->n >= 4 * (16 * 64 + 16) && P->traj_stride >= (int64_t)(P->n_steps + 1) * P->n;
+}
+
+template <int NB, typename K, typename... Args>
+static int go_tile(K kernel, size_t extra_doubles, dim3 grid, cudaStream_t st, const char* what, Args... args) {
+  const size_t bytes = TileSmem<16, 64, NB>::bytes(extra_doubles);
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  kernel<<<grid, 64, bytes, st>>>(args...);
+  count_launch();
+  return check_launch(what);
+}
+
+int launch_tl_tile(const edak_problem* P, const double* vin, double* obs, int ncols, const int32_t* col_traj,
+                   const SweepGeom& geo, int nt, int s0, int s1, double* vout, cudaStream_t st) {
+  CUtensorMap tm;
+  if (!tile_ok(P) || !tile_map(P, &tm)) return EDAK_EUNSUPPORTED;
+  return go_tile<3>(k_tl_tile<16, 64, 4>, 0, dim3(nt, ncols), st, "k_tl_tile", tm, *P, vin, obs, col_traj, geo,
+                    s0, s1, vout);
+}
+
+}  // namespace edak

@@ -199,7 +199,7 @@ def test_pair_staging_equals_generic(gpu, monkeypatch):
     (n=16384, 2 chunks) and periodic mode (n=1024)."""
     from paper_2605_23571_b200.assim import Linearization
     from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
-    for n, N, L in [(16384, 16, 16.0), (1024, 12, 8.0), (6002, 9, 8.0)]:
+    for n, N, L in [(16384, 16, 16.0), (1024, 12, 8.0), (6002, 9, 8.0), (16384, 24, 16.0), (9000, 13, 8.0)]:
         op = _oracle_problem(n, N, 4, 3, L, 11)
         ub = CirculantFactor(n, op.ub.symbol)
         a = Linearization(op.traj.states[None], 0.025, 8.0, op.net, ub, DiagonalNoise(1.0))
@@ -210,6 +210,12 @@ def test_pair_staging_equals_generic(gpu, monkeypatch):
         assert torch.equal(hz, a.hessian_cols(z))
         assert torch.equal(rd, a.rhs_cols(d))
         monkeypatch.delenv("EDAK_NO_PAIR")
+        # TMA-staged tile sweeps (sweep_tile.cu, the default on long even
+        # rings) == the cp.async-staged k_tl / k_ad, wrapped tiles included
+        monkeypatch.setenv("EDAK_SWEEP_LEGACY", "1")
+        assert torch.equal(hz, a.hessian_cols(z)), (n, "legacy")
+        assert torch.equal(rd, a.rhs_cols(d)), (n, "legacy")
+        monkeypatch.delenv("EDAK_SWEEP_LEGACY")
         # U_B register blocking 8 vs 16 outputs per thread: same tap order, same bits
         for r in ("8", "16"):
             monkeypatch.setenv("EDAK_CIRC_R", r)
