@@ -184,6 +184,14 @@ __global__ void __launch_bounds__(256) k_reduce_parts(const double* __restrict__
   }
 }
 
+int launch_reduce_parts(const double* part, int nsplit, int m, int nb, double* C, int ldc, cudaStream_t st) {
+  const int64_t tot = (int64_t)m * nb;
+  const int nblk = (int)((tot * 8 + 255) / 256);
+  k_reduce_parts<<<nblk < 4096 ? nblk : 4096, 256, 0, st>>>(part, nsplit, m, nb, C, ldc);
+  count_launch();
+  return check_launch("k_reduce_parts");
+}
+
 // tiling for N columns: 64 x 112 for 65..112 (EDAK_GEMM_WIDE=0: always 64 x 64)
 static bool gemm_wide(int nb) {
   const char* e = getenv("EDAK_GEMM_WIDE");

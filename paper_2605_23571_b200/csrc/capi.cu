@@ -35,6 +35,12 @@ int launch_circ(const edak_problem*, const double*, double*, int, double, const 
                 double* dotp = nullptr);
 int circ_tiles(int n);
 int64_t gemm_tn_partials(int, int, int64_t);
+bool lmp_gemm_ok(int64_t n, int k, int M);
+int64_t lmp_tn_partials(int64_t n, int k, int M);
+int launch_lmp_tn(const double* S, const double* R, int64_t n, int k, int M, double* part, cudaStream_t st);
+int launch_lmp_nn(const double* S, const double* W, const double* coef, int64_t n, int k, int M, const double* Cin,
+                  const double* colscale, const double* C2, double* D, cudaStream_t st);
+int launch_reduce_parts(const double* part, int nsplit, int m, int nb, double* C, int ldc, cudaStream_t st);
 int launch_gemm_tn(const double*, int64_t, const double*, int64_t, double*, int, int, int, int64_t, double*,
                    cudaStream_t);
 int launch_gemm_nn(const double*, int64_t, const double*, int, const double*, const double*, int64_t, double,
@@ -264,6 +270,13 @@ int edak_pcg_beta(int n, int ncols, const double* z, const double* r, double* p,
                          as_stream(stream));
 }
 
+// the LMP-shaped DMMA kernels (lmp_gemm.cu): rank <= 128 (even), <= 112
+// columns, even n >= 4096, 16-byte aligned operands
+static bool lmp_shapes_ok(int n, int k, int ncols, const double* S, const double* r, const double* out) {
+  return lmp_gemm_ok(n, k, ncols) && ((uintptr_t)S & 15) == 0 && ((uintptr_t)r & 15) == 0 &&
+         ((uintptr_t)out & 15) == 0;
+}
+
 int edak_pcg_lmp_beta(int n, int k, int ncols, const double* S, const double* coef, const double* r, double* p,
                       double* work, double* lmpwork, double rtol, double* hist_rz, double* hist_J, int hist_ld,
                       int32_t* status, int32_t* iters, int it, void* stream) {
@@ -275,12 +288,15 @@ int edak_pcg_lmp_beta(int n, int k, int ncols, const double* S, const double* co
   int rc;
   // W = S^T r (lmp.py:63) as split-K partials; their reduction, rz_new =
   // |r|^2 + W^T diag(coef) W and beta in one kernel
+  bool lg = false;  // LMP-shaped kernels (lmp_gemm.cu)
 #ifdef EDAK_EXP_NOGEMM  // timing experiment only (wrong results): the pass without its LMP GEMMs
   int64_t ks_;
   const int nsplit = 1;
   (void)ks_;
 #else
-  const int nsplit = launch_gemm_tn_parts(S, n, r, n, k, ncols, n, part, st);
+  lg = lmp_shapes_ok(n, k, ncols, S, r, p);
+  int nsplit = lg ? launch_lmp_tn(S, r, n, k, ncols, part, st) : 0;
+  if (nsplit == 0) nsplit = launch_gemm_tn_parts(S, n, r, n, k, ncols, n, part, st);
 #endif
   if ((rc = check_launch("k_gemm_tn"))) return rc;
   if ((rc = launch_pcg_reduce_rz(n, ncols, k, part, nsplit, W, coef, work, rtol, hist_rz, hist_J, hist_ld, status,
@@ -290,6 +306,7 @@ int edak_pcg_lmp_beta(int n, int k, int ncols, const double* S, const double* co
 #ifdef EDAK_EXP_NOGEMM
   return EDAK_OK;
 #endif
+  if (lg) return launch_lmp_nn(S, W, coef, n, k, ncols, r, pcg_beta_ptr(n, ncols, work), p, p, st);
   return launch_gemm_nn(S, n, W, k, coef, r, n, 1.0, p, n, n, ncols, k, st, pcg_beta_ptr(n, ncols, work), p);
 }
 
@@ -304,7 +321,8 @@ int edak_pcg_small(const edak_problem* P, const int32_t* col_traj, int ncols, co
 }
 
 int64_t edak_lmp_work_doubles(int n, int k, int ncols) {
-  return (int64_t)k * ncols + gemm_tn_partials(k, ncols, n);
+  const int64_t a = gemm_tn_partials(k, ncols, n), b = lmp_tn_partials(n, k, ncols);
+  return (int64_t)k * ncols + (a > b ? a : b);
 }
 
 int edak_lmp_apply(int n, int k, int ncols, const double* S, const double* coef, const double* r, double* z,
@@ -316,6 +334,12 @@ int edak_lmp_apply(int n, int k, int ncols, const double* S, const double* coef,
   double* part = work + (int64_t)k * ncols;
   int rc;
   // W = S^T r (lmp.py:63);  z = r + S (coef o W) (lmp.py:64-65)
+  if (lmp_shapes_ok(n, k, ncols, S, r, z)) {
+    int nsplit = launch_lmp_tn(S, r, n, k, ncols, part, st);
+    if (nsplit == 0) nsplit = launch_gemm_tn_parts(S, n, r, n, k, ncols, n, part, st);
+    if ((rc = launch_reduce_parts(part, nsplit, k, ncols, W, k, st))) return rc;
+    return launch_lmp_nn(S, W, coef, n, k, ncols, r, nullptr, nullptr, z, st);
+  }
   if ((rc = launch_gemm_tn(S, n, r, n, W, k, k, ncols, n, part, st))) return rc;
   return launch_gemm_nn(S, n, W, k, coef, r, n, 1.0, z, n, n, ncols, k, st);
 }
