@@ -139,12 +139,14 @@ class Linearization:
                   _lib.ptr(dot_part), _lib.stream())
         return out
 
-    def rhs_cols(self, D, col_traj=None):
-        """U_B^T G^T R^-1 d for a (ncols, p) block of innovations."""
+    def rhs_cols(self, D, col_traj=None, out=None):
+        """U_B^T G^T R^-1 d for a (ncols, p) block of innovations (into
+        ``out`` (ncols, n), a contiguous block, when given)."""
         D = D.contiguous()
         ncols = D.shape[0]
         ct = self._map(col_traj, ncols)
-        out = torch.empty((ncols, self.n), dtype=torch.float64, device=D.device)
+        if out is None:
+            out = torch.empty((ncols, self.n), dtype=torch.float64, device=D.device)
         work = torch.empty((3 * ncols, self.n), dtype=torch.float64, device=D.device)
         _lib.call("edak_rhs", _lib.C.byref(self._P), D.data_ptr(), out.data_ptr(), ncols,
                   _lib.ptr(ct), work.data_ptr(), _lib.stream())
@@ -371,9 +373,9 @@ class Ensemble:
         views only: safe inside CUDA-graph capture)."""
         return Ensemble(self.lin, self.D[lo:hi], self.traj_of[lo:hi])
 
-    def rhs_all(self):
+    def rhs_all(self, out=None):
         """All members' right-hand sides, (M, n) device block (one launch)."""
-        return self.lin.rhs_cols(self.D, self.traj_of)
+        return self.lin.rhs_cols(self.D, self.traj_of, out)
 
     def a_apply_members(self, Z, ident=0.0, obs_out=None, out=None, work=None, dot_part=None):
         """Column j of Z through member j's Hessian term: (M, n) -> (M, n)."""

@@ -56,7 +56,7 @@ __device__ __forceinline__ void wait() {
 template <int TBK, int NST>
 __global__ void __launch_bounds__(256, 1) k_lmp_tn(const double* __restrict__ S, const double* __restrict__ R,
                                                    int64_t n, int k, int M, int nchunks,
-                                                   double* __restrict__ part) {
+                                                   double* __restrict__ part, int ldp, int col0) {
   using namespace lmpg;
   constexpr int TLD = TBK + PAD;
   extern __shared__ __align__(16) double sm[];
@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(256, 1) k_lmp_tn(const double* __restrict__ S,
           dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
   }
-  double* P = part + (size_t)blockIdx.x * k * M;
+  // partial z of column col0 + b at part[z * k * ldp + (col0 + b) * k + a]
+  double* P = part + (size_t)blockIdx.x * k * ldp + (size_t)col0 * k;
 #pragma unroll
   for (int i = 0; i < FM; ++i)
 #pragma unroll
@@ -256,6 +257,9 @@ __global__ void __launch_bounds__(lmpg::NW_NN * 32, 1)
 bool lmp_gemm_ok(int64_t n, int k, int M) {
   const char* e = getenv("EDAK_LMP_GEMM");
   if (e && atoi(e) == 0) return false;
+  // member groups beyond one 112-column tile take the generic kernels: at
+  // cfg5 (128 per group) 692 us per LMP apply vs 1290 us as 112 + 16 blocks
+  // or 3 x 655 us as three 86-member groups (profiles/r2_lmp_gemm_ab.txt)
   return k >= 1 && k <= lmpg::KMAX && k % 2 == 0 && M >= 1 && M <= lmpg::MMAX && n % 2 == 0 && n >= 4096;
 }
 
@@ -265,10 +269,11 @@ static int lmp_tn_ctas(int64_t n) {
   return (int)(nch < 148 ? nch : 148);
 }
 
-int64_t lmp_tn_partials(int64_t n, int k, int M) { return (int64_t)lmp_tn_ctas(n) * k * M; }
+int64_t lmp_tn_partials(int64_t n, int k, int M) { return (int64_t)lmp_tn_ctas(n) * k * M; }  // any M
 
 template <int TBK, int NST>
-static int go_tn(const double* S, const double* R, int64_t n, int k, int M, double* part, cudaStream_t st) {
+static int go_tn(const double* S, const double* R, int64_t n, int k, int M, double* part, int ldp, int col0,
+                 cudaStream_t st) {
   constexpr size_t smem = (size_t)NST * (lmpg::KMAX + lmpg::MMAX) * (TBK + lmpg::PAD) * sizeof(double);
   static bool attr = false;
   if (!attr) {
@@ -277,24 +282,33 @@ static int go_tn(const double* S, const double* R, int64_t n, int k, int M, doub
   }
   const int g = lmp_tn_ctas(n);
   const int nch = (int)((n + TBK - 1) / TBK);
-  k_lmp_tn<TBK, NST><<<g, 256, smem, st>>>(S, R, n, k, M, nch, part);
+  k_lmp_tn<TBK, NST><<<g, 256, smem, st>>>(S, R, n, k, M, nch, part, ldp, col0);
   count_launch();
   return g;
 }
 
-// split-K partials of W = S^T R (layout part[z][b * k + a]); returns the
-// split count, or 0 when the generic split-K GEMM should run instead
-// (EDAK_LMP_TN: 0 generic, 1 chunks of 32 x 3 stages, 2 chunks of 16 x 5)
+// split-K partials of W = S^T R (layout part[z][b * k + a], b < M) for any
+// M: column blocks of <= MMAX, each through k_lmp_tn (a column's partials do
+// not depend on the block it is in); returns the split count, or 0 when the
+// generic split-K GEMM should run instead (EDAK_LMP_TN: 0 generic, 1 chunks
+// of 32 x 3 stages, 2 (default) chunks of 16 x 5)
 int launch_lmp_tn(const double* S, const double* R, int64_t n, int k, int M, double* part, cudaStream_t st) {
   static const int mode = [] {
     const char* e = getenv("EDAK_LMP_TN");
     return e ? atoi(e) : 2;
   }();
-  if (mode == 1) return go_tn<32, 3>(S, R, n, k, M, part, st);
-  if (mode == 2) return go_tn<16, 5>(S, R, n, k, M, part, st);
-  return 0;
+  if (mode != 1 && mode != 2) return 0;
+  int g = 0;
+  for (int c0 = 0; c0 < M; c0 += lmpg::MMAX) {
+    const int m = M - c0 < lmpg::MMAX ? M - c0 : lmpg::MMAX;
+    g = mode == 1 ? go_tn<32, 3>(S, R + (size_t)c0 * n, n, k, m, part, M, c0, st)
+                  : go_tn<16, 5>(S, R + (size_t)c0 * n, n, k, m, part, M, c0, st);
+  }
+  return g;
 }
 
+// column blocks of <= MMAX members (each column's result is independent of
+// its block)
 int launch_lmp_nn(const double* S, const double* W, const double* coef, int64_t n, int k, int M, const double* Cin,
                   const double* colscale, const double* C2, double* D, cudaStream_t st) {
   static bool attr = false;
@@ -303,8 +317,14 @@ int launch_lmp_nn(const double* S, const double* W, const double* coef, int64_t 
     attr = true;
   }
   const unsigned g = (unsigned)((n + lmpg::BI - 1) / lmpg::BI);
-  k_lmp_nn<<<g, lmpg::NW_NN * 32, lmpg::SMEM_NN, st>>>(S, W, coef, n, k, M, Cin, colscale, C2, D);
-  count_launch();
+  for (int c0 = 0; c0 < M; c0 += lmpg::MMAX) {
+    const int m = M - c0 < lmpg::MMAX ? M - c0 : lmpg::MMAX;
+    const size_t off = (size_t)c0 * n;
+    k_lmp_nn<<<g, lmpg::NW_NN * 32, lmpg::SMEM_NN, st>>>(S, W + (size_t)c0 * k, coef, n, k, m,
+                                                          Cin ? Cin + off : nullptr, colscale ? colscale + c0 : nullptr,
+                                                          C2 ? C2 + off : nullptr, D + off);
+    count_launch();
+  }
   return check_launch("k_lmp_nn");
 }
 

@@ -53,6 +53,7 @@ class EdaPass:
         lin = dens.lin
         traj_of = np.asarray(dens.traj_of)
         self.all_rows = Ensemble(lin, dens.innovations, traj_of)
+        self.control_row = Ensemble(lin, dens.innovations[:1], traj_of[:1])
         self.members = Ensemble(lin, dens.innovations[1:], traj_of[1:])
         self.control = TrajectoryOperator(lin, int(traj_of[0]))
         extra = self.ell - min(self.ell, self.total_members)
@@ -79,8 +80,21 @@ class EdaPass:
         approx = nystrom_evd(self.control.a_apply, G.t(), self.ncfg)
         return G, approx, make_lmp(approx, self.rule)
 
+    def rhs(self):
+        """(M + 1, n) right-hand sides, row 0 the control's: the control and
+        the member block are two launches into the same buffer, so a member's
+        column position in every batched launch (the overlap-save U_B pairs
+        columns 2c, 2c + 1 into one complex FFT) depends only on its member
+        id, never on the control row -- the pass is then bit-identical under
+        any even member sharding (tests/test_gpu_multirank.py)."""
+        B = torch.empty((self.members.M + 1, self.cfg.n), dtype=torch.float64,
+                        device=self.dens.innovations.device)
+        self.control_row.rhs_all(out=B[:1])
+        self.members.rhs_all(out=B[1:])
+        return B
+
     def run(self, lmp=None):
-        B = self.all_rows.rhs_all()
+        B = self.rhs()
         G, approx = None, None
         if lmp is None:
             G, approx, lmp = self.build_lmp(B)

@@ -414,7 +414,10 @@ def _stagger():
 def _group_runs(ens, B, Z0, cfg, apply_p, lmp, cost, G, fused):
     """One _PcgRun per member group, each initialised on its own stream."""
     M = ens.M
-    bounds = [M * g // G for g in range(G + 1)]
+    # group bounds on even member offsets: the overlap-save U_B pairs columns
+    # (2c, 2c + 1), so even bounds keep every member's pairing (and bits)
+    # independent of the grouping and of an even sharding across ranks
+    bounds = [0] + [min(M, ((M * g // G) + 1) & ~1) for g in range(1, G)] + [M]
     main = torch.cuda.current_stream()
     streams = [main] + _side_streams(G - 1)
     runs = []

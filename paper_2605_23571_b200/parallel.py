@@ -15,12 +15,17 @@ import torch
 import torch.distributed as dist
 
 
-def shard(total, world, rank):
-    """(offset, count) of a contiguous slice of ``total`` units."""
-    base, extra = divmod(total, world)
-    count = base + (1 if rank < extra else 0)
-    offset = rank * base + min(rank, extra)
-    return offset, count
+def shard(total, world, rank, align=2):
+    """(offset, count) of a contiguous slice of ``total`` units, in blocks of
+    ``align`` units (the last rank takes the remainder).  align=2 keeps every
+    member's column pairing in the overlap-save U_B (columns 2c, 2c + 1) the
+    same on every rank count, so sharded passes are bit-identical."""
+    blocks = -(-total // align)
+    base, extra = divmod(blocks, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    offset = min(total, lo * align)
+    return offset, min(total, hi * align) - offset
 
 
 def gather_sketch_rows(local_rows, member_offset, ell, group=None):

@@ -154,8 +154,11 @@ def build_ensemble(cfg, members=None, member_offset=0, truth=None):
     y = y + cfg.sigma_obs * _dev.f64(substream(cfg.seed, "obsnoise").standard_normal(p))[None]
     # backgrounds: x_b = x_t + U_B eta_0; x_j = x_b + U_B eta_j (eda.py:93-102)
     ids = list(range(member_offset + 1, member_offset + members + 1))
-    eta = _normal_block(cfg.seed, lambda j: ("bg", j), [0] + ids, n)
-    pert = df.apply_cols(_dev.f64(eta))
+    eta = _dev.f64(_normal_block(cfg.seed, lambda j: ("bg", j), [0] + ids, n))
+    # the control's and the members' perturbations as separate blocks: the
+    # overlap-save U_B pairs columns (2c, 2c + 1), so a member's bits depend
+    # only on its id, never on the control row (even shards are bit-identical)
+    pert = torch.cat([df.apply_cols(eta[:1]), df.apply_cols(eta[1:])], 0)
     x_bg = x_true[None] + pert[:1]
     x0 = torch.cat([x_bg, x_bg + pert[1:]], 0).contiguous()
     states, _ = integrate_device(x0, cfg.dt, N, cfg.forcing)

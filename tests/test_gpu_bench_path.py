@@ -136,7 +136,7 @@ def test_cfg4_graph_equals_eager(cfg4):
     for bit, at the full cfg4 size (members and traces)."""
     from paper_2605_23571_b200.krylov import pcg_members
     dens, eng, res, _ = cfg4
-    B = eng.all_rows.rhs_all()
+    B = eng.rhs()
     X, trs = pcg_members(eng.members, B[1:].contiguous(), eng.scfg, res.lmp, graph=False)
     assert torch.equal(X, res.x)
     for a, b in zip(trs, res.traces):
@@ -177,7 +177,7 @@ def test_cfg4_member_traces_increments_and_cost(cfg4):
     from parity import teacher_forced_step
     dens, eng, res, _ = cfg4
     members = [0, 99, 100, 199]
-    B = eng.all_rows.rhs_all()
+    B = eng.rhs()
     snaps = []
     Xs, trs = pcg_members(eng.members, B[1:].contiguous(), eng.scfg, res.lmp, graph=False,
                           snapshots=snaps)
@@ -207,7 +207,7 @@ def test_cfg4_cost_identity_midway(cfg4):
     identity J equals the oracle's exact quadratic_cost of its x."""
     from paper_2605_23571_b200.krylov import SolverConfig, pcg_members
     dens, eng, res, _ = cfg4
-    B = eng.all_rows.rhs_all()
+    B = eng.rhs()
     X40, tr40 = pcg_members(eng.members, B[1:].contiguous(), SolverConfig(max_iters=40),
                             res.lmp)
     for m in (0, 150):

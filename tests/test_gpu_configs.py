@@ -33,7 +33,7 @@ def cfg3_pass():
     dens = build_ensemble(BASELINE_CONFIGS[3])
     eng = EdaPass(dens)
     snaps = []
-    B = eng.all_rows.rhs_all()
+    B = eng.rhs()
     G, approx, lmp = eng.build_lmp(B)
     from paper_2605_23571_b200.krylov import pcg_members
     X, traces = pcg_members(eng.members, B[1:].contiguous(), eng.scfg, lmp, snapshots=snaps)
@@ -144,7 +144,7 @@ def gpu_cfg4():
     from paper_2605_23571_b200.twin import BASELINE_CONFIGS, build_ensemble
     dens = build_ensemble(BASELINE_CONFIGS[4])
     eng = EdaPass(dens)
-    B = eng.all_rows.rhs_all()
+    B = eng.rhs()
     G, approx, lmp = eng.build_lmp(B)
     return dens, eng, B, G, approx, lmp
 

@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-python -m pytest tests/test_gpu_solvers.py tests/test_gpu_bench_path.py -q -x -p no:cacheprovider > gpurun_out/pytest_sol.log 2>&1; echo rc=$? >> gpurun_out/pytest_sol.log
-python bench.py --no-cpu --per-config 5 --steps 5 > gpurun_out/bench_lg.json 2> gpurun_out/bench_lg.err
+for sh in 262144,128,86 262144,128,128 16384,128,100; do for f in 0 1; do SHAPE=$sh FLAGS=$f PROFILE=$f python tools/lmp_gemm_bench.py 2>/dev/null | grep -v Warn; done; done > gpurun_out/lmp_gemm_c5.txt 2>&1

@@ -20,7 +20,7 @@ from paper_2605_23571_b200.twin import BASELINE_CONFIGS, build_ensemble  # noqa:
 dens = build_ensemble(BASELINE_CONFIGS[4])
 eng = EdaPass(dens)
 res = eng.run()
-B = eng.all_rows.rhs_all()
+B = eng.rhs()
 rows = [1, 100, 101, 200]
 sub = Ensemble(dens.lin, dens.innovations[rows], np.asarray(dens.traj_of)[rows])
 snaps = []

@@ -14,7 +14,7 @@ from paper_2605_23571_b200.twin import BASELINE_CONFIGS, build_ensemble
 dens = build_ensemble(BASELINE_CONFIGS[4])
 eng = EdaPass(dens)
 res = eng.run()
-B = eng.all_rows.rhs_all()
+B = eng.rhs()
 X1, t1 = pcg_members(eng.members, B[1:].contiguous(), eng.scfg, res.lmp, graph=False, groups=1)
 J2 = np.array([t.cost for t in res.traces])
 J1 = np.array([t.cost for t in t1])

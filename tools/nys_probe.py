@@ -20,7 +20,7 @@ def spy(M, want_v=False):
 nystrom.svd_jacobi = spy
 for c in (1, 2, 3):
     eng = EdaPass(build_ensemble(BASELINE_CONFIGS[c]))
-    B = eng.all_rows.rhs_all()
+    B = eng.rhs()
     print(f"cfg{c}")
     _, approx, _ = eng.build_lmp(B)
     v = approx.values

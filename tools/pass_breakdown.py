@@ -30,7 +30,7 @@ def t(fn, reps=3):
     return s.elapsed_time(e) / reps, r
 
 
-tr, B = t(lambda: eng.all_rows.rhs_all())
+tr, B = t(lambda: eng.rhs())
 tl, (G, approx, lmp) = t(lambda: eng.build_lmp(B))
 tp, _ = t(lambda: pcg_members(eng.members, B[1:].contiguous(), eng.scfg, lmp, eng.cost))
 tall, _ = t(lambda: eng.run())

@@ -13,7 +13,7 @@ from paper_2605_23571_b200.twin import BASELINE_CONFIGS, build_ensemble  # noqa:
 
 cfg = BASELINE_CONFIGS[int(os.environ.get("CFG", "4"))]
 eng = EdaPass(build_ensemble(cfg))
-B = eng.all_rows.rhs_all()
+B = eng.rhs()
 eng.build_lmp(B)
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStart()

@@ -13,7 +13,7 @@ for c in (1, 2):
     cfg = BASELINE_CONFIGS[c]
     eng = EdaPass(build_ensemble(cfg))
     eng.run()
-    B = eng.all_rows.rhs_all()
+    B = eng.rhs()
     _, _, lmp = eng.build_lmp(B)
     Bm = B[1:].contiguous()
     ens = eng.members
