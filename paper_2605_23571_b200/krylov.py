@@ -526,7 +526,7 @@ def lanczos_eigs(apply_h, n, m, n_eigs, seed=0):
     ``substream(seed, "lanczos")`` host stream; the Ritz problem of the
     tridiagonal matrix is solved by the device Jacobi SVD (it is SPD for the
     I + A operators this is used on; values are |Ritz values| otherwise)."""
-    from .linalg import gemm_nn, gemm_tn, svd_jacobi
+    from .linalg import col_dots, gemm_nn, gemm_tn, svd_jacobi
     from .twin import substream
     m = min(m, n)
     if not 1 <= n_eigs <= m:
@@ -556,11 +556,14 @@ def lanczos_eigs(apply_h, n, m, n_eigs, seed=0):
             v = gemm_nn(basis[:j], c, bscale=neg, Cin=v, beta=1.0)
         return v
 
+    def norm2(v):  # fixed-order device dot (edak_col_dots), one host read
+        return float(np.sqrt(float(col_dots(v, v)[0])))
+
     def fresh(j):
         for _ in range(5):
             v = torch.from_numpy(rng.standard_normal(n)).to(dev)[None]
             v = orth(v, j)
-            norm = float(torch.linalg.vector_norm(v))
+            norm = norm2(v)
             if norm > 1e-8 * np.sqrt(n):
                 return v / norm
         return None
@@ -572,10 +575,10 @@ def lanczos_eigs(apply_h, n, m, n_eigs, seed=0):
     j = 0
     while j < m:
         w = h(basis[j:j + 1])
-        alphas[j] = float((basis[j] * w[0]).sum())
+        alphas[j] = float(col_dots(basis[j:j + 1], w)[0])
         w = w - alphas[j] * basis[j:j + 1]
         w = orth(w, j + 1)
-        beta = float(torch.linalg.vector_norm(w))
+        beta = norm2(w)
         scale = max(scale, abs(alphas[j]), beta)
         if j + 1 == m:
             block_end[j] = beta

@@ -318,12 +318,39 @@ def test_lanczos_gpu(gpu):
     op = build_setup(tw).control
     vals, bounds = lanczos_eigs(_gpu_problem(op).hessian_apply, 120, 60, 40, seed=5)
     ref, ref_b = oalg.lanczos_eigs(op.hessian_apply, 120, 60, 40, seed=5)
-    npt.assert_allclose(vals, ref, rtol=1e-8)
-    assert np.all(bounds <= 1e-6 * ref[0])
+    _assert_ritz(vals, bounds, ref, ref_b)
     # dense diagonal operator with restarts through invariant subspaces
     d = np.linspace(1.0, 30.0, 30)
     v, b = lanczos_eigs(lambda x: d * x, 30, 30, 5, seed=3)
     npt.assert_allclose(v, d[::-1][:5], rtol=1e-10)
+
+
+def _assert_ritz(vals, bounds, ref, ref_b):
+    """Ritz values of two Lanczos implementations: converged ones (residual
+    bound <= 1e-6 of the value) to rel 1e-10, the rest to rel 1e-8 (their
+    position inside the unconverged cluster is rounding-sensitive)."""
+    vals, ref = np.asarray(vals), np.asarray(ref)
+    conv = np.asarray(ref_b) <= 1e-6 * ref
+    assert conv[:5].all()
+    npt.assert_allclose(vals[conv], ref[conv], rtol=1e-10)
+    npt.assert_allclose(vals, ref, rtol=1e-8)
+    npt.assert_allclose(bounds[conv], ref_b[conv], rtol=1e-2, atol=1e-12 * ref[0])
+
+
+def test_lanczos_baseline_scale(gpu):
+    """The eig-study Lanczos (krylov.py:116-168, harness.py:126-175) on the
+    BASELINE cfg4 control operator (n = 16384, 24-step window): 60 steps,
+    top 20 Ritz values against the oracle on the same device-built inputs."""
+    from paper_2605_23571_b200.assim import TrajectoryOperator
+    from paper_2605_23571_b200.krylov import lanczos_eigs
+    from paper_2605_23571_b200.twin import BASELINE_CONFIGS, build_ensemble
+    from parity import oracle_rows
+    dens = build_ensemble(BASELINE_CONFIGS[4], members=2)
+    ctl = TrajectoryOperator(dens.lin, int(dens.traj_of[0]))
+    vals, bounds = lanczos_eigs(ctl.hessian_apply, dens.cfg.n, 60, 20, seed=3)
+    op = oracle_rows(dens, [0])[0]
+    ref, ref_b = oalg.lanczos_eigs(op.hessian_apply, dens.cfg.n, 60, 20, seed=3)
+    _assert_ritz(vals, bounds, ref, ref_b)
 
 
 def test_pcg_fused_lmp_beta_matches_two_step(gpu, ref_problem):
