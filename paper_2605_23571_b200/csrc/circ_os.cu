@@ -195,15 +195,21 @@ template <int LOGM, int NT>
 __device__ __forceinline__ void os_item(double2* Z, double (*red)[NT / 32], const os::Tw<LOGM, NT>& W,
                                         const double2* __restrict__ H, int n, int L, int V, int ncols, int blk,
                                         int ca, double* __restrict__ out, double ident,
-                                        const double* __restrict__ zadd, double* __restrict__ dotp, int dtiles) {
+                                        const double* __restrict__ zadd, double* __restrict__ dotp, int dtiles,
+                                        const double2* hpre = nullptr) {
   using namespace os;
   constexpr int M = 1 << LOGM;
   const int t = threadIdx.x, cb = ca + 1;
   const bool hb = cb < ncols;
   const int i0 = blk * V;
   dif<LOGM, NT>(Z, W);
+  if (hpre) {  // block spectrum fetched at kernel start (its L2 latency hidden)
 #pragma unroll
-  for (int j = t; j < M; j += NT) Z[pz(j)] = cmul(Z[pz(j)], __ldg(H + j));
+    for (int k = 0; k < M / NT; ++k) Z[pz(t + k * NT)] = cmul(Z[pz(t + k * NT)], hpre[k]);
+  } else {
+#pragma unroll
+    for (int j = t; j < M; j += NT) Z[pz(j)] = cmul(Z[pz(j)], __ldg(H + j));
+  }
   __syncthreads();
   dit<LOGM, NT>(Z, W);
   // epilogue: outputs i0 + j, j < V, at block position L + j
@@ -255,7 +261,7 @@ __device__ __forceinline__ void os_item(double2* Z, double (*red)[NT / 32], cons
 
 // grid (blocks of V outputs, column pairs); L = left reach of u (taps k <
 // K act on in[i + tap_w - k]: reach K - 1 - tap_w to the left, tap_w right)
-template <int LOGM, int NT, int MINB = 1>
+template <int LOGM, int NT, int MINB = 1, bool PREH = false>
 __global__ void __launch_bounds__(NT, MINB) k_circ_os(int n, int L, int V, int ncols, const double2* __restrict__ T,
                                                 const double2* __restrict__ H, const double* __restrict__ in,
                                                 double* __restrict__ out, double ident,
@@ -283,10 +289,16 @@ __global__ void __launch_bounds__(NT, MINB) k_circ_os(int n, int L, int V, int n
   }
   Tw<LOGM, NT> W;
   W.load(T);
+  double2 hv[PREH ? M / NT : 1];
+  if (PREH) {
+#pragma unroll
+    for (int k = 0; k < M / NT; ++k) hv[k] = __ldg(H + t + k * NT);
+  }
 #pragma unroll
   for (int k = 0; k < M / NT; ++k) Z[pz(t + k * NT)] = make_double2(ra[k], rb[k]);
   __syncthreads();
-  os_item<LOGM, NT>(Z, red, W, H, n, L, V, ncols, blk, ca, out, ident, zadd, dotp, dtiles);
+  os_item<LOGM, NT>(Z, red, W, H, n, L, V, ncols, blk, ca, out, ident, zadd, dotp, dtiles,
+                    PREH ? hv : nullptr);
 }
 
 // U_B by overlap-save when the problem carries the block spectrum
@@ -305,16 +317,38 @@ int launch_circ_os(const edak_problem* P, const double* in, double* out, int nco
   const double2* H = reinterpret_cast<const double2*>(P->os_spec);
   // resident CTAs per SM the M = 1024 kernel is built for (A/B knob; 6 =
   // 80 registers measured best: cfg4 U_B pair 3% faster than 1 (126 regs))
+  // M = 1024 (cfg4): the block spectrum fetched at kernel start into 4
+  // resident CTAs' registers (122, no spills): 19.2 -> 17.3 us per 100
+  // columns (profiles/r2_circ_os_ab.txt); EDAK_CIRC_OS_PREH=0 / _MINB = A/B
   const char* eb = getenv("EDAK_CIRC_OS_MINB");
-  const int mb = eb ? atoi(eb) : 6;
-  if (logm == 10 && mb == 8)
+  const char* ep = getenv("EDAK_CIRC_OS_PREH");
+  const bool preh = !(ep && atoi(ep) == 0) && logm == 10;
+  const int mb = eb ? atoi(eb) : (preh ? 4 : 6);
+  if (logm == 10 && preh && mb == 4)
+    k_circ_os<10, 128, 4, true><<<grid, 128, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
+  else if (logm == 10 && preh)
+    k_circ_os<10, 128, 6, true><<<grid, 128, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
+  else if (logm == 10 && mb == 8)
     k_circ_os<10, 128, 8><<<grid, 128, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
   else if (logm == 10 && mb == 6)
     k_circ_os<10, 128, 6><<<grid, 128, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
   else if (logm == 10)
     k_circ_os<10, 128><<<grid, 128, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
-  else
-    k_circ_os<11, 256><<<grid, 256, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
+  else {
+    // M = 2048 (cfg5): 166 registers at one CTA per SM left 8 warps per SM to
+    // hide every load and barrier; 3 resident CTAs (80 registers): 435 ->
+    // 321 us per 128 columns (A/B knob EDAK_CIRC_OS2_MINB)
+    const char* e2 = getenv("EDAK_CIRC_OS2_MINB");
+    const int m2 = e2 ? atoi(e2) : 3;
+    if (m2 == 4)
+      k_circ_os<11, 256, 4><<<grid, 256, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
+    else if (m2 == 3)
+      k_circ_os<11, 256, 3><<<grid, 256, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
+    else if (m2 == 2)
+      k_circ_os<11, 256, 2><<<grid, 256, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
+    else
+      k_circ_os<11, 256><<<grid, 256, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
+  }
   count_launch();
   return check_launch("k_circ_os");
 }

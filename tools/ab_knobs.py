@@ -59,5 +59,6 @@ for rnd in range(2):
         t_tl = timeit(lambda: lin.tl_cols(V, ens.traj_of))
         t_ad = timeit(lambda: lin.ad_cols(W, ens.traj_of))
         t_h = timeit(lambda: ens.a_apply_members(V, ident=1.0))
+        t_u = timeit(lambda: lin.dfac.apply_cols(V))
         print(f"cfg{cfg.name[-1]} [{v or 'default'}] round {rnd}: TL {t_tl:.4f} ms  AD {t_ad:.4f} ms  "
-              f"hessian {t_h:.4f} ms  identical={same}", flush=True)
+              f"U_B {t_u:.4f} ms  hessian {t_h:.4f} ms  identical={same}", flush=True)
