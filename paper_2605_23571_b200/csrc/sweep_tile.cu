@@ -145,7 +145,9 @@ __global__ void __launch_bounds__(NT, MINB)
   using SM = TileSmem<C, NT, 3>;
   constexpr int NB = 3;  // X_s, X_{s+1}, X_{s+2}: staged two steps ahead
   extern __shared__ __align__(16) unsigned char dsm_raw[];
-  unsigned char* base = reinterpret_cast<unsigned char*>(((uintptr_t)dsm_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-aligned base by pointer arithmetic on the shared array (an integer
+  // round trip would make every exchange access a generic LD/ST)
+  unsigned char* base = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
   XBuf<NT>& xb = *reinterpret_cast<XBuf<NT>*>(base);
   const uint32_t sb0 = smem_u32(base + SM::XB);  // stage buffer 0
   const uint32_t mb0 = sb0 + NB * TS::BUF;       // mbarrier 0

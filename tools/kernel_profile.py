@@ -21,10 +21,13 @@ for _ in range(3):
 torch.cuda.synchronize()
 reps = int(os.environ.get("REPS", "2"))
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+phase = os.environ.get("PHASE", "pass")
+B = eng.rhs()
+fn = {"pass": eng.run, "nystrom": lambda: eng.build_lmp(B)}[phase]
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     s.record()
     for _ in range(reps):
-        eng.run()
+        fn()
     e.record()
     torch.cuda.synchronize()
 wall = s.elapsed_time(e) * 1e3 / reps
@@ -34,6 +37,6 @@ for ev in prof.key_averages():
         rows.append((ev.device_time_total / reps, ev.count // reps, ev.key))
 rows.sort(reverse=True)
 tot = sum(r[0] for r in rows)
-print(f"{cfg.name}: pass {wall / 1e3:.2f} ms (events); summed kernel time {tot / 1e3:.2f} ms")
+print(f"{cfg.name}: {phase} {wall / 1e3:.2f} ms (events); summed kernel time {tot / 1e3:.2f} ms")
 for us, cnt, name in rows[:25]:
     print(f"  {us / 1e3:8.3f} ms {100 * us / wall:5.1f}%  x{cnt:5d}  {name[:90]}")
