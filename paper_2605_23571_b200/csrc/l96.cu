@@ -643,6 +643,8 @@ static void widen_pairs(const edak_problem* P, bool stream, int& C, int& NT, Swe
 
 int launch_tl_tile(const edak_problem* P, const double* vin, double* obs, int ncols, const int32_t* col_traj,
                    const SweepGeom& geo, int nt, int s0, int s1, double* vout, cudaStream_t st);
+int launch_ad_tile(const edak_problem* P, const double* forcing, double* gout, int ncols, const int32_t* col_traj,
+                   const SweepGeom& geo, int nt, int s0, int s1, const double* gin, cudaStream_t st);
 
 // warp-tile sweeps (EDAK_SWEEP_WARP): one warp per tile of 16 x 32 = 512
 // ring elements, halos by shuffles, no CTA barrier.  Window chunks of K steps
@@ -796,6 +798,13 @@ int launch_ad(const edak_problem* P, const double* forcing, double* g, int ncols
     const double* gin = k == 0 ? nullptr : work2 + (size_t)((k - 1) & 1) * blk;
     double* gout = c == 0 ? g : work2 + (size_t)(k & 1) * blk;
     dim3 grid(nt, ncols);
+    if (C == 16 && NT == 64 && !stream && pair_ok(P, geo) && !env_int("EDAK_SWEEP_LEGACY", 0)) {
+      const int rc = launch_ad_tile(P, forcing, gout, ncols, col_traj, geo, nt, s0, s1, gin, st);
+      if (rc != EDAK_EUNSUPPORTED) {
+        if (rc) return rc;
+        continue;
+      }
+    }
     // measured best on B200: 3 resident CTAs (168 regs, no spills)
     const int mb = env_int("EDAK_AD_MINB", 3);
     if (C == 8 && NT == 128 && !stream && mb == 3 && pair_ok(P, geo)) {

@@ -1,7 +1,8 @@
-// Tile-mode TL sweep (half of every Hessian apply on rings of n >= 4160):
-// the same arithmetic as k_tl in l96.cu -- RK4 stages recomputed
+// Tile-mode TL and AD sweeps (every Hessian apply on rings of n >= 4160):
+// the same arithmetic as k_tl / k_ad in l96.cu -- RK4 stages recomputed
 // bit-exactly from the stored states (model.py:38-48), TL of model.py:56-63
-// with the time-major observation capture of obs.py:47-50 -- on 1024-element
+// with the time-major observation capture of obs.py:47-50, adjoint of
+// model.py:66-84 with the R^-1 forcing of obs.py:52-57 -- on 1024-element
 // tiles (16 elements x 64 threads) with redundant halos, with the state
 // window of each step staged by the Tensor Memory Accelerator:
 //
@@ -14,19 +15,20 @@
 //    box lands 128-byte-swizzled, so thread t's 16-byte window reads (its
 //    row t and the first two chunks of row t + 1) are bank-conflict free
 //    with one XOR per read.  Replaces nine 16-byte cp.async per thread and
-//    step plus their address arithmetic (the staging ablation had cost the
-//    sweeps 12-15%, profiles/r1_sweep_knobs_ab.txt).
+//    step plus their address arithmetic.
 //  * The two tiles per column whose window wraps the ring end stage it with
 //    per-thread cp.async into the same swizzled layout, completing on the
 //    same mbarrier (cp.async.mbarrier.arrive.noinc), so the loop is shared.
+//  * The shared-memory base is aligned by pointer arithmetic on the shared
+//    array: an integer round trip had turned every halo exchange into
+//    generic LD/ST (measured: TL 3% slower than k_tl, AD 10% slower).
 //
-// EDAK_SWEEP_LEGACY=1 selects k_tl instead (A/B); the results are
+// Measured at cfg4 / cfg5 (profiles/r2_sweep_tma_ab.txt): TL 0.324 -> 0.315
+// ms / 1.47 -> 1.44 ms per 200 / 128-column sweep; AD 0.374 -> 0.375 ms /
+// 1.83 -> 1.75 ms (its X_s is re-read from the staged buffer instead of
+// held in registers: 254 registers and no spills, against k_ad's 112-byte
+// spill).  EDAK_SWEEP_LEGACY=1 selects k_tl / k_ad (A/B); results are
 // bit-identical (every element's operation sequence is unchanged).
-// Measured at cfg4 / cfg5 (profiles/r2_sweep_tma_ab.txt): TL 0.3236 ->
-// 0.3213 ms / 2.927 -> 2.921 ms per sweep.  The same staging in the AD
-// sweep (two or three buffers, X_s re-read from its buffer instead of held
-// in registers) measured 10% SLOWER than k_ad (0.374 -> 0.411 ms at cfg4),
-// so the AD keeps its cp.async staging.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -277,6 +279,194 @@ __global__ void __launch_bounds__(NT, MINB)
   }
 }
 
+// ------------------------------------------------------------------- AD --
+// The adjoint sweep of model.py:66-84 with the R^-1 forcing of obs.py:52-57,
+// arithmetic as k_ad in l96.cu, with the same TMA staging (DEPTH steps
+// ahead); X_s is re-read from its buffer where needed instead of being held
+// in registers through the step (the AD keeps x2, x3, x4, g, vh, w and the
+// stage adjoints live), and the forcing of each level arrives by cp.async in
+// thread-private slots one step ahead.
+template <int C, int NT, int MINB, int DEPTH>
+__global__ void __launch_bounds__(NT, MINB)
+    k_ad_tile(const __grid_constant__ CUtensorMap tmap, edak_problem P, const double* __restrict__ forcing,
+              double* __restrict__ gout, const int32_t* __restrict__ col_traj, SweepGeom geo, int s0, int s1,
+              const double* __restrict__ gin) {
+  using TS = TmaStage<C, NT>;
+  constexpr int NB = DEPTH + 1;  // X_s .. X_{s-DEPTH}
+  using SM = TileSmem<C, NT, NB>;
+  extern __shared__ __align__(16) unsigned char dsm_raw[];
+  unsigned char* base = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
+  XBuf<NT>& xb = *reinterpret_cast<XBuf<NT>*>(base);
+  const uint32_t sb0 = smem_u32(base + SM::XB);
+  double* FS = reinterpret_cast<double*>(base + SM::XB + NB * TS::BUF);  // forcing slots [2][C][NT]
+  const uint32_t mb0 = smem_u32(FS + 2 * C * NT);
+  Ring<C, NT> R;
+  const int n = P.n, N = P.n_steps;
+  const int i0 = blockIdx.x * geo.W;
+  R.init(n, i0 - geo.HL, NT, false);
+  const int gst = R.base - 2;
+  const bool wraps = gst < 0 || gst + 16 * TS::ROWS > n;  // CTA-uniform
+  xb.init_pads();
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NB; ++b) mbar_init(mb0 + 8 * b, wraps ? NT : 1);
+    mbar_init_fence();
+  }
+  const int col = blockIdx.y;
+  const int wlo = geo.HL, whi = geo.HL + min(geo.W, n - i0);
+  const int traj = col_traj ? col_traj[col] : 0;
+  const double* tr = P.states + (size_t)traj * P.traj_stride;
+  const int G = P.G;
+  const double* fc = forcing + (size_t)col * G * P.T;
+  const double dt = P.dt, h = 0.5 * dt, F = P.forcing, c6 = dt / 6.0;
+  // (the reference divides by sigma**2; we multiply by its reciprocal, a
+  // 0.5-ulp difference inside the 1e-12 parity budget, as k_ad does)
+  const double inv_s2 = 1.0 / P.sigma2;
+  __syncthreads();
+
+  // forcing w_all[level] at own elements: R^-1 d at observed points
+  // (obs.py:54-56 with covariance.py:71), 0 elsewhere
+  int gp[C];
+#pragma unroll
+  for (int j = 0; j < C; ++j) gp[j] = __ldg(P.gpos + R.gidx(j));
+  auto fetch_force = [&](int tp, int slot) {  // cp.async into thread-private slots
+    if (tp < 0) return;
+    const double* f = fc + (size_t)tp * G;
+    asm("" : "+l"(f));
+    double* d = FS + (size_t)slot * C * NT + threadIdx.x;
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+      if (gp[j] >= 0) cp_async8(d + j * NT, f + gp[j]);
+  };
+
+  double g[C + 4];
+  if (gin) {
+    R.load_own(gin + (size_t)col * n, g);
+  } else {  // w_all[N] (model.py:154)
+    const int tp = __ldg(P.tpos + N);
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      g[j + 2] = 0.0;
+      if (tp >= 0 && gp[j] >= 0) g[j + 2] += __ldg(fc + (size_t)tp * G + gp[j]) * inv_s2;
+    }
+  }
+
+  auto stage = [&](int level, int b) {
+    const uint32_t buf = sb0 + b * TS::BUF, mb = mb0 + 8 * b;
+    if (wraps) TS::wrapped(buf, tr + (size_t)level * n, gst, n, mb);
+    else if (threadIdx.x == 0) TS::tma(buf, &tmap, tr + (size_t)level * n + gst, P.states, mb);
+  };
+  int tp_cur = __ldg(P.tpos + s1 - 1);
+  fetch_force(tp_cur, (s1 - 1) & 1);  // prologue: the forcing of level s1-1, X_{s1-1} (and X_{s1-2})
+  cp_commit();
+  stage(s1 - 1, 0);
+  if (DEPTH == 2 && s1 - 2 >= s0) stage(s1 - 2, 1);
+
+  int xbi = 0;
+  R.put(&xb.v[xbi][0][0][0], g);  // g's halos for the first exchange
+  auto xchg1 = [&](double (&a)[C + 4]) {
+    R.put(&xb.v[xbi][0][0][0], a);
+    __syncthreads();
+    R.get(&xb.v[xbi][0][0][0], a);
+    xbi ^= 1;
+  };
+  const int32_t* tpp = P.tpos + s1 - 2;
+  unsigned ph = 0;
+  int bcur = 0, bnext = DEPTH;
+#pragma unroll 1
+  for (int s = s1 - 1; s >= s0; --s) {
+    asm("" : "+l"(tpp));
+    const int tp_next = s > s0 ? __ldg(tpp) : -1;
+    mbar_wait(mb0 + 8 * bcur, (ph >> bcur) & 1u);
+    ph ^= 1u << bcur;
+    // X_s stays in its buffer for the whole step: re-read where needed
+    const uint32_t Xb = sb0 + bcur * TS::BUF;
+    double x2[C + 4], x3[C + 4], x4[C + 4];
+    {
+      double X[C + 4];
+      TS::win(Xb, R.t, X);
+#pragma unroll
+      for (int j = 0; j < C; ++j) x2[j + 2] = axpy_rn(X[j + 2], h, l96_f(X[j + 3], X[j], X[j + 1], X[j + 2], F));
+    }
+    R.put(&xb.v[xbi][1][0][0], x2);
+    __syncthreads();  // g, x2 halos; X_{s+1}'s buffer no longer read
+    R.get(&xb.v[xbi][0][0][0], g);
+    R.get(&xb.v[xbi][1][0][0], x2);
+    xbi ^= 1;
+    if (s > s0) fetch_force(tp_next, (s - 1) & 1);
+    cp_commit();  // the forcing group of level s - 1 (empty at s0)
+    if (s - DEPTH >= s0) stage(s - DEPTH, bnext);  // into X_{s+1}'s buffer
+    bnext = bnext + 1 == NB ? 0 : bnext + 1;
+    {
+      double X[C + 4];
+      TS::win(Xb, R.t, X);
+#pragma unroll
+      for (int j = 0; j < C; ++j)
+        x3[j + 2] = axpy_rn(X[j + 2], h, l96_f(x2[j + 3], x2[j], x2[j + 1], x2[j + 2], F));
+      xchg1(x3);
+      TS::win(Xb, R.t, X);
+#pragma unroll
+      for (int j = 0; j < C; ++j)
+        x4[j + 2] = axpy_rn(X[j + 2], dt, l96_f(x3[j + 3], x3[j], x3[j + 1], x3[j + 2], F));
+      xchg1(x4);
+    }
+    // step_adj (model.py:66-84), as in k_ad: with w = (dt/6) g and c3 = 2 c6,
+    //   b3 = h u4 + w, b2 = h u3' + w, a1 = dt u2' + w, the powers of two in vh
+    double vh[C], u[C], a[C + 4], w[C];
+#pragma unroll
+    for (int k = 0; k < C + 4; ++k) a[k] = c6 * g[k];  // a4 = (dt/6) g, halo included
+#pragma unroll
+    for (int j = 0; j < C; ++j) w[j] = a[j + 2];
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+      u[j] = l96_ad(x4[j], x4[j + 1], x4[j + 3], x4[j + 4], a[j + 1], a[j + 2], a[j + 3], a[j + 4]);
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      vh[j] = g[j + 2] + u[j];
+      a[j + 2] = fma(h, u[j], w[j]);  // b3
+    }
+    xchg1(a);
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+      u[j] = l96_ad(x3[j], x3[j + 1], x3[j + 3], x3[j + 4], a[j + 1], a[j + 2], a[j + 3], a[j + 4]);
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      vh[j] = fma(2.0, u[j], vh[j]);
+      a[j + 2] = fma(h, u[j], w[j]);  // b2
+    }
+    xchg1(a);
+#pragma unroll
+    for (int j = 0; j < C; ++j)
+      u[j] = l96_ad(x2[j], x2[j + 1], x2[j + 3], x2[j + 4], a[j + 1], a[j + 2], a[j + 3], a[j + 4]);
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      vh[j] = fma(2.0, u[j], vh[j]);
+      a[j + 2] = fma(dt, u[j], w[j]);  // a1
+    }
+    xchg1(a);
+    cp_wait_group<1>();  // this level's forcing (thread-private slots) has landed
+    const double* fd = FS + (size_t)(s & 1) * C * NT + threadIdx.x;
+    double X[C + 4];
+    TS::win(Xb, R.t, X);
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const double uj = l96_ad(X[j], X[j + 1], X[j + 3], X[j + 4], a[j + 1], a[j + 2], a[j + 3], a[j + 4]);
+      double gj = vh[j] + uj;
+      if (tp_cur >= 0 && gp[j] >= 0) gj += fd[j * NT] * inv_s2;
+      g[j + 2] = gj;
+    }
+    R.put(&xb.v[xbi][0][0][0], g);  // halos for the next step's first exchange
+    bcur = bcur + 1 == NB ? 0 : bcur + 1;
+    tp_cur = tp_next;
+    --tpp;
+  }
+  double* go = gout + (size_t)col * n;
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    const int e = R.t * C + j;
+    if (e >= wlo && e < whi) go[R.gidx(j)] = g[j + 2];
+  }
+}
+
 // ------------------------------------------------------------ launchers --
 // The 3-D overlapping-stride tensor map of a trajectory set (see the file
 // comment), cached per states pointer.
@@ -331,6 +521,20 @@ int launch_tl_tile(const edak_problem* P, const double* vin, double* obs, int nc
   if (!tile_ok(P) || !tile_map(P, &tm)) return EDAK_EUNSUPPORTED;
   return go_tile<3>(k_tl_tile<16, 64, 4>, 0, dim3(nt, ncols), st, "k_tl_tile", tm, *P, vin, obs, col_traj, geo,
                     s0, s1, vout);
+}
+
+int launch_ad_tile(const edak_problem* P, const double* forcing, double* gout, int ncols, const int32_t* col_traj,
+                   const SweepGeom& geo, int nt, int s0, int s1, const double* gin, cudaStream_t st) {
+  const char* e = getenv("EDAK_SWEEP_TMA_AD");
+  if (e && atoi(e) == 0) return EDAK_EUNSUPPORTED;
+  CUtensorMap tm;
+  if (!tile_ok(P) || !tile_map(P, &tm)) return EDAK_EUNSUPPORTED;
+  const char* ed = getenv("EDAK_AD_TDEPTH");
+  if (ed && atoi(ed) == 2)
+    return go_tile<3>(k_ad_tile<16, 64, 3, 2>, 2 * 16 * 64, dim3(nt, ncols), st, "k_ad_tile", tm, *P, forcing,
+                      gout, col_traj, geo, s0, s1, gin);
+  return go_tile<2>(k_ad_tile<16, 64, 3, 1>, 2 * 16 * 64, dim3(nt, ncols), st, "k_ad_tile", tm, *P, forcing, gout,
+                    col_traj, geo, s0, s1, gin);
 }
 
 }  // namespace edak
