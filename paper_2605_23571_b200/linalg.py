@@ -59,12 +59,50 @@ def potrf_shifted(W, mode, scale=0.0):
     return Cm, nu, info
 
 
+BLOCK_L = 128  # the register-resident Cholesky-inverse kernel's limit
+
+
+def _chol_inv_2x2(W):
+    """Unshifted upper Cholesky W = C^T C and C^-1 of a 129..256 Gram as a
+    2 x 2 block factorisation over the register kernel (l <= 128) and DMMA
+    GEMMs (dpotrf's blocked right-looking order):
+        C11 = chol(W11), C12 = C11^-T W12, C22 = chol(W22 - C12^T C12),
+        C^-1 = [[C11^-1, -C11^-1 C12 C22^-1], [0, C22^-1]].
+    Returns (C, C^-1, nu = 0, info) or None when a pivot broke down (the
+    caller then runs the single-kernel factorisation with its shift
+    schedule from the start, nystrom.py:67-93).  One host read of the two
+    breakdown flags."""
+    l, h = W.shape[0], BLOCK_L
+    m = l - h
+    W11, W12, W22 = W[:h, :h].contiguous(), W[h:, :h].contiguous(), W[h:, h:].contiguous()
+    C11, C11i, _, info1 = chol_inv(W11, 0)
+    C12 = gemm_tn(C11i, W12)                      # C11^-T W12 (h x m): block (m, h)
+    S = W22 - gemm_tn(C12, C12)                   # W22 - C12^T C12
+    C22, C22i, _, info2 = chol_inv(S.contiguous(), 0)
+    if int(info1[1]) or int(info2[1]):
+        return None
+    X = gemm_nn(C11i, gemm_nn(C12, C22i))          # C11^-1 C12 C22^-1 (h x m): block (m, h)
+    C = torch.zeros_like(W)
+    Ci = torch.zeros_like(W)
+    C[:h, :h], C[h:, :h], C[h:, h:] = C11, C12, C22
+    Ci[:h, :h], Ci[h:, :h], Ci[h:, h:] = C11i, -X, C22i
+    nu = torch.zeros(1, dtype=torch.float64, device=W.device)
+    info = torch.zeros(2, dtype=torch.int32, device=W.device)
+    return C, Ci, nu, info
+
+
 def chol_inv(W, mode, scale=0.0, want_inv=True):
     """Fused blocked Cholesky + inverse (edak_chol_inv): (C, C^-1 or None,
     nu tensor[1], info int32[2]) with potrf_shifted's schedule -- no host
-    sync."""
+    sync (except for 129..256 Grams: the 2 x 2 block path, see
+    _chol_inv_2x2, reads its breakdown flags once)."""
+    import os
     W = W.contiguous()
     l = W.shape[0]
+    if BLOCK_L < l <= 2 * BLOCK_L and os.environ.get("EDAK_CHOL_BLOCKED", "1") != "0":
+        r = _chol_inv_2x2(W)
+        if r is not None:
+            return r[0], (r[1] if want_inv else None), r[2], r[3]
     Cm = torch.empty_like(W)
     Ci = torch.empty_like(W) if want_inv else None
     nu = _empty(1, like=W)
