@@ -359,7 +359,15 @@ def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fu
     if (small and snapshots is None and fused and cost in ("recurrence", None)
             and _small_ok(ens, lmp, precond)):
         return pcg_members_small(ens, B, cfg, lmp, cost)
-    Z0 = apply_p(B) if apply_p is not None else B
+    Z0 = B
+    if apply_p is not None:
+        # z0 = P b per member group, so every member's LMP GEMMs are the
+        # group-sized kernels of its later iterations (the same kernels, hence
+        # the same bits, whatever the member count of the pass or the rank)
+        Z0 = torch.empty_like(B)
+        bounds = _group_bounds(M, G)
+        for lo, hi in zip(bounds[:-1], bounds[1:]):
+            apply_p(B[lo:hi], out=Z0[lo:hi])
     if graph:
         return _pcg_members_graph(ens, B, Z0, cfg, lmp, cost, G)
     runs, streams = _group_runs(ens, B, Z0, cfg, apply_p, lmp, cost, G, fused)
@@ -411,13 +419,17 @@ def _stagger():
     return os.environ.get("EDAK_PCG_STAGGER", "1") != "0"
 
 
+def _group_bounds(M, G):
+    """Member-group bounds on even offsets: the overlap-save U_B pairs columns
+    (2c, 2c + 1), so even bounds keep every member's pairing (and bits)
+    independent of the grouping and of an even sharding across ranks."""
+    return [0] + [min(M, ((M * g // G) + 1) & ~1) for g in range(1, G)] + [M]
+
+
 def _group_runs(ens, B, Z0, cfg, apply_p, lmp, cost, G, fused):
     """One _PcgRun per member group, each initialised on its own stream."""
     M = ens.M
-    # group bounds on even member offsets: the overlap-save U_B pairs columns
-    # (2c, 2c + 1), so even bounds keep every member's pairing (and bits)
-    # independent of the grouping and of an even sharding across ranks
-    bounds = [0] + [min(M, ((M * g // G) + 1) & ~1) for g in range(1, G)] + [M]
+    bounds = _group_bounds(M, G)
     main = torch.cuda.current_stream()
     streams = [main] + _side_streams(G - 1)
     runs = []
