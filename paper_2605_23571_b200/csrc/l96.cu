@@ -531,7 +531,7 @@ static void go(K kernel, dim3 grid, cudaStream_t st, Args... args) {
 
 // pick (C, NT) and tile geometry for a sweep with halos (hl, hr) per step
 static bool plan(int n, int hl_total, int hr_total, int& C, int& NT, SweepGeom& geo, int& ntiles,
-                 bool sweep = true) {
+                 bool sweep = true, int force_c = 0, int force_nt = 0) {
   // periodic single tile: the whole ring in one CTA (no halo redundancy)
   const int cand_p[][2] = {{8, 128}, {4, 64}, {4, 128}, {4, 256}, {4, 512},
                            {2, 64}, {2, 128}, {2, 256}, {2, 512}};
@@ -551,8 +551,11 @@ static bool plan(int n, int hl_total, int hr_total, int& C, int& NT, SweepGeom& 
   // fastest on B200 for the cfg4 sweeps (tools/ab_sweeps.py, profiles/)
   C = 8;
   NT = 128;
-  const char* f = sweep ? getenv("EDAK_SWEEP_FAMILY") : nullptr;
-  if (f) {  // A/B testing of the TL/AD sweeps: "C,NT"
+  const char* f = sweep && !force_c ? getenv("EDAK_SWEEP_FAMILY") : nullptr;
+  if (force_c) {
+    C = force_c;
+    NT = force_nt;
+  } else if (f) {  // A/B testing of the TL/AD sweeps: "C,NT"
     int c2 = 0, t2 = 0;
     if (sscanf(f, "%d,%d", &c2, &t2) == 2) {
       C = c2;
@@ -615,6 +618,22 @@ static int sweep_depth(const char* knob, int dflt) {
   return v == 2 ? 2 : 1;
 }
 
+// The TMA tile sweeps on long rings (sweep_tile.cu tile_family_nt) with a
+// window of at most one 12-step chunk: 16 x 128 element tiles (half the
+// halo share, 2 CTAs per SM) -- cfg5: Hessian block 3.85 -> 3.73 ms, pass
+// 231 -> 225 ms.  Longer windows keep 16 x 64 tiles and 12-step chunks: the
+// 16 x 128 family as ONE 24-step chunk is faster alone (cfg4 Hessian block
+// 0.758 -> 0.750 ms) but slows the two-stream PCG pass (72.4 -> 73.4 ms),
+// and as two chunks it gains nothing (profiles/r2_sweep_family_ab.txt).
+// EDAK_SWEEP_FAMILY / EDAK_SWEEP_CHUNK override.
+int tile_family_nt(const edak_problem* P);
+static int big_tiles(const edak_problem* P) {
+  if (getenv("EDAK_SWEEP_FAMILY") || P->stage_mode != 0 || env_int("EDAK_SWEEP_LEGACY", 0)) return 0;
+  // the pair-staged layout the TMA kernels need (pair_ok's problem-level part)
+  if (getenv("EDAK_NO_PAIR") || P->n % 2 || P->traj_stride % 2 || ((uintptr_t)P->states & 15)) return 0;
+  return tile_family_nt(P) == 128;
+}
+
 static int plan_chunks(int N, bool periodic, const double* work2) {
   const int K = sweep_chunk();
   if (periodic || !work2 || N <= K) return 1;
@@ -642,9 +661,9 @@ static void widen_pairs(const edak_problem* P, bool stream, int& C, int& NT, Swe
 }
 
 int launch_tl_tile(const edak_problem* P, const double* vin, double* obs, int ncols, const int32_t* col_traj,
-                   const SweepGeom& geo, int nt, int s0, int s1, double* vout, cudaStream_t st);
+                   const SweepGeom& geo, int nt, int NT, int s0, int s1, double* vout, cudaStream_t st);
 int launch_ad_tile(const edak_problem* P, const double* forcing, double* gout, int ncols, const int32_t* col_traj,
-                   const SweepGeom& geo, int nt, int s0, int s1, const double* gin, cudaStream_t st);
+                   const SweepGeom& geo, int nt, int NT, int s0, int s1, const double* gin, cudaStream_t st);
 
 // warp-tile sweeps (EDAK_SWEEP_WARP): one warp per tile of 16 x 32 = 512
 // ring elements, halos by shuffles, no CTA barrier.  Window chunks of K steps
@@ -700,6 +719,7 @@ int launch_tl(const edak_problem* P, const double* v0, double* obs, int ncols, c
     set_error("window too long for the tile family");
     return EDAK_EUNSUPPORTED;
   }
+  const bool big = !geo.periodic && N <= sweep_chunk() && big_tiles(P);
   const int nch = plan_chunks(N, geo.periodic && nt == 1, work2);
   const bool stream = P->stage_mode != 0;  // 1 stream, 2 hybrid (small rings)
   const size_t blk = (size_t)ncols * P->n;
@@ -707,7 +727,7 @@ int launch_tl(const edak_problem* P, const double* v0, double* obs, int ncols, c
     const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch), K = s1 - s0;
     // halos: stencil reach per step (TL 8 left / 4 right) plus the edge
     // garbage of the exchanged stage recompute
-    if (!plan(P->n, 8 * K + 4, 4 * K + 4, C, NT, geo, nt)) {
+    if (!plan(P->n, 8 * K + 4, 4 * K + 4, C, NT, geo, nt, true, big ? 16 : 0, big ? 128 : 0)) {
       set_error("window chunk too long for the tile family");
       return EDAK_EUNSUPPORTED;
     }
@@ -715,8 +735,8 @@ int launch_tl(const edak_problem* P, const double* v0, double* obs, int ncols, c
     const double* vin = c == 0 ? v0 : work2 + (size_t)((c - 1) & 1) * blk;
     double* vout = c + 1 < nch ? work2 + (size_t)(c & 1) * blk : nullptr;
     dim3 grid(nt, ncols);
-    if (C == 16 && NT == 64 && !stream && pair_ok(P, geo) && !env_int("EDAK_SWEEP_LEGACY", 0)) {
-      const int rc = launch_tl_tile(P, vin, obs, ncols, col_traj, geo, nt, s0, s1, vout, st);
+    if (C == 16 && (NT == 64 || NT == 128) && !stream && pair_ok(P, geo) && !env_int("EDAK_SWEEP_LEGACY", 0)) {
+      const int rc = launch_tl_tile(P, vin, obs, ncols, col_traj, geo, nt, NT, s0, s1, vout, st);
       if (rc != EDAK_EUNSUPPORTED) {
         if (rc) return rc;
         continue;
@@ -785,12 +805,13 @@ int launch_ad(const edak_problem* P, const double* forcing, double* g, int ncols
     set_error("window too long for the tile family");
     return EDAK_EUNSUPPORTED;
   }
+  const bool big = !geo.periodic && N <= sweep_chunk() && big_tiles(P);
   const int nch = plan_chunks(N, geo.periodic && nt == 1, work2);
   const bool stream = P->stage_mode != 0;  // 1 stream, 2 hybrid (small rings)
   const size_t blk = (size_t)ncols * P->n;
   for (int c = nch - 1, k = 0; c >= 0; --c, ++k) {
     const int s0 = (int)((long)N * c / nch), s1 = (int)((long)N * (c + 1) / nch), K = s1 - s0;
-    if (!plan(P->n, 4 * K + 8, 8 * K + 8, C, NT, geo, nt)) {
+    if (!plan(P->n, 4 * K + 8, 8 * K + 8, C, NT, geo, nt, true, big ? 16 : 0, big ? 128 : 0)) {
       set_error("window chunk too long for the tile family");
       return EDAK_EUNSUPPORTED;
     }
@@ -798,8 +819,8 @@ int launch_ad(const edak_problem* P, const double* forcing, double* g, int ncols
     const double* gin = k == 0 ? nullptr : work2 + (size_t)((k - 1) & 1) * blk;
     double* gout = c == 0 ? g : work2 + (size_t)(k & 1) * blk;
     dim3 grid(nt, ncols);
-    if (C == 16 && NT == 64 && !stream && pair_ok(P, geo) && !env_int("EDAK_SWEEP_LEGACY", 0)) {
-      const int rc = launch_ad_tile(P, forcing, gout, ncols, col_traj, geo, nt, s0, s1, gin, st);
+    if (C == 16 && (NT == 64 || NT == 128) && !stream && pair_ok(P, geo) && !env_int("EDAK_SWEEP_LEGACY", 0)) {
+      const int rc = launch_ad_tile(P, forcing, gout, ncols, col_traj, geo, nt, NT, s0, s1, gin, st);
       if (rc != EDAK_EUNSUPPORTED) {
         if (rc) return rc;
         continue;

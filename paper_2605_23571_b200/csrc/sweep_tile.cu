@@ -469,11 +469,12 @@ __global__ void __launch_bounds__(NT, MINB)
 
 // ------------------------------------------------------------ launchers --
 // The 3-D overlapping-stride tensor map of a trajectory set (see the file
-// comment), cached per states pointer.
-static bool tile_map(const edak_problem* P, CUtensorMap* out) {
+// comment) with a box of `rows` 128-byte rows, cached per (states, rows).
+static bool tile_map(const edak_problem* P, int rows, CUtensorMap* out) {
   static PFN_cuTensorMapEncodeTiled enc = nullptr;
-  static const void* last = nullptr;
-  static CUtensorMap cached;
+  static const void* last[2] = {nullptr, nullptr};
+  static int last_rows[2] = {0, 0};
+  static CUtensorMap cached[2];
   if (!enc) {
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) != cudaSuccess ||
@@ -482,59 +483,73 @@ static bool tile_map(const edak_problem* P, CUtensorMap* out) {
       return false;
     }
   }
-  if (last != P->states) {
+  const int slot = rows > 65 ? 1 : 0;
+  if (last[slot] != P->states || last_rows[slot] != rows) {
     // rows: TMA checks coordinates only; every box the kernels request lies
     // inside the allocation (states hold N + 1 levels, the sweeps read
     // levels 0..N-1, a box ends at most 12 elements past its window)
     cuuint64_t dims[3] = {16, (cuuint64_t)1 << 31, 8};
     cuuint64_t strides[2] = {128, 16};
-    cuuint32_t box[3] = {16, 65, 1};
+    cuuint32_t box[3] = {16, (cuuint32_t)rows, 1};
     cuuint32_t es[3] = {1, 1, 1};
-    if (enc(&cached, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(P->states), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+    if (enc(&cached[slot], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(P->states), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
-    last = P->states;
+    last[slot] = P->states;
+    last_rows[slot] = rows;
   }
-  *out = cached;
+  *out = cached[slot];
   return true;
 }
 
-static bool tile_ok(const edak_problem* P) {
+static bool tile_ok(const edak_problem* P, int NT) {
   // 16-byte aligned rows (pair_ok in l96.cu), a ring long enough that only
   // two tiles wrap, and an (N + 1)-th level behind the last swept one
-  return P->n >= 4 * (16 * 64 + 16) && P->traj_stride >= (int64_t)(P->n_steps + 1) * P->n;
+  return P->n >= 4 * (16 * NT + 16) && P->traj_stride >= (int64_t)(P->n_steps + 1) * P->n;
 }
 
-template <int NB, typename K, typename... Args>
+template <int NB, int NT, typename K, typename... Args>
 static int go_tile(K kernel, size_t extra_doubles, dim3 grid, cudaStream_t st, const char* what, Args... args) {
-  const size_t bytes = TileSmem<16, 64, NB>::bytes(extra_doubles);
+  const size_t bytes = TileSmem<16, NT, NB>::bytes(extra_doubles);
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  kernel<<<grid, 64, bytes, st>>>(args...);
+  kernel<<<grid, NT, bytes, st>>>(args...);
   count_launch();
   return check_launch(what);
 }
 
+// the tile width of the TMA sweeps for this ring: 128 threads (2048-element
+// tiles, 2 CTAs per SM) where the ring holds at least four of them, else 64
+int tile_family_nt(const edak_problem* P) { return tile_ok(P, 128) ? 128 : 64; }
+
+// tiles of 16 x NT elements: NT = 128 (long rings, l96.cu big_tiles) or 64
+// (4 TL / 3-4 AD CTAs per SM)
 int launch_tl_tile(const edak_problem* P, const double* vin, double* obs, int ncols, const int32_t* col_traj,
-                   const SweepGeom& geo, int nt, int s0, int s1, double* vout, cudaStream_t st) {
+                   const SweepGeom& geo, int nt, int NT, int s0, int s1, double* vout, cudaStream_t st) {
   CUtensorMap tm;
-  if (!tile_ok(P) || !tile_map(P, &tm)) return EDAK_EUNSUPPORTED;
-  return go_tile<3>(k_tl_tile<16, 64, 4>, 0, dim3(nt, ncols), st, "k_tl_tile", tm, *P, vin, obs, col_traj, geo,
-                    s0, s1, vout);
+  if ((NT != 64 && NT != 128) || !tile_ok(P, NT) || !tile_map(P, NT + 1, &tm)) return EDAK_EUNSUPPORTED;
+  if (NT == 128)
+    return go_tile<3, 128>(k_tl_tile<16, 128, 2>, 0, dim3(nt, ncols), st, "k_tl_tile", tm, *P, vin, obs, col_traj,
+                           geo, s0, s1, vout);
+  return go_tile<3, 64>(k_tl_tile<16, 64, 4>, 0, dim3(nt, ncols), st, "k_tl_tile", tm, *P, vin, obs, col_traj, geo,
+                        s0, s1, vout);
 }
 
 int launch_ad_tile(const edak_problem* P, const double* forcing, double* gout, int ncols, const int32_t* col_traj,
-                   const SweepGeom& geo, int nt, int s0, int s1, const double* gin, cudaStream_t st) {
+                   const SweepGeom& geo, int nt, int NT, int s0, int s1, const double* gin, cudaStream_t st) {
   const char* e = getenv("EDAK_SWEEP_TMA_AD");
   if (e && atoi(e) == 0) return EDAK_EUNSUPPORTED;
   CUtensorMap tm;
-  if (!tile_ok(P) || !tile_map(P, &tm)) return EDAK_EUNSUPPORTED;
+  if ((NT != 64 && NT != 128) || !tile_ok(P, NT) || !tile_map(P, NT + 1, &tm)) return EDAK_EUNSUPPORTED;
+  if (NT == 128)
+    return go_tile<2, 128>(k_ad_tile<16, 128, 2, 1>, 2 * 16 * 128, dim3(nt, ncols), st, "k_ad_tile", tm, *P,
+                           forcing, gout, col_traj, geo, s0, s1, gin);
   const char* ed = getenv("EDAK_AD_TDEPTH");
   if (ed && atoi(ed) == 2)
-    return go_tile<3>(k_ad_tile<16, 64, 3, 2>, 2 * 16 * 64, dim3(nt, ncols), st, "k_ad_tile", tm, *P, forcing,
-                      gout, col_traj, geo, s0, s1, gin);
-  return go_tile<2>(k_ad_tile<16, 64, 3, 1>, 2 * 16 * 64, dim3(nt, ncols), st, "k_ad_tile", tm, *P, forcing, gout,
-                    col_traj, geo, s0, s1, gin);
+    return go_tile<3, 64>(k_ad_tile<16, 64, 3, 2>, 2 * 16 * 64, dim3(nt, ncols), st, "k_ad_tile", tm, *P, forcing,
+                          gout, col_traj, geo, s0, s1, gin);
+  return go_tile<2, 64>(k_ad_tile<16, 64, 3, 1>, 2 * 16 * 64, dim3(nt, ncols), st, "k_ad_tile", tm, *P, forcing,
+                        gout, col_traj, geo, s0, s1, gin);
 }
 
 }  // namespace edak
