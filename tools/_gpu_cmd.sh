@@ -1,3 +1,4 @@
-mkdir -p gpurun_out
-python -m pytest tests/test_gpu_operator.py tests/test_gpu_bench_path.py -q -x -p no:cacheprovider -k "not member_traces" > gpurun_out/pytest_fam.log 2>&1; echo rc=$? >> gpurun_out/pytest_fam.log
-python bench.py --no-cpu --no-e2e --per-config 5 --steps 5 > gpurun_out/bench_fam.json 2> gpurun_out/bench_fam.err
+mkdir -p gpurun_out/r2full
+O=gpurun_out/r2full
+timeout 1500 ncu --set full --import-source on --clock-control none -k regex:'k_ad_tile|k_tl_tile|k_lmp_nn|k_lmp_tn|k_circ_os' -s 60 -c 8 -o $O/cfg4_top python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --per-config "" > $O/ncu.log 2>&1
+echo rc=$? >> $O/ncu.log
