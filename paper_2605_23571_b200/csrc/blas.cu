@@ -166,14 +166,22 @@ __global__ void __launch_bounds__(256) k_gemm_tn(const double* __restrict__ A, i
 // q, q+8, q+16, ... in order, then the 8 lane sums are combined in a fixed
 // butterfly order -- deterministic, and 8x the memory-level parallelism of
 // one thread per output (the reduction was latency-bound: 50 CTAs).
+// sym: the partials hold only the upper-triangle 128 x 128 tiles of a
+// symmetric product (launch_big_tn); outputs of the other tiles are read
+// from their mirror image.
 __global__ void __launch_bounds__(256) k_reduce_parts(const double* __restrict__ part, int nsplit, int m, int nb,
-                                                      double* __restrict__ C, int ldc) {
+                                                      double* __restrict__ C, int ldc, int sym = 0) {
   const int64_t tot = (int64_t)m * nb;
   const int q = threadIdx.x & 7;
   for (int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3; e < tot;
        e += ((int64_t)gridDim.x * blockDim.x) >> 3) {
+    int64_t src = e;
+    if (sym) {
+      const int a = (int)(e % m), b = (int)(e / m);
+      if ((a >> 7) > (b >> 7)) src = b + (int64_t)a * m;
+    }
     double s = 0.0;
-    for (int z = q; z < nsplit; z += 8) s += part[(size_t)z * tot + e];
+    for (int z = q; z < nsplit; z += 8) s += part[(size_t)z * tot + src];
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     s += __shfl_xor_sync(0xffffffffu, s, 4);
@@ -216,10 +224,18 @@ static int tn_nsplit(int m, int nb, int64_t K, int64_t& kslice) {
   return (int)s;
 }
 
+bool big_tn_ok(const double* A, int64_t lda, const double* B, int64_t ldb, int m, int nb, int64_t K);
+bool big_tn_sym(const double* A, int64_t lda, const double* B, int64_t ldb, int m, int nb);
+int64_t big_tn_partials(int m, int nb, int64_t K);
+int launch_big_tn(const double* A, int64_t lda, const double* B, int64_t ldb, int m, int nb, int64_t K, double* part,
+                  cudaStream_t st);
+
 int64_t gemm_tn_partials(int m, int nb, int64_t K) {
   if (m < 1 || nb < 1 || K < 1) return 0;  // empty block: no partials
   int64_t ks;
-  return (int64_t)tn_nsplit(m, nb, K, ks) * m * nb;
+  const int64_t a = (int64_t)tn_nsplit(m, nb, K, ks) * m * nb;
+  const int64_t b = m >= 128 && nb >= 128 ? big_tn_partials(m, nb, K) : 0;
+  return a > b ? a : b;
 }
 
 // split-K partials only (the consumer reduces them): returns the split count
@@ -227,6 +243,7 @@ int launch_gemm_tn_parts(const double* A, int64_t lda, const double* B, int64_t 
                          double* part, cudaStream_t st) {
   using G0 = GTile<2, 4, 2>;
   using G1 = GTile<4, 2, 7>;
+  if (big_tn_ok(A, lda, B, ldb, m, nb, K)) return launch_big_tn(A, lda, B, ldb, m, nb, K, part, st);
   int64_t ks;
   const int s = tn_nsplit(m, nb, K, ks);
   static bool attr = false;
@@ -260,9 +277,10 @@ int launch_gemm_tn_parts(const double* A, int64_t lda, const double* B, int64_t 
 int launch_gemm_tn(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int ldc, int m, int nb,
                    int64_t K, double* part, cudaStream_t st) {
   const int s = launch_gemm_tn_parts(A, lda, B, ldb, m, nb, K, part, st);
+  const int sym = big_tn_ok(A, lda, B, ldb, m, nb, K) && big_tn_sym(A, lda, B, ldb, m, nb);
   int64_t tot = (int64_t)m * nb;
   int nblk = (int)((tot * 8 + 255) / 256);
-  k_reduce_parts<<<nblk < 4096 ? nblk : 4096, 256, 0, st>>>(part, s, m, nb, C, ldc);
+  k_reduce_parts<<<nblk < 4096 ? nblk : 4096, 256, 0, st>>>(part, s, m, nb, C, ldc, sym);
   count_launch();
   return check_launch("k_gemm_tn");
 }

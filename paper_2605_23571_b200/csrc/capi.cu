@@ -36,6 +36,7 @@ int launch_circ(const edak_problem*, const double*, double*, int, double, const 
 int circ_tiles(int n);
 int64_t gemm_tn_partials(int, int, int64_t);
 bool lmp_gemm_ok(int64_t n, int k, int M);
+bool lmp_nn_ok(int M);
 int64_t lmp_tn_partials(int64_t n, int k, int M);
 int launch_lmp_tn(const double* S, const double* R, int64_t n, int k, int M, double* part, cudaStream_t st);
 int launch_lmp_nn(const double* S, const double* W, const double* coef, int64_t n, int k, int M, const double* Cin,
@@ -270,8 +271,8 @@ int edak_pcg_beta(int n, int ncols, const double* z, const double* r, double* p,
                          as_stream(stream));
 }
 
-// the LMP-shaped DMMA kernels (lmp_gemm.cu): rank <= 128 (even), <= 112
-// columns, even n >= 4096, 16-byte aligned operands
+// the LMP-shaped DMMA kernels (lmp_gemm.cu): rank <= 128 (even), even n >=
+// 4096, 16-byte aligned operands
 static bool lmp_shapes_ok(int n, int k, int ncols, const double* S, const double* r, const double* out) {
   return lmp_gemm_ok(n, k, ncols) && ((uintptr_t)S & 15) == 0 && ((uintptr_t)r & 15) == 0 &&
          ((uintptr_t)out & 15) == 0;
@@ -306,7 +307,7 @@ int edak_pcg_lmp_beta(int n, int k, int ncols, const double* S, const double* co
 #ifdef EDAK_EXP_NOGEMM
   return EDAK_OK;
 #endif
-  if (lg) return launch_lmp_nn(S, W, coef, n, k, ncols, r, pcg_beta_ptr(n, ncols, work), p, p, st);
+  if (lg && lmp_nn_ok(ncols)) return launch_lmp_nn(S, W, coef, n, k, ncols, r, pcg_beta_ptr(n, ncols, work), p, p, st);
   return launch_gemm_nn(S, n, W, k, coef, r, n, 1.0, p, n, n, ncols, k, st, pcg_beta_ptr(n, ncols, work), p);
 }
 
@@ -338,7 +339,8 @@ int edak_lmp_apply(int n, int k, int ncols, const double* S, const double* coef,
     int nsplit = launch_lmp_tn(S, r, n, k, ncols, part, st);
     if (nsplit == 0) nsplit = launch_gemm_tn_parts(S, n, r, n, k, ncols, n, part, st);
     if ((rc = launch_reduce_parts(part, nsplit, k, ncols, W, k, st))) return rc;
-    return launch_lmp_nn(S, W, coef, n, k, ncols, r, nullptr, nullptr, z, st);
+    if (lmp_nn_ok(ncols)) return launch_lmp_nn(S, W, coef, n, k, ncols, r, nullptr, nullptr, z, st);
+    return launch_gemm_nn(S, n, W, k, coef, r, n, 1.0, z, n, n, ncols, k, st);
   }
   if ((rc = launch_gemm_tn(S, n, r, n, W, k, k, ncols, n, part, st))) return rc;
   return launch_gemm_nn(S, n, W, k, coef, r, n, 1.0, z, n, n, ncols, k, st);

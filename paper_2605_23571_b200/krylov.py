@@ -267,12 +267,19 @@ def _side_streams(count):
     return lst[:count]
 
 
-def _default_groups(M):
+GROUPS_MAX_ELEMS = 1 << 23  # members x n up to which >= 64 members run as two staggered groups
+
+
+def _default_groups(M, n=0):
+    """Two member groups on two streams fill what one group's launches leave
+    idle at cfg4 (200 x 16384: 71.9 vs 76.5 ms per pass); at cfg5 (256 x
+    262144) every launch already fills the GPU and one group is faster
+    (216.4 vs 219.4 ms, tools/ab_pass.py)."""
     import os
     g = os.environ.get("EDAK_PCG_GROUPS")
     if g is not None:
         return max(1, int(g))
-    return 2 if M >= 64 else 1
+    return 2 if M >= 64 and M * n <= GROUPS_MAX_ELEMS else 1
 
 
 SMALL_MAX_N = 256  # rings up to which pcg_members runs the persistent one-CTA-per-member solve
@@ -325,7 +332,8 @@ def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fu
     so the streams only share the GPU, and one group's sweeps fill the SMs
     the other leaves idle (the last partial wave of every sweep launch, the
     HBM-bound vector updates and the DMMA GEMMs).  Default: 2 for >= 64
-    members (EDAK_PCG_GROUPS overrides).
+    members while members x n <= 2^23 (cfg4), else 1 (cfg5: every launch
+    fills the GPU on its own); EDAK_PCG_GROUPS overrides.
 
     ``graph`` (default: for members x n <= 2^22, when the iteration count is
     fixed -- no residual_rtol -- and the LMP is single-pass or absent) records the whole
@@ -338,7 +346,7 @@ def pcg_members(ens, B, cfg, precond=None, cost="recurrence", snapshots=None, fu
     Returns (X (M, n), [SolveTrace] * M)."""
     import os
     M = ens.M
-    G = _default_groups(M) if groups is None else groups
+    G = _default_groups(M, B.shape[1]) if groups is None else groups
     if M < 2:
         G = 1
     G = max(1, min(G, M))

@@ -10,9 +10,11 @@ with every dense step on the device:
 * W = Phi^T Y, Gram matrices: DMMA split-K GEMM (edak_gemm_tn);
 * Cholesky with the identical nu schedule and dpotrf breakdown test
   (edak_potrf_shifted), C^-1 (edak_trinv_upper);
-* tall, large n: CholeskyQR2 of Y (two DMMA Grams + two triangular
-  solves as GEMMs), T = R_Y C^-1, one-sided Jacobi SVD of the l x l T,
-  S = Q_Y U_T (DMMA GEMM);
+* tall, large n: CholeskyQR2 of Y (DMMA Grams and triangular solves as
+  GEMMs; a third pass only when the second Cholesky factor is not close to
+  I, the shifted CholeskyQR3 when a Gram is not numerically SPD), T =
+  R_Y C^-1, one-sided Jacobi SVD of the l x l T, S = Q_Y U_T with the last
+  pass's triangular solve applied to U_T instead of to the n x l basis;
 * small n, wide (l > n, cfg2) or when CholeskyQR2's Gram is not positive
   definite: one-sided Jacobi SVD straight on F (or F^T when l > n),
   which handles exact rank deficiency.
@@ -144,6 +146,45 @@ def _cholqr2(Y):
     return Q, R
 
 
+ORTHO_TOL = 0.1   # ||R_k - I||_F below which the pass's input basis counts as orthonormal
+MAX_PLAIN = 4     # unshifted CholeskyQR passes before the shifted CholeskyQR3 takes over
+
+
+def _cholqr_lazy(Y):
+    """Y = Q_Y R_Y with Q_Y = Qp Ti and R_Y = R, for blocks Qp (l, n),
+    the last pass's triangular inverse Ti (l, l) and R (l, l) upper, so the
+    caller forms Q_Y U only as Qp (Ti U) and never materialises Q_Y (the
+    n x l x l product of the last pass).
+
+    Unshifted CholeskyQR passes Q_k = Q_{k-1} R_k^-1 until the Cholesky
+    factor R_k of a pass's Gram is within ORTHO_TOL of I in Frobenius norm:
+    then its input Q_{k-1} has cond <= (1 + tol) / (1 - tol) and CholeskyQR
+    of it is orthonormal to O(u cond^2) = O(u) (Yamamoto, Nakatsukasa,
+    Yanagisawa, Fukaya, ETNA 2015), the level of the reference's
+    Householder QR (nystrom.py:118).  A well-conditioned sketch takes two
+    passes (CholeskyQR2) instead of shifted CholeskyQR3's three; a Gram that
+    is not numerically SPD (cond(Y) >~ u^-1/2), or no convergence in
+    MAX_PLAIN passes, falls back to the shifted CholeskyQR3 (_cholqr2).
+    One host read per pass (the breakdown flag and the deviation)."""
+    l = Y.shape[0]
+    eye = torch.eye(l, dtype=Y.dtype, device=Y.device)
+    Q, R = Y, None
+    for _ in range(MAX_PLAIN):
+        Rk, Rki, _, info = chol_inv(gemm_tn(Q, Q), 0)
+        dev = torch.linalg.matrix_norm(Rk - eye)
+        chk = torch.cat([info.to(torch.float64), dev.view(1)]).cpu().numpy()
+        if chk[1] or not np.isfinite(chk[2]):
+            break
+        R = Rk if R is None else gemm_nn(Rk, R)  # upper R_k ... R_1
+        if chk[2] <= ORTHO_TOL and Q is not Y:
+            return Q, Rki, R
+        Q = gemm_nn(Q, Rki)
+    qr = _cholqr2(Y)
+    if qr is None:
+        return None
+    return qr[0], eye, qr[1]
+
+
 def _use_qr(n, ell):
     """Tall sketches go through CholeskyQR + an (l x l) Jacobi SVD; short or
     wide ones (n < 4 l, e.g. cfg2's l = 50 > n = 40) through a Jacobi SVD
@@ -198,12 +239,12 @@ def nystrom_evd(a_apply, sketch, cfg):
         raise NystromBreakdownError("sketched Gram matrix stayed indefinite after shifting")
     shift = float(nu[0])
     k_eff = min(cfg.k, ell, n)
-    qr = _cholqr2(Y) if _use_qr(n, ell) else None
+    qr = _cholqr_lazy(Y) if _use_qr(n, ell) else None
     if qr is not None:
-        Q, R = qr
+        Qp, Ti, R = qr
         T = gemm_nn(R, Cinv)                 # R_Y C^-1 (l x l)
         U_T, sig, _ = svd_jacobi(T)
-        S = gemm_nn(Q, U_T[:k_eff])          # Q_Y U_T[:, :k]
+        S = gemm_nn(Qp, gemm_nn(Ti, U_T[:k_eff].contiguous()))  # Q_Y U_T[:, :k] = Qp (Ti U_T[:, :k])
     else:
         F = gemm_nn(Y, Cinv)                 # Y C^-1 (n x l)
         if n >= ell:

@@ -225,10 +225,10 @@ def test_cfg5_pass_ritz_traces_increments():
     """cfg5 (n = 262144, 12-step window, 256 members with their own
     trajectories, l = 256, rank-128 LMP, 20 PCG iterations): Ritz values on
     the GPU's own Y (the cluster Jacobi route), and J / residual traces and
-    final increments of members 0 (group 1) and 255 (group 2)."""
+    final increments of members 0 and 255 (one member group at this size)."""
     dens, eng, res = _run(5)
     from paper_2605_23571_b200.krylov import _default_groups
-    assert _default_groups(eng.members.M) == 2
+    assert _default_groups(eng.members.M, eng.cfg.n) == 1
     _check_nystrom(eng, res, oalg.NystromConfig(256, 128, shift_mode="trace"), trials=2)
     worst = _check_members(dens, res, [0, 255], 20, trials=3)
     print("cfg5 rel x error per member:", worst)

@@ -642,3 +642,44 @@ def test_gemm_16byte_staging_edges(gpu):
     ref = Cin + (B[:, :kk] * s) @ A[:, :M]
     assert torch.allclose(outs[0], ref, rtol=1e-12, atol=1e-12 * kk)
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("m,nb,K,sym", [(256, 256, 65536, True), (256, 256, 65538, False),
+                                        (200, 200, 70000, True), (200, 136, 65536, False),
+                                        (128, 128, 262144, True)])
+def test_gemm_tn_big_tiles(gpu, m, nb, K, sym):
+    """The 128 x 128 k_lmp_tn tiles that carry the big-K Nystrom Grams
+    (cfg5: 256 x 256 over n = 262144; symmetric products compute the upper
+    tiles and mirror the rest) against torch and the generic kernels."""
+    from paper_2605_23571_b200.linalg import gemm_tn
+    g = torch.Generator(device="cuda").manual_seed(m + nb)
+    A = torch.randn(m, K, dtype=torch.float64, device="cuda", generator=g)
+    B = A if sym else torch.randn(nb, K, dtype=torch.float64, device="cuda", generator=g)
+    C = gemm_tn(A, B)  # block (nb, m)
+    ref = B @ A.t()
+    assert torch.allclose(C, ref, rtol=1e-12, atol=1e-11 * K ** 0.5)
+    if sym:
+        assert torch.equal(C, C.t())  # mirrored, not recomputed
+    os.environ["EDAK_BIG_TN"] = "0"
+    try:
+        Cg = gemm_tn(A, B)
+    finally:
+        del os.environ["EDAK_BIG_TN"]
+    assert torch.allclose(C, Cg, rtol=1e-12, atol=1e-11 * K ** 0.5)
+
+
+@pytest.mark.parametrize("n,k,ncols", [(262144, 128, 128), (16384, 128, 120), (16384, 64, 113),
+                                       (16384, 128, 100), (8192, 128, 256)])
+def test_lmp_apply_member_tiles(gpu, n, k, ncols):
+    """z = r + S (c o S^T r) (lmp.py:62-65) through the LMP-shaped kernels at
+    112- and 128-member tiles (and 2 x 128 column blocks) against torch."""
+    g = torch.Generator(device="cuda").manual_seed(n + k + ncols)
+    S = torch.randn(k, n, dtype=torch.float64, device="cuda", generator=g) / n ** 0.5
+    coef = torch.rand(k, dtype=torch.float64, device="cuda", generator=g) - 0.5
+    R = torch.randn(ncols, n, dtype=torch.float64, device="cuda", generator=g)
+    Z = torch.empty_like(R)
+    work = torch.empty(int(_lib.lib().edak_lmp_work_doubles(n, k, ncols)), dtype=torch.float64, device="cuda")
+    _lib.call("edak_lmp_apply", n, k, ncols, S.data_ptr(), coef.data_ptr(), R.data_ptr(), Z.data_ptr(),
+              work.data_ptr(), _lib.stream())
+    ref = R + ((R @ S.t()) * coef) @ S
+    assert torch.allclose(Z, ref, rtol=1e-12, atol=1e-12)

@@ -1,4 +1,4 @@
-mkdir -p gpurun_out/r2full
-O=gpurun_out/r2full
-timeout 1500 ncu --set full --import-source on --clock-control none -k regex:'k_ad_tile|k_tl_tile|k_lmp_nn|k_lmp_tn|k_circ_os' -s 60 -c 8 -o $O/cfg4_top python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --per-config "" > $O/ncu.log 2>&1
-echo rc=$? >> $O/ncu.log
+mkdir -p gpurun_out/it
+O=gpurun_out/it
+CFG=5 REPS=3 python tools/ab_pass.py "" "EDAK_LMP_TN=0" "EDAK_LMP_GEMM=0" > $O/ab5c.txt 2>&1
+CFG=5 PHASE=pass python tools/kernel_profile.py > $O/kp5_pass.txt 2>&1
