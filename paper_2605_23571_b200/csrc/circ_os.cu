@@ -301,6 +301,244 @@ __global__ void __launch_bounds__(NT, MINB) k_circ_os(int n, int L, int V, int n
                     PREH ? hv : nullptr);
 }
 
+// ---------------------------------------------------------------------
+// Register-pass variant (k_circ_os16): the same overlap-save block FFT --
+// the same in-place radix-2 DIF network, so the same bit-reversed output
+// order and the same host spectrum H -- with its stages grouped into three
+// register passes per direction instead of two radix-2 stages plus three
+// radix-8 passes, each a shared-memory round trip:
+//
+//   M = 2048 (cfg5): radix-16 over bits [7, 11) straight from the global
+//   window, radix-16 over bits [3, 7), then radix-8 over bits [0, 3) with
+//   the spectrum product and the first inverse radix-8 on the same
+//   registers; the inverse radix-16 over bits [3, 7) and over bits [7, 11),
+//   whose registers are the natural-order outputs, stored straight to the
+//   output column.  Shared memory carries 4 round trips of the block
+//   instead of ~11: the 2048-point kernel was shared-memory-bandwidth bound
+//   (~770 KB of LDS/STS traffic per block).
+//
+// A radix-2^K pass at bit offset b holds the elements base + m 2^b (m <
+// 2^K; base has zero bits in [b, b + K)); local stage j (span 2^j in m)
+// multiplies the difference of pair (m, m + 2^j) by W_{2^(j+1)}^(m mod 2^j)
+// (compile-time roots) and by W_M^(r 2^(LOGM-1-b-j)), r = base mod 2^b.
+namespace os16 {
+
+using os::cadd;
+using os::cconj;
+using os::cmul;
+using os::csub;
+
+// a * W_{2^(J+1)}^p (forward) or its conjugate (INV), p < 2^J, J <= 3
+template <int J, bool INV>
+__device__ __forceinline__ double2 root(double2 a, int p) {
+  if (p == 0) return a;
+  constexpr int S = 3 - J;  // W_{2^(J+1)}^p = W_16^(p 2^S)
+  const int q = p << S;     // 1..7 eighths of pi
+  if (q == 4) return INV ? os::cmul_pi(a) : os::cmul_mi(a);
+  if (q == 2 || q == 6) return os::w8<INV>(a, q >> 1);
+  // odd sixteenths: cos / sin of pi q / 8
+  const double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
+  double c, sn;
+  if (q == 1) c = c1, sn = s1;
+  else if (q == 3) c = s1, sn = c1;
+  else if (q == 5) c = -s1, sn = c1;
+  else c = -c1, sn = s1;  // q == 7
+  const double w_im = INV ? sn : -sn;
+  return make_double2(fma(a.x, c, -a.y * w_im), fma(a.x, w_im, a.y * c));
+}
+
+// forward DIF of 2^K registers; tw[j] = W_M^(r 2^(LOGM-1-b-j)) (TW: apply)
+template <int K, bool TW>
+__device__ __forceinline__ void dif(double2 (&a)[1 << K], const double2 (&tw)[K]) {
+#pragma unroll
+  for (int j = K - 1; j >= 0; --j) {
+    const int hl = 1 << j;
+#pragma unroll
+    for (int m = 0; m < (1 << K); ++m) {
+      if (m & hl) continue;
+      const double2 x = a[m], y = a[m + hl];
+      a[m] = cadd(x, y);
+      double2 d = csub(x, y);
+      switch (j) {
+        case 0: break;
+        case 1: d = root<1, false>(d, m & 1); break;
+        case 2: d = root<2, false>(d, m & 3); break;
+        default: d = root<3, false>(d, m & 7); break;
+      }
+      a[m + hl] = TW ? cmul(d, tw[j]) : d;
+    }
+  }
+}
+
+// inverse DIT (unscaled), the exact mirror of dif
+template <int K, bool TW>
+__device__ __forceinline__ void dit(double2 (&a)[1 << K], const double2 (&tw)[K]) {
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const int hl = 1 << j;
+#pragma unroll
+    for (int m = 0; m < (1 << K); ++m) {
+      if (m & hl) continue;
+      double2 y = a[m + hl];
+      if (TW) y = cmul(y, cconj(tw[j]));
+      switch (j) {
+        case 0: break;
+        case 1: y = root<1, true>(y, m & 1); break;
+        case 2: y = root<2, true>(y, m & 3); break;
+        default: y = root<3, true>(y, m & 7); break;
+      }
+      const double2 x = a[m];
+      a[m] = cadd(x, y);
+      a[m + hl] = csub(x, y);
+    }
+  }
+}
+
+template <int M, int K>
+__device__ __forceinline__ void load_tw(double2 (&tw)[K], const double2* __restrict__ T, int r, int sh) {
+  // tw[j] = W_M^(r 2^(sh - j)), sh = LOGM - 1 - b
+#pragma unroll
+  for (int j = 0; j < K; ++j) tw[j] = os::tw<M>(T, (r << (sh - j)) & (M - 1));
+}
+
+}  // namespace os16
+
+// M = 2^LOGM points, M / 16 threads: pass A = radix-16 over bits
+// [LOGM - 4, LOGM) (one group per thread), pass B = radix-2^KB over bits
+// [3, LOGM - 4) (KB = 4 at M = 2048: one group per thread; KB = 3 at M =
+// 1024: two), pass C = radix-8 over bits [0, 3) (two groups per thread).
+template <int LOGM, int MINB>
+__global__ void __launch_bounds__((1 << LOGM) / 16, MINB)
+    k_circ_os16(int n, int L, int V, int ncols, const double2* __restrict__ T, const double2* __restrict__ H,
+                const double* __restrict__ in, double* __restrict__ out, double ident,
+                const double* __restrict__ zadd, double* __restrict__ dotp, int dtiles) {
+  using namespace os16;
+  static_assert(LOGM == 10 || LOGM == 11, "passes: [LOGM-4, LOGM) [3, LOGM-4) [0, 3)");
+  constexpr int M = 1 << LOGM, NT = M / 16;
+  constexpr int BA = LOGM - 4, BB = 3, KB = LOGM - 7;  // pass A / B bit offsets, pass B radix log2
+  constexpr int GB = 16 >> KB;                         // pass-B groups per thread
+  __shared__ __align__(16) double2 Z[M + M / 8];
+  __shared__ double red[2][NT / 32 > 0 ? NT / 32 : 1];
+  const int t = threadIdx.x, blk = blockIdx.x;
+  const int ca = 2 * blockIdx.y, cb = ca + 1;
+  const bool hb = cb < ncols;
+  const int i0 = blk * V;
+  const double* A = in + (size_t)ca * n;
+  const double* B = in + (size_t)(hb ? cb : ca) * n;
+  // pass A: elements t + NT m of the window [i0 - L, i0 - L + M), from HBM
+  double2 a[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    int g = i0 - L + t + NT * m;
+    g = g < 0 ? g + n : (g >= n ? g - n : g);
+    a[m] = make_double2(__ldg(A + g), hb ? __ldg(B + g) : 0.0);
+  }
+  double2 tw[4], twb[KB];
+  load_tw<M, 4>(tw, T, t, LOGM - 1 - BA);
+  dif<4, true>(a, tw);
+#pragma unroll
+  for (int m = 0; m < 16; ++m) Z[os::pz(t + NT * m)] = a[m];
+  __syncthreads();
+  // pass B: group q = t + NT h: base = (q mod 8) + 2^(LOGM-4) (q / 8),
+  // elements base + 8 m; r = q mod 8 = t mod 8 for every h
+  load_tw<M, KB>(twb, T, t & 7, LOGM - 1 - BB);
+  auto baseB = [&](int h) {
+    const int q = t + NT * h;
+    return (q & 7) + ((q >> 3) << BA);
+  };
+#pragma unroll
+  for (int h = 0; h < GB; ++h) {
+    double2 b[1 << KB];
+    const int bb = baseB(h);
+#pragma unroll
+    for (int m = 0; m < (1 << KB); ++m) b[m] = Z[os::pz(bb + (m << BB))];
+    dif<KB, true>(b, twb);
+#pragma unroll
+    for (int m = 0; m < (1 << KB); ++m) Z[os::pz(bb + (m << BB))] = b[m];
+  }
+  __syncthreads();
+  // pass C: bits [0, 3), groups g = t and t + NT (elements 8 g + m): the
+  // last forward radix-8, the spectrum product, the first inverse radix-8
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int g8 = 8 * (t + NT * h);
+    double2 c[8], hv[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) hv[m] = __ldg(H + g8 + m);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) c[m] = Z[os::pz(g8 + m)];
+    const double2 none[3] = {};
+    dif<3, false>(c, none);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) c[m] = cmul(c[m], hv[m]);
+    dit<3, false>(c, none);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) Z[os::pz(g8 + m)] = c[m];
+  }
+  __syncthreads();
+  // inverse pass B
+#pragma unroll
+  for (int h = 0; h < GB; ++h) {
+    double2 b[1 << KB];
+    const int bb = baseB(h);
+#pragma unroll
+    for (int m = 0; m < (1 << KB); ++m) b[m] = Z[os::pz(bb + (m << BB))];
+    dit<KB, true>(b, twb);
+#pragma unroll
+    for (int m = 0; m < (1 << KB); ++m) Z[os::pz(bb + (m << BB))] = b[m];
+  }
+  __syncthreads();
+  // inverse pass A: natural-order outputs q = t + NT m, straight to HBM
+#pragma unroll
+  for (int m = 0; m < 16; ++m) a[m] = Z[os::pz(t + NT * m)];
+  dit<4, true>(a, tw);
+  const int nv = min(V, n - i0);
+  double* oa = out + (size_t)ca * n;
+  double* ob = out + (size_t)cb * n;
+  const double* za = zadd ? zadd + (size_t)ca * n : nullptr;
+  const double* zb = zadd ? zadd + (size_t)cb * n : nullptr;
+  double da = 0.0, db = 0.0;
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int j = t + NT * m - L;  // output i0 + j
+    if (j < 0 || j >= nv) continue;
+    double va = a[m].x, vb = a[m].y;
+    const int i = i0 + j;
+    if (za) {
+      const double z1 = za[i];
+      va = fma(ident, z1, va);
+      da = fma(z1, va, da);
+      if (hb) {
+        const double z2 = zb[i];
+        vb = fma(ident, z2, vb);
+        db = fma(z2, vb, db);
+      }
+    }
+    oa[i] = va;
+    if (hb) ob[i] = vb;
+  }
+  if (dotp) {  // fixed-order CTA reduction -> dotp[col][blk]; slots past the last block get 0
+    da = warp_sum(da);
+    db = warp_sum(db);
+    if ((t & 31) == 0) {
+      red[0][t >> 5] = da;
+      red[1][t >> 5] = db;
+    }
+    __syncthreads();
+    if (t < 2 && (t == 0 || hb)) {
+      double s = 0.0;
+      for (int w = 0; w < NT / 32; ++w) s += red[t][w];
+      dotp[(size_t)(ca + t) * dtiles + blk] = s;
+    }
+    if (blk == 0) {
+      for (int q = (int)gridDim.x + t; q < dtiles; q += NT) {
+        dotp[(size_t)ca * dtiles + q] = 0.0;
+        if (hb) dotp[(size_t)cb * dtiles + q] = 0.0;
+      }
+    }
+  }
+}
+
 // U_B by overlap-save when the problem carries the block spectrum
 // (edak_problem.os_logm/os_spec/os_tw, covariance.py DeviceFactor); returns
 // EDAK_EUNSUPPORTED when it does not apply (the caller then convolves)
@@ -320,6 +558,20 @@ int launch_circ_os(const edak_problem* P, const double* in, double* out, int nco
   // M = 1024 (cfg4): the block spectrum fetched at kernel start into 4
   // resident CTAs' registers (122, no spills): 19.2 -> 17.3 us per 100
   // columns (profiles/r2_circ_os_ab.txt); EDAK_CIRC_OS_PREH=0 / _MINB = A/B
+  const char* e16 = getenv("EDAK_CIRC_OS16");
+  const int os16 = e16 ? atoi(e16) : 1;  // register-pass kernels (0: the shared-memory radix-2/8 passes)
+  if (logm == 10 && os16) {
+    const char* e1 = getenv("EDAK_CIRC_OS16_MINB10");
+    const int m1 = e1 ? atoi(e1) : 6;
+    if (m1 == 8)
+      k_circ_os16<10, 8><<<grid, 64, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
+    else if (m1 == 4)
+      k_circ_os16<10, 4><<<grid, 64, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
+    else
+      k_circ_os16<10, 6><<<grid, 64, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
+    count_launch();
+    return check_launch("k_circ_os16");
+  }
   const char* eb = getenv("EDAK_CIRC_OS_MINB");
   const char* ep = getenv("EDAK_CIRC_OS_PREH");
   const bool preh = !(ep && atoi(ep) == 0) && logm == 10;
@@ -334,7 +586,15 @@ int launch_circ_os(const edak_problem* P, const double* in, double* out, int nco
     k_circ_os<10, 128, 6><<<grid, 128, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
   else if (logm == 10)
     k_circ_os<10, 128><<<grid, 128, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
-  else {
+  else if (os16) {
+    // M = 2048 (cfg5): register-pass variant (k_circ_os16), 128 threads
+    const char* e2 = getenv("EDAK_CIRC_OS16_MINB");
+    const int m2 = e2 ? atoi(e2) : 4;
+    if (m2 == 3)
+      k_circ_os16<11, 3><<<grid, 128, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
+    else
+      k_circ_os16<11, 4><<<grid, 128, 0, st>>>(n, L, V, ncols, T, H, in, out, ident, zadd, dotp, dtiles);
+  } else {
     // M = 2048 (cfg5): 166 registers at one CTA per SM left 8 warps per SM to
     // hide every load and barrier; 3 resident CTAs (80 registers): 435 ->
     // 321 us per 128 columns (A/B knob EDAK_CIRC_OS2_MINB)

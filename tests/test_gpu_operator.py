@@ -350,3 +350,35 @@ def test_overlap_save_factor_equals_taps(gpu, monkeypatch):
         assert float((hz - hz2).abs().max()) <= 1e-13 * float(hz.abs().max()), n
         assert torch.allclose(dp.sum(1), (z * hz).sum(1), rtol=1e-13)
         assert torch.allclose(dp2.sum(1), (z * hz2).sum(1), rtol=1e-13)
+
+
+@pytest.mark.parametrize("n,nc,L,logm", [(262144, 7, 32.0, 11), (99999, 2, 32.0, 11), (16400, 1, 32.0, 11),
+                                         (16384, 5, 16.0, 10), (8190, 3, 8.0, 10), (5001, 2, 16.0, 10)])
+def test_overlap_save_register_passes(gpu, monkeypatch, n, nc, L, logm):
+    """The 1024- and 2048-point overlap-save U_B as three register passes per
+    direction (k_circ_os16, the default) against the shared-memory
+    radix-2/8 kernel (EDAK_CIRC_OS16=0) and numpy: same spectrum table,
+    same bit-reversed order, outputs and the I + A epilogue's p.Hp partials
+    to 1e-14."""
+    from paper_2605_23571_b200.assim import Linearization
+    from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
+    op = _oracle_problem(n, 2, 8, 2, L, 29)
+    ub = CirculantFactor(n, op.ub.symbol)
+    lin = Linearization(op.traj.states[None], 0.025, 8.0, op.net, ub, DiagonalNoise(1.0))
+    assert lin.dfac.os_logm == logm
+    z = torch.randn(nc, n, dtype=torch.float64, device="cuda")
+    new = lin.dfac.apply_cols(z)
+    tiles = lin.dot_tiles()
+    dp = torch.full((nc, tiles), float("nan"), dtype=torch.float64, device="cuda")
+    hz = lin.hessian_cols(z, None, 1.0, None, None, None, dp)
+    monkeypatch.setenv("EDAK_CIRC_OS16", "0")
+    old = lin.dfac.apply_cols(z)
+    dp2 = torch.full_like(dp, float("nan"))
+    hz2 = lin.hessian_cols(z, None, 1.0, None, None, None, dp2)
+    ref = np.fft.irfft(np.fft.rfft(z.cpu().numpy(), axis=1) * op.ub.symbol, n=n, axis=1)
+    scale = float(old.abs().max())
+    assert float((new - old).abs().max()) <= 1e-14 * scale
+    assert np.abs(new.cpu().numpy() - ref).max() <= 1e-14 * np.abs(ref).max()
+    assert float((hz - hz2).abs().max()) <= 1e-13 * float(hz.abs().max())
+    assert torch.allclose(dp.sum(1), (z * hz).sum(1), rtol=1e-13)
+    assert torch.allclose(dp, dp2, rtol=1e-12, atol=1e-12 * float(dp.abs().max()))
