@@ -81,17 +81,22 @@ def test_potrf_paths(gpu):
     assert potrf_shifted(Z, 2, 0.0)[2].cpu().tolist()[1] == 1
 
 
-@pytest.mark.parametrize("kind", ["auto", "single", "cluster"])
-@pytest.mark.parametrize("rows,cols", [(10, 10), (64, 64), (1024, 64), (128, 128), (50, 40), (200, 50)])
+@pytest.mark.parametrize("kind", ["auto", "single", "cluster", "colcluster"])
+@pytest.mark.parametrize("rows,cols", [(10, 10), (64, 64), (1024, 64), (128, 128), (50, 40), (200, 50),
+                                       (120, 100)])
 def test_svd_jacobi(gpu, rows, cols, kind, monkeypatch):
     """Shared-memory single-CTA, register one-CTA (auto for small l) and
-    8-CTA cluster Jacobi (both register kernels carry V as the tail of each
-    extended column when rows + cols fits)."""
+    8-CTA cluster Jacobi -- over blocks of columns (the default from 32
+    columns, zero-padded to 16 even blocks) or over single columns
+    (EDAK_JACOBI_BLOCK=0) -- all carrying V as the tail of each extended
+    column when rows + cols fits."""
     from paper_2605_23571_b200.linalg import svd_jacobi
     if kind == "single":
         monkeypatch.setenv("EDAK_JACOBI_SINGLE", "1")
-    if kind == "cluster":
+    if kind in ("cluster", "colcluster"):
         monkeypatch.setenv("EDAK_JACOBI_CLUSTER", "1")
+    if kind == "colcluster":
+        monkeypatch.setenv("EDAK_JACOBI_BLOCK", "0")
     rng = np.random.default_rng(rows + cols)
     m = rng.standard_normal((rows, cols)) * np.logspace(0, -6, cols)
     U, sig, V = svd_jacobi(torch.tensor(m.T.copy(), device="cuda"), want_v=True)
@@ -104,14 +109,17 @@ def test_svd_jacobi(gpu, rows, cols, kind, monkeypatch):
     npt.assert_allclose(v.T @ v, np.eye(cols), atol=1e-12)
 
 
-@pytest.mark.parametrize("kind", ["auto", "cluster"])
+@pytest.mark.parametrize("kind", ["auto", "cluster", "colcluster"])
 def test_svd_jacobi_256_no_v(gpu, kind, monkeypatch):
     """The cfg5 route of the Nystrom stage: l = 256, T = R_Y C^-1 square,
-    left vectors only (8-CTA cluster kernel, jacobi_cluster.cu): singular
+    left vectors only (8-CTA cluster kernels, jacobi_cluster.cu: blocks of
+    16 columns, or single columns with EDAK_JACOBI_BLOCK=0): singular
     values vs LAPACK, U orthonormal, U^T T has orthogonal rows of norm sig."""
     from paper_2605_23571_b200.linalg import svd_jacobi
-    if kind == "cluster":
+    if kind in ("cluster", "colcluster"):
         monkeypatch.setenv("EDAK_JACOBI_CLUSTER", "1")
+    if kind == "colcluster":
+        monkeypatch.setenv("EDAK_JACOBI_BLOCK", "0")
     rng = np.random.default_rng(256)
     q1, _ = np.linalg.qr(rng.standard_normal((256, 256)))
     q2, _ = np.linalg.qr(rng.standard_normal((256, 256)))

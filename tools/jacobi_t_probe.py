@@ -1,0 +1,45 @@
+"""Sweeps and time of the cluster Jacobi variants on the Nystrom T of a
+config (CFG env, default 4): column tournament vs block tournament."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2605_23571_b200 import _lib, build, linalg, nystrom  # noqa: E402
+
+build.build()
+from paper_2605_23571_b200.engine import EdaPass  # noqa: E402
+from paper_2605_23571_b200.twin import BASELINE_CONFIGS, build_ensemble  # noqa: E402
+
+cfg = BASELINE_CONFIGS[int(os.environ.get("CFG", "4"))]
+eng = EdaPass(build_ensemble(cfg))
+saved = []
+orig = nystrom.svd_jacobi
+
+
+def grab(M, want_v=False):
+    saved.append(M.clone())
+    return orig(M, want_v)
+
+
+nystrom.svd_jacobi = grab
+eng.build_lmp(eng.rhs())
+nystrom.svd_jacobi = orig
+T = saved[0]
+cols, rows = T.shape
+ref = np.linalg.svd(T.cpu().numpy().T, compute_uv=False)
+for variant in ("1", "0"):
+    os.environ["EDAK_JACOBI_BLOCK"] = variant
+    ts = []
+    for _ in range(4):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        U, sig, _ = linalg.svd_jacobi(T)
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    err = np.max(np.abs(sig.cpu().numpy() - ref) / ref[0])
+    print(f"{cfg.name} T {rows}x{cols} block={variant}: {np.median(ts):.3f} ms, "
+          f"{linalg.last_svd_sweeps()} sweeps, max sigma err {err:.1e}")
