@@ -62,7 +62,7 @@ def potrf_shifted(W, mode, scale=0.0):
 BLOCK_L = 128  # the register-resident Cholesky-inverse kernel's limit
 
 
-def _chol_inv_2x2(W):
+def _chol_inv_2x2(W, defer=False):
     """Unshifted upper Cholesky W = C^T C and C^-1 of a 129..256 Gram as a
     2 x 2 block factorisation over the register kernel (l <= 128) and DMMA
     GEMMs (dpotrf's blocked right-looking order):
@@ -71,7 +71,8 @@ def _chol_inv_2x2(W):
     Returns (C, C^-1, nu = 0, info) or None when a pivot broke down (the
     caller then runs the single-kernel factorisation with its shift
     schedule from the start, nystrom.py:67-93).  One host read of the two
-    breakdown flags."""
+    breakdown flags -- or, with ``defer``, none: the factors are returned
+    whatever happened and info[1] != 0 flags a breakdown on the device."""
     l, h = W.shape[0], BLOCK_L
     m = l - h
     W11, W12, W22 = W[:h, :h].contiguous(), W[h:, :h].contiguous(), W[h:, h:].contiguous()
@@ -79,7 +80,7 @@ def _chol_inv_2x2(W):
     C12 = gemm_tn(C11i, W12)                      # C11^-T W12 (h x m): block (m, h)
     S = W22 - gemm_tn(C12, C12)                   # W22 - C12^T C12
     C22, C22i, _, info2 = chol_inv(S.contiguous(), 0)
-    if int(info1[1]) or int(info2[1]):
+    if not defer and (int(info1[1]) or int(info2[1])):
         return None
     X = gemm_nn(C11i, gemm_nn(C12, C22i))          # C11^-1 C12 C22^-1 (h x m): block (m, h)
     C = torch.zeros_like(W)
@@ -87,20 +88,28 @@ def _chol_inv_2x2(W):
     C[:h, :h], C[h:, :h], C[h:, h:] = C11, C12, C22
     Ci[:h, :h], Ci[h:, :h], Ci[h:, h:] = C11i, -X, C22i
     nu = torch.zeros(1, dtype=torch.float64, device=W.device)
-    info = torch.zeros(2, dtype=torch.int32, device=W.device)
+    info = torch.maximum(info1, info2) if defer else torch.zeros(2, dtype=torch.int32, device=W.device)
     return C, Ci, nu, info
 
 
-def chol_inv(W, mode, scale=0.0, want_inv=True):
+def chol_blocked(l):
+    """True when chol_inv factors an l x l Gram by the 2 x 2 block path."""
+    import os
+    return BLOCK_L < l <= 2 * BLOCK_L and os.environ.get("EDAK_CHOL_BLOCKED", "1") != "0"
+
+
+def chol_inv(W, mode, scale=0.0, want_inv=True, defer=False, single=False):
     """Fused blocked Cholesky + inverse (edak_chol_inv): (C, C^-1 or None,
     nu tensor[1], info int32[2]) with potrf_shifted's schedule -- no host
     sync (except for 129..256 Grams: the 2 x 2 block path, see
-    _chol_inv_2x2, reads its breakdown flags once)."""
-    import os
+    _chol_inv_2x2, reads its breakdown flags once).  ``defer``: no host
+    read on the 2 x 2 path either; its breakdown shows in info[1] and, for
+    a shifted mode, the caller re-runs with ``single`` (the one-kernel
+    factorisation with the shift schedule)."""
     W = W.contiguous()
     l = W.shape[0]
-    if BLOCK_L < l <= 2 * BLOCK_L and os.environ.get("EDAK_CHOL_BLOCKED", "1") != "0":
-        r = _chol_inv_2x2(W)
+    if chol_blocked(l) and not single:
+        r = _chol_inv_2x2(W, defer=defer)
         if r is not None:
             return r[0], (r[1] if want_inv else None), r[2], r[3]
     Cm = torch.empty_like(W)

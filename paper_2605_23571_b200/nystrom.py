@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _dev
-from .linalg import chol_inv, col_dots, gemm_nn, gemm_tn, svd_jacobi
+from .linalg import chol_blocked, chol_inv, col_dots, gemm_nn, gemm_tn, svd_jacobi
 
 SHIFT_MODES = (None, "trace", "ynorm")
 _MODE_CODE = {None: 0, "trace": 1, "ynorm": 2}
@@ -150,7 +150,7 @@ ORTHO_TOL = 0.1   # ||R_k - I||_F below which the pass's input basis counts as o
 MAX_PLAIN = 4     # unshifted CholeskyQR passes before the shifted CholeskyQR3 takes over
 
 
-def _cholqr_lazy(Y):
+def _cholqr_lazy(Y, extra=()):
     """Y = Q_Y R_Y with Q_Y = Qp Ti and R_Y = R, for blocks Qp (l, n),
     the last pass's triangular inverse Ti (l, l) and R (l, l) upper, so the
     caller forms Q_Y U only as Qp (Ti U) and never materialises Q_Y (the
@@ -165,24 +165,49 @@ def _cholqr_lazy(Y):
     passes (CholeskyQR2) instead of shifted CholeskyQR3's three; a Gram that
     is not numerically SPD (cond(Y) >~ u^-1/2), or no convergence in
     MAX_PLAIN passes, falls back to the shifted CholeskyQR3 (_cholqr2).
-    One host read per pass (the breakdown flag and the deviation)."""
+
+    The first two passes run without a host read; ONE read then fetches
+    their breakdown flags, the deviation of R_2 and the ``extra`` device
+    tensors (returned as a host array).  Returns (qr or None, extra)."""
     l = Y.shape[0]
     eye = torch.eye(l, dtype=Y.dtype, device=Y.device)
-    Q, R = Y, None
-    for _ in range(MAX_PLAIN):
-        Rk, Rki, _, info = chol_inv(gemm_tn(Q, Q), 0)
-        dev = torch.linalg.matrix_norm(Rk - eye)
-        chk = torch.cat([info.to(torch.float64), dev.view(1)]).cpu().numpy()
-        if chk[1] or not np.isfinite(chk[2]):
-            break
-        R = Rk if R is None else gemm_nn(Rk, R)  # upper R_k ... R_1
-        if chk[2] <= ORTHO_TOL and Q is not Y:
-            return Q, Rki, R
-        Q = gemm_nn(Q, Rki)
+    R1, R1i, _, i1 = chol_inv(gemm_tn(Y, Y), 0, defer=True)
+    Q1 = gemm_nn(Y, R1i)
+    R2, R2i, _, i2 = chol_inv(gemm_tn(Q1, Q1), 0, defer=True)
+    dev = torch.linalg.matrix_norm(R2 - eye)
+    chk = torch.cat([i1.to(torch.float64), i2.to(torch.float64), dev.view(1)]
+                    + [e.to(torch.float64).reshape(-1) for e in extra]).cpu().numpy()
+    host = chk[5:]
+    ok = not chk[1] and not chk[3] and np.isfinite(chk[4])
+    if ok:
+        R = gemm_nn(R2, R1)  # upper R_2 R_1
+        if chk[4] <= ORTHO_TOL:
+            return (Q1, R2i, R), host
+        Q = gemm_nn(Q1, R2i)
+        for _ in range(MAX_PLAIN - 2):
+            Rk, Rki, _, info = chol_inv(gemm_tn(Q, Q), 0)
+            dk = torch.linalg.matrix_norm(Rk - eye)
+            c = torch.cat([info.to(torch.float64), dk.view(1)]).cpu().numpy()
+            if c[1] or not np.isfinite(c[2]):
+                break
+            R = gemm_nn(Rk, R)
+            if c[2] <= ORTHO_TOL:
+                return (Q, Rki, R), host
+            Q = gemm_nn(Q, Rki)
     qr = _cholqr2(Y)
     if qr is None:
-        return None
-    return qr[0], eye, qr[1]
+        return None, host
+    return (qr[0], eye, qr[1]), host
+
+
+_SIDE = {}
+
+
+def _side_stream():
+    dev = torch.cuda.current_device()
+    if dev not in _SIDE:
+        _SIDE[dev] = torch.cuda.Stream()
+    return _SIDE[dev]
 
 
 def _use_qr(n, ell):
@@ -219,27 +244,51 @@ def nystrom_evd(a_apply, sketch, cfg):
     if ell != cfg.ell:
         raise ValueError(f"sketch has {ell} columns, cfg.ell={cfg.ell}")
     Y = _apply_block(a_apply, phi, n)
-    _check_rank(Y)
+    if cfg.q > 1:
+        _check_rank(Y)
     for _ in range(cfg.q - 1):
         phi = _orthobasis(Y)
         Y = _apply_block(a_apply, phi, n)
         _check_rank(Y)
-    W = gemm_tn(phi, Y)  # block (l, l): W[a][b] = phi_a . y_b
     mode = _MODE_CODE[cfg.shift_mode]
     scale = 0.0
     if cfg.shift_mode == "ynorm":
         scale = float(torch.sqrt(col_dots(Y, Y).sum()))
-    Cm, Cinv, nu, info = chol_inv(W, mode, scale)
-    info = info.cpu().numpy()
+    k_eff = min(cfg.k, ell, n)
+    ydots = col_dots(Y, Y)  # the rank check (nystrom.py:136-140), read with the QR flags
+    use_qr = _use_qr(n, ell)
+    # W = Phi^T Y and its shifted Cholesky (nystrom.py:125-127) on a side
+    # stream, overlapping the CholeskyQR passes of Y on the main stream
+    main = torch.cuda.current_stream()
+    side = _side_stream() if use_qr else main
+    ready = torch.cuda.Event()
+    ready.record(main)
+    with torch.cuda.stream(side):
+        side.wait_event(ready)
+        W = gemm_tn(phi, Y)  # block (l, l): W[a][b] = phi_a . y_b
+        Cm, Cinv, nu, winfo = chol_inv(W, mode, scale, defer=True)
+        wdone = torch.cuda.Event()
+        wdone.record(side)
+    main.wait_event(wdone)
+    if use_qr:
+        qr, host = _cholqr_lazy(Y, extra=(ydots, winfo, nu))
+    else:
+        qr, host = None, torch.cat([ydots, winfo.to(torch.float64), nu]).cpu().numpy()
+    dead = np.flatnonzero(host[:ell] == 0.0)
+    if dead.size:
+        raise NystromBreakdownError(f"sketch column {dead[0]} was annihilated by the operator")
+    info, shift = host[ell:ell + 2], float(host[ell + 2])
+    if info[1] and chol_blocked(ell) and mode != 0:
+        # the deferred 2 x 2 block factorisation broke down: the one-kernel
+        # factorisation with the reference's shift schedule from the start
+        Cm, Cinv, nu, winfo = chol_inv(W, mode, scale, single=True)
+        info, shift = winfo.cpu().numpy(), float(nu[0])
     if info[1]:
         if info[0] <= 1:
             raise NystromBreakdownError(
                 "Cholesky of the sketched Gram matrix broke down and no "
                 "usable shift is available")
         raise NystromBreakdownError("sketched Gram matrix stayed indefinite after shifting")
-    shift = float(nu[0])
-    k_eff = min(cfg.k, ell, n)
-    qr = _cholqr_lazy(Y) if _use_qr(n, ell) else None
     if qr is not None:
         Qp, Ti, R = qr
         T = gemm_nn(R, Cinv)                 # R_Y C^-1 (l x l)
