@@ -285,7 +285,7 @@ def cpu_description(kind, cores, iters, cfg, busy, per_step=False):
 
 # ------------------------------------------------------------ GPU leg -----
 NCU_FILE = os.path.join(ROOT, "profiles", "r2_sweep_ncu.json")
-SWEEP_SOURCES = ("l96.cu", "sweep.cuh", "common.cuh")
+SWEEP_SOURCES = ("l96.cu", "sweep_tile.cu", "sweep.cuh", "common.cuh")
 
 
 def sweep_sources_sha():
