@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
   const int G = P.G;
   const double* fc = forcing + (size_t)col * G * P.T;
   const double dt = P.dt, h = 0.5 * dt, F = P.forcing;
-  const double c6 = dt / 6.0, c3 = 2.0 * dt / 6.0, s2 = P.sigma2;
+  const double c6 = dt / 6.0, s2 = P.sigma2;
   int buf = 0;
 
   // forcing w_all[level] at own elements: R^-1 d at observed points

@@ -305,9 +305,15 @@ bool lmp_nn_ok(int M) {
 }
 
 // 148 CTAs (one per SM) over the tiles, fewer for short rings
+// (EDAK_LMP_TN_CTAS: another CTA budget, A/B)
+static int tn_ctas() {
+  const char* e = getenv("EDAK_LMP_TN_CTAS");
+  const int v = e ? atoi(e) : 148;
+  return v >= 1 ? v : 148;
+}
 static int tn_splits(int64_t n, int tiles) {
   const int64_t nch = (n + 15) / 16;
-  int s = 148 / tiles;
+  int s = tn_ctas() / tiles;
   if (s < 1) s = 1;
   return (int)(nch < s ? nch : s);
 }

@@ -691,3 +691,53 @@ def test_lmp_apply_member_tiles(gpu, n, k, ncols):
               work.data_ptr(), _lib.stream())
     ref = R + ((R @ S.t()) * coef) @ S
     assert torch.allclose(Z, ref, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("cond", [1e2, 1e6, 1e9])
+def test_cholqr_lazy_paths(gpu, cond):
+    """The Nystrom stage's CholeskyQR (nystrom._cholqr_lazy): two unshifted
+    passes with the last triangular solve left to the caller for a
+    well-conditioned sketch, more passes / the shifted CholeskyQR3 for an
+    ill-conditioned one; Q_Y = Qp Ti orthonormal and Y = Q_Y R_Y to the
+    level of Householder QR (nystrom.py:118) in every case."""
+    from paper_2605_23571_b200.linalg import gemm_nn
+    from paper_2605_23571_b200.nystrom import _cholqr_lazy
+    rng = np.random.default_rng(int(np.log10(cond)))
+    n, l = 8192, 64
+    U, _ = np.linalg.qr(rng.standard_normal((n, l)))
+    V, _ = np.linalg.qr(rng.standard_normal((l, l)))
+    Y = (U * np.logspace(0, -np.log10(cond), l)) @ V.T
+    Yd = torch.tensor(np.ascontiguousarray(Y.T), device="cuda")  # block (l, n)
+    qr, _ = _cholqr_lazy(Yd)
+    Qp, Ti, R = qr
+    Q = gemm_nn(Qp, Ti).cpu().numpy().T   # (n, l)
+    Rm = R.cpu().numpy().T                # upper (l, l)
+    assert np.abs(Q.T @ Q - np.eye(l)).max() <= 1e-13
+    assert np.linalg.norm(Y - Q @ Rm) <= 1e-14 * np.linalg.norm(Y) * l
+    assert np.abs(np.tril(Rm, -1)).max() == 0.0
+    if cond <= 1e6:  # CholeskyQR2: the second pass's inverse is left to the caller
+        assert not torch.equal(Ti, torch.eye(l, dtype=Ti.dtype, device=Ti.device))
+
+
+def test_nystrom_blocked_gram_shift(gpu):
+    """l = 160 (the 2 x 2 block Cholesky of 129..256 Grams, deferred on a
+    side stream) on a rank-100 operator: the sketched Gram is singular, the
+    unshifted block factorisation breaks down and the one-kernel
+    factorisation with the reference's shift schedule (nystrom.py:67-93)
+    takes over -- same shift as the oracle, Ritz values to its envelope."""
+    from paper_2605_23571_b200.nystrom import NystromConfig, nystrom_evd
+    rng = np.random.default_rng(160)
+    n, r, l, k = 2048, 100, 160, 64
+    Vr, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    lam = np.logspace(2, -1, r)
+
+    def a_apply(z):
+        return Vr @ (lam[:, None] * (Vr.T @ z)) if z.ndim == 2 else Vr @ (lam * (Vr.T @ z))
+
+    phi = rng.standard_normal((n, l))
+    approx = nystrom_evd(a_apply, phi, NystromConfig(l, k, shift_mode="trace"))
+    ref = oalg.nystrom_evd(a_apply, phi, oalg.NystromConfig(l, k, shift_mode="trace"))
+    assert ref.shift > 0.0
+    assert approx.shift == pytest.approx(ref.shift, rel=1e-12)
+    big = ref.values >= 1e-6 * ref.values[0]
+    npt.assert_allclose(approx.values[big], ref.values[big], rtol=1e-9)

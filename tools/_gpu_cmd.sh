@@ -1,4 +1,3 @@
 mkdir -p gpurun_out/it
 O=gpurun_out/it
-CFG=4 python tools/ab_knobs.py "EDAK_X2=0" "EDAK_X2=2" "EDAK_X2=3" > $O/ab_x2_4.txt 2>&1
-CFG=5 python tools/ab_knobs.py "EDAK_X2=0" "EDAK_X2=2" > $O/ab_x2_5.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_solvers.py -m gpu -q -x -p no:cacheprovider -k "cholqr_lazy or blocked_gram or nystrom" > $O/newtests.log 2>&1; echo rc=$? >> $O/newtests.log

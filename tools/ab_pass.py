@@ -35,6 +35,7 @@ for rnd in range(2):
             if kv:
                 a, b = kv.split("=", 1)
                 os.environ[a] = b
+        eng.members.__dict__.pop("_pcg_graphs", None)  # re-capture under this variant
         r = eng.run()
         torch.cuda.synchronize()
         x = r.x.cpu().numpy()
