@@ -407,32 +407,25 @@ __device__ __forceinline__ void load_tw(double2 (&tw)[K], const double2* __restr
 // [LOGM - 4, LOGM) (one group per thread), pass B = radix-2^KB over bits
 // [3, LOGM - 4) (KB = 4 at M = 2048: one group per thread; KB = 3 at M =
 // 1024: two), pass C = radix-8 over bits [0, 3) (two groups per thread).
-template <int LOGM, int MINB>
-__global__ void __launch_bounds__((1 << LOGM) / 16, MINB)
-    k_circ_os16(int n, int L, int V, int ncols, const double2* __restrict__ T, const double2* __restrict__ H,
-                const double* __restrict__ in, double* __restrict__ out, double ident,
-                const double* __restrict__ zadd, double* __restrict__ dotp, int dtiles) {
+// The transform and epilogue of one item (block blk of the column pair
+// (ca, ca + 1)) whose pass-A input a[m] = window element t + NT m is in
+// registers; nb = blocks per column (the dot-partial slots past it get 0).
+template <int LOGM>
+__device__ __forceinline__ void os16_item(double2 (&a)[16], double2* Z, double (*red)[(1 << LOGM) / 16 / 32 > 0
+                                                                                   ? (1 << LOGM) / 16 / 32
+                                                                                   : 1],
+                                          const double2* __restrict__ T, const double2* __restrict__ H, int n,
+                                          int L, int V, int ncols, int blk, int ca, int nb,
+                                          double* __restrict__ out, double ident, const double* __restrict__ zadd,
+                                          double* __restrict__ dotp, int dtiles) {
   using namespace os16;
   static_assert(LOGM == 10 || LOGM == 11, "passes: [LOGM-4, LOGM) [3, LOGM-4) [0, 3)");
   constexpr int M = 1 << LOGM, NT = M / 16;
   constexpr int BA = LOGM - 4, BB = 3, KB = LOGM - 7;  // pass A / B bit offsets, pass B radix log2
   constexpr int GB = 16 >> KB;                         // pass-B groups per thread
-  __shared__ __align__(16) double2 Z[M + M / 8];
-  __shared__ double red[2][NT / 32 > 0 ? NT / 32 : 1];
-  const int t = threadIdx.x, blk = blockIdx.x;
-  const int ca = 2 * blockIdx.y, cb = ca + 1;
+  const int t = threadIdx.x, cb = ca + 1;
   const bool hb = cb < ncols;
   const int i0 = blk * V;
-  const double* A = in + (size_t)ca * n;
-  const double* B = in + (size_t)(hb ? cb : ca) * n;
-  // pass A: elements t + NT m of the window [i0 - L, i0 - L + M), from HBM
-  double2 a[16];
-#pragma unroll
-  for (int m = 0; m < 16; ++m) {
-    int g = i0 - L + t + NT * m;
-    g = g < 0 ? g + n : (g >= n ? g - n : g);
-    a[m] = make_double2(__ldg(A + g), hb ? __ldg(B + g) : 0.0);
-  }
   double2 tw[4], twb[KB];
   load_tw<M, 4>(tw, T, t, LOGM - 1 - BA);
   dif<4, true>(a, tw);
@@ -531,12 +524,39 @@ __global__ void __launch_bounds__((1 << LOGM) / 16, MINB)
       dotp[(size_t)(ca + t) * dtiles + blk] = s;
     }
     if (blk == 0) {
-      for (int q = (int)gridDim.x + t; q < dtiles; q += NT) {
+      for (int q = nb + t; q < dtiles; q += NT) {
         dotp[(size_t)ca * dtiles + q] = 0.0;
         if (hb) dotp[(size_t)cb * dtiles + q] = 0.0;
       }
     }
   }
+}
+
+
+// one item per CTA, the window straight from HBM into registers
+template <int LOGM, int MINB>
+__global__ void __launch_bounds__((1 << LOGM) / 16, MINB)
+    k_circ_os16(int n, int L, int V, int ncols, const double2* __restrict__ T, const double2* __restrict__ H,
+                const double* __restrict__ in, double* __restrict__ out, double ident,
+                const double* __restrict__ zadd, double* __restrict__ dotp, int dtiles) {
+  constexpr int M = 1 << LOGM, NT = M / 16;
+  __shared__ __align__(16) double2 Z[M + M / 8];
+  __shared__ double red[2][NT / 32 > 0 ? NT / 32 : 1];
+  const int t = threadIdx.x, blk = blockIdx.x;
+  const int ca = 2 * blockIdx.y, cb = ca + 1;
+  const bool hb = cb < ncols;
+  const int i0 = blk * V;
+  const double* A = in + (size_t)ca * n;
+  const double* B = in + (size_t)(hb ? cb : ca) * n;
+  // pass A: elements t + NT m of the window [i0 - L, i0 - L + M), from HBM
+  double2 a[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    int g = i0 - L + t + NT * m;
+    g = g < 0 ? g + n : (g >= n ? g - n : g);
+    a[m] = make_double2(__ldg(A + g), hb ? __ldg(B + g) : 0.0);
+  }
+  os16_item<LOGM>(a, Z, red, T, H, n, L, V, ncols, blk, ca, (int)gridDim.x, out, ident, zadd, dotp, dtiles);
 }
 
 // U_B by overlap-save when the problem carries the block spectrum
