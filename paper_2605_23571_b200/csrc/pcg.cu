@@ -40,24 +40,36 @@ __global__ void __launch_bounds__(PCG_NT) k_dot_partial(int n, int T, const doub
   if (threadIdx.x == 0) part[(size_t)c * T + t] = s;
 }
 
-__global__ void __launch_bounds__(PCG_NT) k_pcg_init(int n, const double* __restrict__ b,
-                                                     const double* __restrict__ z, double* __restrict__ x,
-                                                     double* __restrict__ r, double* __restrict__ p,
-                                                     double* __restrict__ rzb, double* __restrict__ hist_rz,
-                                                     int hist_ld, int32_t* __restrict__ status,
-                                                     int32_t* __restrict__ iters) {
+// one CTA of 1024 threads per member; each thread keeps four independent
+// partial dots (the loads of four strides in flight: a 256-thread loop with
+// one chain was latency-bound, 0.5 ms for cfg5's 256 members), combined in
+// a fixed order, then the fixed-order block tree
+constexpr int PCG_INIT_NT = 1024;
+__global__ void __launch_bounds__(PCG_INIT_NT) k_pcg_init(int n, const double* __restrict__ b,
+                                                          const double* __restrict__ z, double* __restrict__ x,
+                                                          double* __restrict__ r, double* __restrict__ p,
+                                                          double* __restrict__ rzb, double* __restrict__ hist_rz,
+                                                          int hist_ld, int32_t* __restrict__ status,
+                                                          int32_t* __restrict__ iters) {
   __shared__ double sh[32];
   const int c = blockIdx.x;
   const size_t o = (size_t)c * n;
-  double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += PCG_NT) {
-    const double bi = b[o + i], zi = z[o + i];
-    x[o + i] = 0.0;
-    r[o + i] = bi;
-    p[o + i] = zi;
-    s += bi * zi;
+  double s4[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int i0 = threadIdx.x; i0 < n; i0 += 4 * PCG_INIT_NT) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * PCG_INIT_NT;
+      if (i < n) {
+        const double bi = b[o + i], zi = z[o + i];
+        x[o + i] = 0.0;
+        r[o + i] = bi;
+        p[o + i] = zi;
+        s4[u] += bi * zi;
+      }
+    }
   }
-  s = block_sum<PCG_NT>(s, sh);
+  double s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  s = block_sum<PCG_INIT_NT>(s, sh);
   if (threadIdx.x == 0) {
     rzb[c] = s;  // buffer 0 = iteration 0
     hist_rz[(size_t)c * hist_ld] = s;
@@ -198,18 +210,26 @@ __global__ void __launch_bounds__(PCG_NT) k_pcg_upd_p(int n, int T, int M, const
   for (int i = i0 + threadIdx.x; i < i1; i += PCG_NT) p[o + i] = z[o + i] + beta * p[o + i];
 }
 
-// initial cost J(0) = 1/2 d.R^-1 d  (misfit = -d, assim.py:81-82)
-__global__ void __launch_bounds__(PCG_NT) k_pcg_cost0(int np_obs, const double* __restrict__ d, double sigma2,
-                                                      double* __restrict__ hist_J, int hist_ld) {
+// initial cost J(0) = 1/2 d.R^-1 d  (misfit = -d, assim.py:81-82); one
+// 1024-thread CTA per member with four partial sums per thread, as k_pcg_init
+__global__ void __launch_bounds__(PCG_INIT_NT) k_pcg_cost0(int np_obs, const double* __restrict__ d, double sigma2,
+                                                           double* __restrict__ hist_J, int hist_ld) {
   __shared__ double sh[32];
   const int c = blockIdx.x;
   const size_t q0 = (size_t)c * np_obs;
-  double mm = 0.0;
-  for (int q = threadIdx.x; q < np_obs; q += PCG_NT) {
-    const double e = -d[q0 + q];
-    mm += e * (e / sigma2);
+  double m4[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int b0 = threadIdx.x; b0 < np_obs; b0 += 4 * PCG_INIT_NT) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = b0 + u * PCG_INIT_NT;
+      if (q < np_obs) {
+        const double e = -d[q0 + q];
+        m4[u] += e * (e / sigma2);
+      }
+    }
   }
-  mm = block_sum<PCG_NT>(mm, sh);
+  double mm = (m4[0] + m4[1]) + (m4[2] + m4[3]);
+  mm = block_sum<PCG_INIT_NT>(mm, sh);
   if (threadIdx.x == 0) hist_J[(size_t)c * hist_ld] = 0.5 * mm;
 }
 
@@ -219,7 +239,7 @@ int64_t pcg_work_doubles(int n, int M) { return 4LL * M * pcg_tiles(n) + 3LL * M
 int launch_pcg_init(int n, int M, const double* b, const double* z, double* x, double* r, double* p, double* work,
                     double* hist_rz, int hist_ld, int32_t* status, int32_t* iters, cudaStream_t st) {
   double* rzb = work + 4LL * M * pcg_tiles(n);
-  k_pcg_init<<<M, PCG_NT, 0, st>>>(n, b, z, x, r, p, rzb, hist_rz, hist_ld, status, iters);
+  k_pcg_init<<<M, PCG_INIT_NT, 0, st>>>(n, b, z, x, r, p, rzb, hist_rz, hist_ld, status, iters);
   count_launch();
   return check_launch("k_pcg_init");
 }
@@ -356,7 +376,7 @@ int launch_pcg_beta(int n, int M, const double* z, const double* r, double* p, d
 
 int launch_pcg_cost0(int np_obs, int ncols, const double* d, double sigma2, double* hist_J, int hist_ld,
                      cudaStream_t st) {
-  k_pcg_cost0<<<ncols, PCG_NT, 0, st>>>(np_obs, d, sigma2, hist_J, hist_ld);
+  k_pcg_cost0<<<ncols, PCG_INIT_NT, 0, st>>>(np_obs, d, sigma2, hist_J, hist_ld);
   count_launch();
   return check_launch("k_pcg_cost0");
 }
