@@ -293,8 +293,18 @@ __global__ void __launch_bounds__(1024) k_pcg_reduce_rz(int T, int M, int k, con
     double s = 0.0;
     if (i < k) {
       const double* pp = part + i + (size_t)c * k;
-#pragma unroll 4
-      for (int z = g; z < nsplit; z += 8) s += pp[(size_t)z * tot];
+      // up to 19 partials per thread (148 splits / 8 groups): all of their
+      // loads in flight before the (fixed-order) sum -- the reduction was
+      // load-latency bound with four in flight
+      double v[19];
+#pragma unroll
+      for (int u = 0; u < 19; ++u) {
+        const int z = g + 8 * u;
+        v[u] = z < nsplit ? pp[(size_t)z * tot] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 19; ++u) s += v[u];
+      for (int z = g + 8 * 19; z < nsplit; z += 8) s += pp[(size_t)z * tot];
     }
     gs[g][e] = s;
     __syncthreads();
