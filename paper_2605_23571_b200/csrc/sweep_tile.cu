@@ -173,6 +173,17 @@ __global__ void __launch_bounds__(NT, MINB)
   const double dt = P.dt, h = 0.5 * dt, c6 = dt / 6.0, F = P.forcing;
   __syncthreads();  // mbarriers initialised before any copy or wait
 
+  // prologue staging first: X_{s0} and X_{s0+1} are in flight while the
+  // column, the grid positions and the level-0 capture load (they used to
+  // be issued after them, exposing the first load's whole latency)
+  auto stage = [&](int level, int b) {
+    const uint32_t buf = sb0 + b * TS::BUF, mb = mb0 + 8 * b;
+    if (wraps) TS::wrapped(buf, tr + (size_t)level * n, gst, n, mb);
+    else if (threadIdx.x == 0) TS::tma(buf, &tmap, tr + (size_t)level * n + gst, P.states, mb);
+  };
+  stage(s0, 0);
+  if (s0 + 1 < s1) stage(s0 + 1, 1);
+
   // window chunk [s0, s1): v enters at level s0 and leaves at level s1
   double v[C + 4];
   R.load_own(vin + (size_t)col * n, v);
@@ -192,13 +203,6 @@ __global__ void __launch_bounds__(NT, MINB)
   };
   if (s0 == 0) capture_tp(__ldg(P.tpos));
 
-  auto stage = [&](int level, int b) {
-    const uint32_t buf = sb0 + b * TS::BUF, mb = mb0 + 8 * b;
-    if (wraps) TS::wrapped(buf, tr + (size_t)level * n, gst, n, mb);
-    else if (threadIdx.x == 0) TS::tma(buf, &tmap, tr + (size_t)level * n + gst, P.states, mb);
-  };
-  stage(s0, 0);  // prologue: X_{s0}, X_{s0+1}
-  if (s0 + 1 < s1) stage(s0 + 1, 1);
 
   int xbi = 0;  // exchange buffer (double-buffered)
   R.put(&xb.v[xbi][0][0][0], v);  // v's halos for the first step's exchange
@@ -323,6 +327,17 @@ __global__ void __launch_bounds__(NT, MINB)
   const double inv_s2 = 1.0 / P.sigma2;
   __syncthreads();
 
+  // prologue staging first (X_{s1-1}, and X_{s1-2} at DEPTH 2): in flight
+  // while the grid positions, the initial forcing / g and the first
+  // forcing slots load
+  auto stage = [&](int level, int b) {
+    const uint32_t buf = sb0 + b * TS::BUF, mb = mb0 + 8 * b;
+    if (wraps) TS::wrapped(buf, tr + (size_t)level * n, gst, n, mb);
+    else if (threadIdx.x == 0) TS::tma(buf, &tmap, tr + (size_t)level * n + gst, P.states, mb);
+  };
+  stage(s1 - 1, 0);
+  if (DEPTH == 2 && s1 - 2 >= s0) stage(s1 - 2, 1);
+
   // forcing w_all[level] at own elements: R^-1 d at observed points
   // (obs.py:54-56 with covariance.py:71), 0 elsewhere
   int gp[C];
@@ -350,16 +365,9 @@ __global__ void __launch_bounds__(NT, MINB)
     }
   }
 
-  auto stage = [&](int level, int b) {
-    const uint32_t buf = sb0 + b * TS::BUF, mb = mb0 + 8 * b;
-    if (wraps) TS::wrapped(buf, tr + (size_t)level * n, gst, n, mb);
-    else if (threadIdx.x == 0) TS::tma(buf, &tmap, tr + (size_t)level * n + gst, P.states, mb);
-  };
   int tp_cur = __ldg(P.tpos + s1 - 1);
-  fetch_force(tp_cur, (s1 - 1) & 1);  // prologue: the forcing of level s1-1, X_{s1-1} (and X_{s1-2})
+  fetch_force(tp_cur, (s1 - 1) & 1);  // prologue: the forcing of level s1-1
   cp_commit();
-  stage(s1 - 1, 0);
-  if (DEPTH == 2 && s1 - 2 >= s0) stage(s1 - 2, 1);
 
   int xbi = 0;
   R.put(&xb.v[xbi][0][0][0], g);  // g's halos for the first exchange
