@@ -28,18 +28,23 @@ nystrom.svd_jacobi = grab
 eng.build_lmp(eng.rhs())
 nystrom.svd_jacobi = orig
 T = saved[0]
+want_v = T.shape[0] < 2 * 64 and cfg.n < cfg.ell  # the wide cfg2 route takes V
 cols, rows = T.shape
 ref = np.linalg.svd(T.cpu().numpy().T, compute_uv=False)
-for variant in ("1", "0"):
-    os.environ["EDAK_JACOBI_BLOCK"] = variant
+variants = os.environ.get("VARIANTS", "EDAK_JACOBI_BLOCK=1,EDAK_JACOBI_BLOCK=0").split(",")
+for variant in variants:
+    for k in ("EDAK_JACOBI_BLOCK", "EDAK_JACOBI_CLUSTER", "EDAK_JACOBI_SINGLE"):
+        os.environ.pop(k, None)
+    a, b = variant.split("=")
+    os.environ[a] = b
     ts = []
     for _ in range(4):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        U, sig, _ = linalg.svd_jacobi(T)
+        U, sig, _ = linalg.svd_jacobi(T, want_v=want_v)
         e.record()
         torch.cuda.synchronize()
         ts.append(s.elapsed_time(e))
     err = np.max(np.abs(sig.cpu().numpy() - ref) / ref[0])
-    print(f"{cfg.name} T {rows}x{cols} block={variant}: {np.median(ts):.3f} ms, "
+    print(f"{cfg.name} T {rows}x{cols} {variant}: {np.median(ts):.3f} ms, "
           f"{linalg.last_svd_sweeps()} sweeps, max sigma err {err:.1e}")
