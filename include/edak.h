@@ -88,6 +88,28 @@ int edak_integrate(int n, int n_steps, double dt, double forcing,
                    int64_t out_stride, double* stages_out, int64_t stg_stride,
                    void* stream);
 
+/* ---- model: per-vector operators (model.py:20-84) --------------------- */
+/* Blocks of ncols vectors of length n (column c at c * n), each operation
+ * IEEE-rounded in the reference's numpy order (bit-identical results).
+ * out = tendency(x, forcing)                     (model.py:20-22) */
+int edak_tendency(int n, int ncols, const double* x, double forcing, double* out,
+                  void* stream);
+/* out = tendency_tlm(x, v) = J(x) v              (model.py:25-28) */
+int edak_tendency_tlm(int n, int ncols, const double* x, const double* v,
+                      double* out, void* stream);
+/* out = tendency_adj(x, w) = J(x)^T w            (model.py:31-35) */
+int edak_tendency_adj(int n, int ncols, const double* x, const double* w,
+                      double* out, void* stream);
+/* out = y + c * z (product rounded, then the sum): the stage updates of
+ * _rk4_stages / step_tlm / step_adj (model.py:41-45, 58-61, 71-83); with
+ * y == NULL, out = c * z (the scalings of step_adj, model.py:71-74) */
+int edak_axpy_rn(int64_t len, const double* y, double c, const double* z,
+                 double* out, void* stream);
+/* out = y + c * (((a1 + 2 a2) + 2 a3) + a4)  (model.py:47, 63) */
+int edak_rk4_combine(int64_t len, const double* y, double c, const double* a1,
+                     const double* a2, const double* a3, const double* a4,
+                     double* out, void* stream);
+
 /* nonlinear observation G(x) (ObsNetwork.observe, obs.py:43-45):
  * y[c][t_pos*G+g_pos] = states[c][times[t_pos]][grid[g_pos]] */
 int edak_observe(const double* states, int64_t traj_stride, int n,

@@ -34,6 +34,11 @@ _PROTOS = {
     "edak_last_error": (C.c_char_p, []),
     "edak_launch_count": (i64, []),
     "edak_integrate": (C.c_int, [C.c_int, C.c_int, f64, f64, vp, C.c_int, vp, i64, vp, i64, vp]),
+    "edak_tendency": (C.c_int, [C.c_int, C.c_int, vp, f64, vp, vp]),
+    "edak_tendency_tlm": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, vp]),
+    "edak_tendency_adj": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, vp]),
+    "edak_axpy_rn": (C.c_int, [i64, vp, f64, vp, vp, vp]),
+    "edak_rk4_combine": (C.c_int, [i64, vp, f64, vp, vp, vp, vp, vp, vp]),
     "edak_observe": (C.c_int, [vp, i64, C.c_int, vp, C.c_int, vp, C.c_int, C.c_int, vp, vp]),
     "edak_circ_apply": (C.c_int, [C.POINTER(Problem), vp, vp, C.c_int, vp]),
     "edak_sweep_work_doubles": (i64, [C.POINTER(Problem), C.c_int]),

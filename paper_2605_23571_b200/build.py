@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libedak.so")
-SOURCES = ["capi.cu", "l96.cu", "sweep_tile.cu", "circ.cu", "circ_os.cu", "blas.cu", "lmp_gemm.cu", "small.cu", "cholinv.cu", "jacobi_cluster.cu", "pcg.cu", "pcg_small.cu", "peak.cu"]
+SOURCES = ["capi.cu", "l96.cu", "l96_ops.cu", "sweep_tile.cu", "circ.cu", "circ_os.cu", "blas.cu", "lmp_gemm.cu", "small.cu", "cholinv.cu", "jacobi_cluster.cu", "pcg.cu", "pcg_small.cu", "peak.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
          "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

@@ -50,6 +50,10 @@ int launch_gemm_nn(const double*, int64_t, const double*, int, const double*, co
 int launch_col_dots(int, int, const double*, const double*, double*, cudaStream_t);
 int launch_potrf_shifted(const double*, int, double*, int, double, double*, int32_t*, cudaStream_t);
 int launch_trinv_upper(const double*, int, double*, cudaStream_t);
+int launch_l96_tend(int op, int n, int ncols, const double* x, const double* v, double forcing, double* out,
+                    cudaStream_t st);
+int launch_l96_comb(int op, int64_t len, const double* y, double c, const double* a1, const double* a2,
+                    const double* a3, const double* a4, double* out, cudaStream_t st);
 int launch_chol_inv(const double*, int, double*, double*, int, double, double*, int32_t*, double*, cudaStream_t);
 int64_t chol_inv_work_doubles(int l);
 int64_t svd_work_doubles(int, int);
@@ -107,6 +111,37 @@ int edak_integrate(int n, int n_steps, double dt, double forcing, const double* 
   }
   return launch_integrate(n, n_steps, dt, forcing, x0, ncols, states_out, out_stride, stages_out, stg_stride,
                           as_stream(stream));
+}
+
+int edak_tendency(int n, int ncols, const double* x, double forcing, double* out, void* stream) {
+  if (ncols == 0 || n == 0) return EDAK_OK;
+  if (!x || !out || n < 3 || ncols < 0) return EDAK_EINVAL;
+  return launch_l96_tend(0, n, ncols, x, nullptr, forcing, out, as_stream(stream));
+}
+
+int edak_tendency_tlm(int n, int ncols, const double* x, const double* v, double* out, void* stream) {
+  if (ncols == 0 || n == 0) return EDAK_OK;
+  if (!x || !v || !out || n < 3 || ncols < 0) return EDAK_EINVAL;
+  return launch_l96_tend(1, n, ncols, x, v, 0.0, out, as_stream(stream));
+}
+
+int edak_tendency_adj(int n, int ncols, const double* x, const double* w, double* out, void* stream) {
+  if (ncols == 0 || n == 0) return EDAK_OK;
+  if (!x || !w || !out || n < 3 || ncols < 0) return EDAK_EINVAL;
+  return launch_l96_tend(2, n, ncols, x, w, 0.0, out, as_stream(stream));
+}
+
+int edak_axpy_rn(int64_t len, const double* y, double c, const double* z, double* out, void* stream) {
+  if (len == 0) return EDAK_OK;
+  if (!z || !out || len < 0) return EDAK_EINVAL;
+  return launch_l96_comb(y ? 0 : 2, len, y, c, z, nullptr, nullptr, nullptr, out, as_stream(stream));
+}
+
+int edak_rk4_combine(int64_t len, const double* y, double c, const double* a1, const double* a2, const double* a3,
+                     const double* a4, double* out, void* stream) {
+  if (len == 0) return EDAK_OK;
+  if (!y || !a1 || !a2 || !a3 || !a4 || !out || len < 0) return EDAK_EINVAL;
+  return launch_l96_comb(1, len, y, c, a1, a2, a3, a4, out, as_stream(stream));
 }
 
 int edak_observe(const double* states, int64_t traj_stride, int n, const int32_t* grid, int G, const int32_t* times,

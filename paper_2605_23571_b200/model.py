@@ -34,6 +34,116 @@ class Trajectory:
         return self.states.shape[1]
 
 
+# ---- per-vector operators (model.py:20-84) on the device ------------------
+# numpy (n,) in -> numpy out; device tensors (n,) or (ncols, n) -> tensors.
+# Every operation is IEEE-rounded in the reference's numpy order, so the
+# results equal the reference's bit for bit.
+
+def _vec_in(*arrays):
+    host = not isinstance(arrays[0], torch.Tensor)
+    out = []
+    for a in arrays:
+        t = torch.as_tensor(np.asarray(a, dtype=float) if host else a, dtype=torch.float64)
+        out.append(t.to(_dev.device()).contiguous())
+    return host, out
+
+
+def _vec_out(host, t):
+    return t.cpu().numpy() if host else t
+
+
+def _dims(t):
+    return (t.shape[-1], 1 if t.dim() == 1 else t.shape[0])
+
+
+def _tend(op, x, v, forcing=0.0):
+    out = torch.empty_like(x)
+    n, m = _dims(x)
+    if op == 0:
+        _lib.call("edak_tendency", n, m, x.data_ptr(), float(forcing), out.data_ptr(), _lib.stream())
+    else:
+        _lib.call("edak_tendency_tlm" if op == 1 else "edak_tendency_adj", n, m, x.data_ptr(),
+                  v.data_ptr(), out.data_ptr(), _lib.stream())
+    return out
+
+
+def _axpy(y, c, z):
+    """y + c z, or c z for y None."""
+    out = torch.empty_like(z)
+    _lib.call("edak_axpy_rn", z.numel(), _lib.ptr(y), float(c), z.data_ptr(), out.data_ptr(),
+              _lib.stream())
+    return out
+
+
+def _combine(y, c, a1, a2, a3, a4):
+    out = torch.empty_like(y)
+    _lib.call("edak_rk4_combine", y.numel(), y.data_ptr(), float(c), a1.data_ptr(), a2.data_ptr(),
+              a3.data_ptr(), a4.data_ptr(), out.data_ptr(), _lib.stream())
+    return out
+
+
+def tendency(x, forcing):
+    """Time derivative of the cyclic Lorenz-96 state (model.py:20-22)."""
+    host, (xd,) = _vec_in(x)
+    return _vec_out(host, _tend(0, xd, None, forcing))
+
+
+def tendency_tlm(x, v):
+    """J(x) v (model.py:25-28)."""
+    host, (xd, vd) = _vec_in(x, v)
+    return _vec_out(host, _tend(1, xd, vd))
+
+
+def tendency_adj(x, w):
+    """J(x)^T w (model.py:31-35)."""
+    host, (xd, wd) = _vec_in(x, w)
+    return _vec_out(host, _tend(2, xd, wd))
+
+
+def _rk4_stages(x, dt, forcing):
+    """One RK4 step: (new state, (x, x2, x3, x4)) (model.py:38-48)."""
+    host, (xd,) = _vec_in(x)
+    k1 = _tend(0, xd, None, forcing)
+    x2 = _axpy(xd, 0.5 * dt, k1)
+    k2 = _tend(0, x2, None, forcing)
+    x3 = _axpy(xd, 0.5 * dt, k2)
+    k3 = _tend(0, x3, None, forcing)
+    x4 = _axpy(xd, dt, k3)
+    k4 = _tend(0, x4, None, forcing)
+    xn = _combine(xd, dt / 6.0, k1, k2, k3, k4)
+    return _vec_out(host, xn), tuple(_vec_out(host, t) for t in (xd, x2, x3, x4))
+
+
+def step_tlm(stages, dt, v):
+    """Tangent-linear of one RK4 step around stored stages (model.py:56-63)."""
+    host, (x1, x2, x3, x4, vd) = _vec_in(*stages, v)
+    a1 = _tend(1, x1, vd)
+    a2 = _tend(1, x2, _axpy(vd, 0.5 * dt, a1))
+    a3 = _tend(1, x3, _axpy(vd, 0.5 * dt, a2))
+    a4 = _tend(1, x4, _axpy(vd, dt, a3))
+    return _vec_out(host, _combine(vd, dt / 6.0, a1, a2, a3, a4))
+
+
+def step_adj(stages, dt, w):
+    """Adjoint of step_tlm around the same stages (model.py:66-84)."""
+    host, (x1, x2, x3, x4, wd) = _vec_in(*stages, w)
+    a4 = _axpy(None, dt / 6.0, wd)
+    a3 = _axpy(None, 2.0 * dt / 6.0, wd)
+    a2 = _axpy(None, 2.0 * dt / 6.0, wd)
+    a1 = _axpy(None, dt / 6.0, wd)
+    u4 = _tend(2, x4, a4)
+    vhat = _axpy(wd, 1.0, u4)
+    a3 = _axpy(a3, dt, u4)
+    u3 = _tend(2, x3, a3)
+    vhat = _axpy(vhat, 1.0, u3)
+    a2 = _axpy(a2, 0.5 * dt, u3)
+    u2 = _tend(2, x2, a2)
+    vhat = _axpy(vhat, 1.0, u2)
+    a1 = _axpy(a1, 0.5 * dt, u2)
+    vhat = _axpy(vhat, 1.0, _tend(2, x1, a1))
+    return _vec_out(host, vhat)
+
+
 def integrate_device(x0, dt, n_steps, forcing, want_stages=False):
     """Batched nonlinear runs on the GPU.
 

@@ -382,3 +382,46 @@ def test_overlap_save_register_passes(gpu, monkeypatch, n, nc, L, logm):
     assert float((hz - hz2).abs().max()) <= 1e-13 * float(hz.abs().max())
     assert torch.allclose(dp.sum(1), (z * hz).sum(1), rtol=1e-13)
     assert torch.allclose(dp, dp2, rtol=1e-12, atol=1e-12 * float(dp.abs().max()))
+
+
+def test_model_operator_dropins_golden(gpu, ref_model):
+    """tendency / tendency_tlm / tendency_adj (model.py:20-35) on the GPU,
+    bit-identical to the reference's own outputs (golden written by the
+    reference, tests/golden/make_golden.py)."""
+    from paper_2605_23571_b200 import model as m
+    g = ref_model
+    npt.assert_array_equal(m.tendency(g["x"], 8.0), g["tend"])
+    npt.assert_array_equal(m.tendency_tlm(g["x"], g["v"]), g["tend_tl"])
+    npt.assert_array_equal(m.tendency_adj(g["x"], g["v"]), g["tend_ad"])
+    # one RK4 step and its stages: the reference's stored trajectory
+    xn, st = m._rk4_stages(g["int_states"][0], 0.025, 8.0)
+    npt.assert_array_equal(xn, g["int_states"][1])
+    for k in range(4):
+        npt.assert_array_equal(st[k], g["int_stages"][0, k])
+
+
+@pytest.mark.parametrize("n", [40, 1024, 4099])
+def test_model_step_dropins(gpu, n):
+    """step_tlm / step_adj / _rk4_stages (model.py:38-84) on the GPU,
+    bit-identical to the oracle restatement, for numpy vectors and for a
+    device block of columns; the step adjoint identity to 1e-13
+    (test_model.py:83-95)."""
+    from paper_2605_23571_b200 import model as m
+    rng = np.random.default_rng(n)
+    x = ol96.integrate(8.0 + 3.0 * rng.standard_normal(n), 0.025, 20, 8.0).states[-1]
+    v, w = rng.standard_normal(n), rng.standard_normal(n)
+    xn, st = m._rk4_stages(x, 0.025, 8.0)
+    xr, sr = ol96.rk4_stages(x, 0.025, 8.0)
+    npt.assert_array_equal(xn, xr)
+    for a, b in zip(st, sr):
+        npt.assert_array_equal(a, b)
+    tl, ad = m.step_tlm(st, 0.025, v), m.step_adj(st, 0.025, w)
+    npt.assert_array_equal(tl, ol96.step_tl(sr, 0.025, v))
+    npt.assert_array_equal(ad, ol96.step_ad(sr, 0.025, w))
+    assert abs(tl @ w - v @ ad) <= 1e-13 * abs(tl @ w)
+    # batched device block: column c equals the single-vector result
+    X = torch.tensor(np.stack([x, xr, -x]), device="cuda")
+    V = torch.tensor(np.stack([v, w, v]), device="cuda")
+    Tb = m.tendency_tlm(X, V).cpu().numpy()
+    for c in range(3):
+        npt.assert_array_equal(Tb[c], ol96.tendency_tl(X[c].cpu().numpy(), V[c].cpu().numpy()))
