@@ -89,6 +89,31 @@ class EigenApproximation:
                 f"shift={self.shift!r}, n_build_matvecs={self.n_build_matvecs})")
 
 
+def shifted_cholesky(w, mode, scale):
+    """Upper Cholesky factor of ``w``, shifted on breakdown if allowed
+    (nystrom.py:67-93): the plain factorization first, then w + nu I with
+    nu = eps * scale grown by factors of 10 (5 tries) when ``mode`` is not
+    None.  Returns ``(c, nu_used)``; raises NystromBreakdownError with the
+    reference's messages.  On the device (edak_potrf_shifted, dpotrf's
+    breakdown test); numpy in, numpy out."""
+    from .linalg import potrf_shifted
+    w = np.asarray(w, dtype=float)
+    if w.ndim != 2 or w.shape[0] != w.shape[1]:
+        raise ValueError("shifted_cholesky needs a square matrix")
+    # the block layout holds columns contiguously: the transpose of numpy's rows
+    W = _dev.f64(np.ascontiguousarray(w.T))
+    code = 0 if mode is None else 2  # 2: nu0 = eps * scale with the caller's scale
+    Cm, nu, info = potrf_shifted(W, code, float(scale))
+    info = info.cpu().numpy()
+    if info[1]:
+        if info[0] <= 1:
+            raise NystromBreakdownError(
+                "Cholesky of the sketched Gram matrix broke down and no "
+                "usable shift is available")
+        raise NystromBreakdownError("sketched Gram matrix stayed indefinite after shifting")
+    return Cm.cpu().numpy().T.copy(), float(nu[0])
+
+
 def _device_owner(a_apply):
     """Our operator object when a_apply is its bound ``a_apply`` (then the
     sketch never leaves the device)."""

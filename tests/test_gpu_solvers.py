@@ -741,3 +741,28 @@ def test_nystrom_blocked_gram_shift(gpu):
     assert approx.shift == pytest.approx(ref.shift, rel=1e-12)
     big = ref.values >= 1e-6 * ref.values[0]
     npt.assert_allclose(approx.values[big], ref.values[big], rtol=1e-9)
+
+
+def test_shifted_cholesky_dropin(gpu):
+    """nystrom.shifted_cholesky (nystrom.py:67-93) on the device: plain
+    factor of an SPD matrix, the eps * scale * 10^j shift schedule on a
+    singular Gram (same nu as the oracle), and the reference's two
+    breakdown messages."""
+    import scipy.linalg
+    from paper_2605_23571_b200.nystrom import NystromBreakdownError, shifted_cholesky
+    rng = np.random.default_rng(67)
+    a = rng.standard_normal((30, 30))
+    w = a @ a.T + 30 * np.eye(30)
+    c, nu = shifted_cholesky(w, "trace", np.trace(w))
+    assert nu == 0.0
+    npt.assert_allclose(c, scipy.linalg.cholesky(w, lower=False), rtol=1e-12, atol=1e-13)
+    b = rng.standard_normal((30, 12))
+    ws = b @ b.T  # rank 12: the plain factorization breaks down
+    c, nu = shifted_cholesky(ws, "trace", np.trace(ws))
+    c_ref, nu_ref = oalg.shifted_cholesky(ws, "trace", np.trace(ws))
+    assert nu > 0.0 and nu == pytest.approx(nu_ref, rel=1e-12)
+    npt.assert_allclose(c.T @ c, ws + nu * np.eye(30), rtol=0, atol=1e-10 * np.abs(ws).max())
+    with pytest.raises(NystromBreakdownError, match="no usable shift"):
+        shifted_cholesky(ws, None, np.trace(ws))
+    with pytest.raises(NystromBreakdownError, match="stayed indefinite"):
+        shifted_cholesky(-np.eye(30), "trace", 1.0)
