@@ -1,3 +1,3 @@
 mkdir -p gpurun_out/it
 O=gpurun_out/it
-timeout 600 python -m pytest tests/test_gpu_solvers.py -m gpu -q -x -p no:cacheprovider -k "shifted_cholesky or nystrom or potrf" > $O/sc.log 2>&1; echo rc=$? >> $O/sc.log
+CFG=5 REPS=3 python tools/ab_pass.py "" "EDAK_PCG_GRAPH=1" "EDAK_PCG_GROUPS=2+EDAK_PCG_GRAPH=1" > $O/ab_g5.txt 2>&1
