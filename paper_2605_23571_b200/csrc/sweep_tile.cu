@@ -90,7 +90,8 @@ struct TmaStage {
   // wrapped windows (the tiles across the ring end): per-thread 16-byte
   // cp.async into the same layout; each thread's copies arrive on the
   // mbarrier (initialised with NT arrivals for these CTAs) when they land
-  __device__ static __forceinline__ void wrapped(uint32_t buf, const double* row, int gm2, int n, uint32_t mbar) {
+  __device__ static __forceinline__ void wrapped(uint32_t buf, const double* row, int gm2, int n, uint32_t mbar,
+                                                 bool arrive = true) {
     const int t = threadIdx.x;
 #pragma unroll
     for (int k = 0; k < (R + 4) / 2 / NT + 1; ++k) {
@@ -103,7 +104,7 @@ struct TmaStage {
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(row + g) : "memory");
       }
     }
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(mbar) : "memory");
+    if (arrive) asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(mbar) : "memory");
   }
   // thread t's window (own elements 16t .. 16t + 15 and the 2 + 2 halo):
   // row t's chunks 0..7 and row t + 1's chunks 0, 1.  Chunk c of row r sits
@@ -136,6 +137,37 @@ struct TileSmem {
     return 1024 /* alignment slack */ + XB + NB * (size_t)TS::BUF + extra_doubles * 8 + NB * 8;
   }
 };
+
+// The grid-position map of a tile's own range [base, base + NT C) (obs.py
+// position maps), copied by coalesced 4-byte cp.async into the second
+// exchange buffer (idle until the first step; its zero pads are rewritten
+// afterwards) and read back as four 16-byte loads per thread -- the 16
+// scalar loads per thread, 64 B apart, were on the prologue's critical path.
+template <int C, int NT>
+__device__ __forceinline__ void gpos_copy(XBuf<NT>& xb, const int32_t* __restrict__ gpos, int base, int n) {
+  static_assert(sizeof(xb.v[1]) >= C * NT * sizeof(int32_t), "the map fits one exchange buffer");
+  int32_t* gs = reinterpret_cast<int32_t*>(&xb.v[1][0][0][0]);
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    const int q = (int)threadIdx.x + k * NT;
+    int g = base + q;
+    g = g < 0 ? g + n : (g >= n ? g - n : g);
+    const unsigned d = (unsigned)__cvta_generic_to_shared(gs + q);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gpos + g) : "memory");
+  }
+}
+template <int C, int NT>
+__device__ __forceinline__ void gpos_read(const XBuf<NT>& xb, int (&gp)[C]) {
+  const int4* gs = reinterpret_cast<const int4*>(&xb.v[1][0][0][0]) + threadIdx.x * (C / 4);
+#pragma unroll
+  for (int k = 0; k < C / 4; ++k) {
+    const int4 q = gs[k];
+    gp[4 * k] = q.x;
+    gp[4 * k + 1] = q.y;
+    gp[4 * k + 2] = q.z;
+    gp[4 * k + 3] = q.w;
+  }
+}
 
 // ------------------------------------------------------------------- TL --
 template <int C, int NT, int MINB>
@@ -184,14 +216,30 @@ __global__ void __launch_bounds__(NT, MINB)
   stage(s0, 0);
   if (s0 + 1 < s1) stage(s0 + 1, 1);
 
-  // window chunk [s0, s1): v enters at level s0 and leaves at level s1
+  // window chunk [s0, s1): v enters at level s0 and leaves at level s1.
+  // Its window (own elements and halo) arrives by coalesced 16-byte cp.async
+  // into stage buffer 2 (free until the first step stages X_{s0+2}) in the
+  // stage layout, read back like X: 16 scalar loads per thread, 128 B apart,
+  // had put their latency on the prologue's critical path
   double v[C + 4];
-  R.load_own(vin + (size_t)col * n, v);
   int gw[C];  // observed own elements inside the output window: grid position or -1
+  const int tp0 = s0 == 0 ? __ldg(P.tpos) : -1;  // level 0's time position (before the copies)
+  {
+    const uint32_t sbuf = sb0 + 2 * TS::BUF;
+    TS::wrapped(sbuf, vin + (size_t)col * n, gst, n, 0, false);
+    gpos_copy<C, NT>(xb, P.gpos, R.base, n);
+    cp_commit();
+    cp_wait_all();
+    __syncthreads();
+    TS::win(sbuf, R.t, v);
+    gpos_read<C, NT>(xb, gw);
 #pragma unroll
-  for (int j = 0; j < C; ++j) {
-    const int e = R.t * C + j;
-    gw[j] = (e >= wlo && e < whi) ? __ldg(P.gpos + R.gidx(j)) : -1;
+    for (int j = 0; j < C; ++j) {
+      const int e = R.t * C + j;
+      if (!(e >= wlo && e < whi)) gw[j] = -1;
+    }
+    __syncthreads();  // the map is read: the exchange buffer's pads back
+    xb.init_pads();
   }
   auto capture_tp = [&](int tp) {
     if (tp < 0) return;
@@ -201,7 +249,7 @@ __global__ void __launch_bounds__(NT, MINB)
     for (int j = 0; j < C; ++j)
       if (gw[j] >= 0) ot[gw[j]] = v[j + 2];
   };
-  if (s0 == 0) capture_tp(__ldg(P.tpos));
+  if (s0 == 0) capture_tp(tp0);
 
 
   int xbi = 0;  // exchange buffer (double-buffered)
@@ -340,9 +388,24 @@ __global__ void __launch_bounds__(NT, MINB)
 
   // forcing w_all[level] at own elements: R^-1 d at observed points
   // (obs.py:54-56 with covariance.py:71), 0 elsewhere
+  // the grid-position map and (second window chunk) the incoming g window,
+  // both by coalesced cp.async in one group: g through the stage slot the
+  // prologue leaves free, as the TL's v
+  // the time positions the prologue needs, loaded before the copies so
+  // they are in registers when the forcing addresses are formed
+  const int tp_top = gin ? -1 : __ldg(P.tpos + N), tp_first = __ldg(P.tpos + s1 - 1);
   int gp[C];
-#pragma unroll
-  for (int j = 0; j < C; ++j) gp[j] = __ldg(P.gpos + R.gidx(j));
+  double g[C + 4];
+  const uint32_t gbuf = sb0 + (NB - 1) * TS::BUF;
+  gpos_copy<C, NT>(xb, P.gpos, R.base, n);
+  if (gin) TS::wrapped(gbuf, gin + (size_t)col * n, gst, n, 0, false);
+  cp_commit();
+  cp_wait_all();
+  __syncthreads();
+  gpos_read<C, NT>(xb, gp);
+  if (gin) TS::win(gbuf, R.t, g);
+  __syncthreads();  // the map is read: the exchange buffer's pads back
+  xb.init_pads();
   auto fetch_force = [&](int tp, int slot) {  // cp.async into thread-private slots
     if (tp < 0) return;
     const double* f = fc + (size_t)tp * G;
@@ -353,11 +416,8 @@ __global__ void __launch_bounds__(NT, MINB)
       if (gp[j] >= 0) cp_async8(d + j * NT, f + gp[j]);
   };
 
-  double g[C + 4];
-  if (gin) {
-    R.load_own(gin + (size_t)col * n, g);
-  } else {  // w_all[N] (model.py:154)
-    const int tp = __ldg(P.tpos + N);
+  if (!gin) {  // w_all[N] (model.py:154)
+    const int tp = tp_top;
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       g[j + 2] = 0.0;
@@ -365,7 +425,7 @@ __global__ void __launch_bounds__(NT, MINB)
     }
   }
 
-  int tp_cur = __ldg(P.tpos + s1 - 1);
+  int tp_cur = tp_first;
   fetch_force(tp_cur, (s1 - 1) & 1);  // prologue: the forcing of level s1-1
   cp_commit();
 
