@@ -53,7 +53,23 @@ __global__ void __launch_bounds__(NT) k_integrate(int n, int K, int s0, double d
   int buf = 0;
 
   double x[C + 4];
-  R.load_halo(xin + (size_t)col * in_stride, x);
+  {
+    // 16-byte pairs where the window does not wrap and the row is 16-byte
+    // aligned (even C, ring bases and n: every tile base is even), else the
+    // scalar loads
+    const double* src = xin + (size_t)col * in_stride;
+    const int g = R.g0 >= 2 ? R.g0 - 2 : R.g0 - 2 + n;
+    if (C % 2 == 0 && g % 2 == 0 && g + C + 4 <= n && ((uintptr_t)src & 15) == 0) {
+#pragma unroll
+      for (int k = 0; k < (C + 4) / 2; ++k) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(src + g) + k);
+        x[2 * k] = v.x;
+        x[2 * k + 1] = v.y;
+      }
+    } else {
+      R.load_halo(src, x);
+    }
+  }
   for (int s = 0; s < K; ++s) {
     double k1[C], k2[C], k3[C], k4[C], x2[C + 4], x3[C + 4], x4[C + 4];
     l96_stage<C>(x, x, h, F, k1, x2);
@@ -70,8 +86,23 @@ __global__ void __launch_bounds__(NT) k_integrate(int n, int K, int s0, double d
       double sum = __dadd_rn(__dadd_rn(__dadd_rn(k1[j], 2.0 * k2[j]), 2.0 * k3[j]), k4[j]);
       xn[j + 2] = __dadd_rn(x[j + 2], __dmul_rn(c6, sum));
     }
-    // store own elements inside the output window
-    if (R.t < R.nact) {
+    // store own elements inside the output window (16-byte pairs when the
+    // row, the thread's first element and the window bounds are even)
+    double* srow = st + (size_t)(s0 + s + 1) * n;
+    if (R.t < R.nact && !sg && C % 2 == 0 && n % 2 == 0 && R.g0 % 2 == 0 && wlo % 2 == 0 && whi % 2 == 0 &&
+        ((uintptr_t)srow & 15) == 0) {
+#pragma unroll
+      for (int k = 0; k < C / 2; ++k) {
+        const int e = R.t * C + 2 * k;
+        const int g = R.gidx(2 * k);
+        if (e >= wlo && e < whi && g + 1 < n)
+          *reinterpret_cast<double2*>(srow + g) = make_double2(xn[2 * k + 2], xn[2 * k + 3]);
+        else if (e >= wlo && e < whi) {
+          srow[g] = xn[2 * k + 2];
+          srow[R.gidx(2 * k + 1)] = xn[2 * k + 3];
+        }
+      }
+    } else if (R.t < R.nact) {
 #pragma unroll
       for (int j = 0; j < C; ++j) {
         const int e = R.t * C + j;

@@ -1,4 +1,4 @@
 mkdir -p gpurun_out/it
 O=gpurun_out/it
-python tools/sweep_ncu.py 5 > $O/sw5.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:'k_tl_tile|k_ad_tile' -s 2 -c 2 -o $O/sw5_full python tools/sweep_ncu.py 5 > $O/sw5_full.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_operator.py tests/test_gpu_configs.py -m gpu -q -x -p no:cacheprovider -k "integrate or refresh or stream or model or ensemble or config" > $O/int.log 2>&1; echo rc=$? >> $O/int.log
+python bench.py --steps 5 --warmup 3 --no-cpu --per-config "" > $O/b.json 2> $O/b.err
