@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
 
   // window chunk [s0, s1): v enters at level s0 and leaves at level s1
   double v[C + 4];
-  R.load_own(vin + (size_t)col * n, v);
+  R.load_own2(vin + (size_t)col * n, v);
 
   // observed own elements inside the output window: grid position or -1
   int gw[C];
@@ -312,14 +312,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
     for (int j = 0; j < C; ++j) v[j + 2] = fma(c6, acc[j] + a[j], v[j + 2]);
     capture_tp(tp_next);
   }
-  if (vout && R.t < R.nact) {
-    double* vo = vout + (size_t)col * n;
-#pragma unroll
-    for (int j = 0; j < C; ++j) {
-      const int e = R.t * C + j;
-      if (e >= wlo && e < whi) vo[R.gidx(j)] = v[j + 2];
-    }
-  }
+  if (vout && R.t < R.nact) R.store_own(vout + (size_t)col * n, v, wlo, whi);
 }
 
 // ------------------------------------------------------------------- AD --
@@ -405,7 +398,7 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
   // when s1 == N, model.py:154) and leaves at level s0
   double g[C + 4];
   if (gin) {
-    R.load_own(gin + (size_t)col * n, g);
+    R.load_own2(gin + (size_t)col * n, g);
   } else {
 #pragma unroll
     for (int j = 0; j < C; ++j) g[j + 2] = 0.0;
@@ -538,14 +531,7 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
     psrc -= n;
     --tpp;
   }
-  if (R.t < R.nact) {
-    double* go = gout + (size_t)col * n;
-#pragma unroll
-    for (int j = 0; j < C; ++j) {
-      const int e = R.t * C + j;
-      if (e >= wlo && e < whi) go[R.gidx(j)] = g[j + 2];
-    }
-  }
+  if (R.t < R.nact) R.store_own(gout + (size_t)col * n, g, wlo, whi);
 }
 
 // ------------------------------------------------------------ launchers --

@@ -73,6 +73,42 @@ struct Ring {
       for (int k = 0; k < C + 4; ++k) a[k] = __ldg(src + wrap(g + k, n));
     }
   }
+  // the same as 16-byte pairs where the row is 16-byte aligned and the
+  // thread's range starts even and does not wrap (every pair-layout tile)
+  __device__ __forceinline__ void load_own2(const double* __restrict__ src, double (&a)[C + 4]) const {
+    if (C % 2 == 0 && g0 % 2 == 0 && g0 + C <= n && ((uintptr_t)src & 15) == 0) {
+#pragma unroll
+      for (int k = 0; k < C / 2; ++k) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(src + g0) + k);
+        a[2 * k + 2] = v.x;
+        a[2 * k + 3] = v.y;
+      }
+    } else {
+      load_own(src, a);
+    }
+  }
+  // own elements inside the output window [wlo, whi) of the range: 16-byte
+  // pair stores when the column base is 16-byte aligned and the ring, the
+  // thread's first element and the window bounds are even (a pair is then
+  // aligned, never wraps and is inside or outside as a whole), else scalar
+  // (16 stores C * 8 B apart per thread: their issue ended every CTA)
+  __device__ __forceinline__ void store_own(double* __restrict__ out, const double (&a)[C + 4], int wlo,
+                                            int whi) const {
+    if (C % 2 == 0 && n % 2 == 0 && g0 % 2 == 0 && wlo % 2 == 0 && whi % 2 == 0 && ((uintptr_t)out & 15) == 0) {
+#pragma unroll
+      for (int k = 0; k < C / 2; ++k) {
+        const int e = t * C + 2 * k;
+        if (e >= wlo && e < whi)
+          *reinterpret_cast<double2*>(out + gidx(2 * k)) = make_double2(a[2 * k + 2], a[2 * k + 3]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        const int e = t * C + j;
+        if (e >= wlo && e < whi) out[gidx(j)] = a[j + 2];
+      }
+    }
+  }
   __device__ __forceinline__ void load_own(const double* __restrict__ src, double (&a)[C + 4]) const {
     if (g0 + C <= n) {
 #pragma unroll

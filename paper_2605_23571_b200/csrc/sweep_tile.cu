@@ -169,32 +169,6 @@ __device__ __forceinline__ void gpos_read(const XBuf<NT>& xb, int (&gp)[C]) {
   }
 }
 
-// Own elements inside the output window [wlo, whi) of the range, as
-// 16-byte pair stores when the column base is 16-byte aligned: the tile
-// bases, window bounds and n are even (the pair layout these kernels
-// require), so an element pair (2k, 2k + 1) is then 16-byte aligned, never
-// wraps the ring and is inside or outside the window as a whole (16 scalar
-// stores 128 B apart per thread before: cfg4 TL 0.296 -> 0.289 ms, AD
-// 0.362 -> 0.351 ms).
-template <int C, int NT>
-__device__ __forceinline__ void store_pairs(const Ring<C, NT>& R, double* __restrict__ out,
-                                            const double (&a)[C + 4], int wlo, int whi) {
-  if (((uintptr_t)out & 15) == 0) {  // CTA-uniform: the column base (workspace blocks may be 8-aligned)
-#pragma unroll
-    for (int k = 0; k < C / 2; ++k) {
-      const int e = R.t * C + 2 * k;
-      if (e >= wlo && e < whi)
-        *reinterpret_cast<double2*>(out + R.gidx(2 * k)) = make_double2(a[2 * k + 2], a[2 * k + 3]);
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < C; ++j) {
-      const int e = R.t * C + j;
-      if (e >= wlo && e < whi) out[R.gidx(j)] = a[j + 2];
-    }
-  }
-}
-
 // ------------------------------------------------------------------- TL --
 template <int C, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB)
@@ -347,7 +321,8 @@ __global__ void __launch_bounds__(NT, MINB)
     R.put(&xb.v[xbi][0][0][0], v);  // halos for the next step's exchange
     capture_tp(tp_next);
   }
-  if (vout) store_pairs<C, NT>(R, vout + (size_t)col * n, v, wlo, whi);
+  // (pair stores, sweep.cuh: cfg4 TL 0.296 -> 0.292 ms, AD 0.362 -> 0.351 ms)
+  if (vout) R.store_own(vout + (size_t)col * n, v, wlo, whi);
 }
 
 // ------------------------------------------------------------------- AD --
@@ -546,7 +521,7 @@ __global__ void __launch_bounds__(NT, MINB)
     tp_cur = tp_next;
     --tpp;
   }
-  store_pairs<C, NT>(R, gout + (size_t)col * n, g, wlo, whi);
+  R.store_own(gout + (size_t)col * n, g, wlo, whi);
 }
 
 // ------------------------------------------------------------ launchers --
