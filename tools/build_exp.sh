@@ -4,7 +4,7 @@ set -e
 cd "$(dirname "$0")/.."
 OUT=build/exp_$2
 mkdir -p $OUT
-for f in capi l96 circ circ_os circ_fft blas small cholinv jacobi_cluster pcg pcg_small peak sweep2 sweep3; do
+for f in capi l96 l96_ops sweep_tile circ circ_os blas lmp_gemm small cholinv jacobi_cluster pcg pcg_small peak; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC $1 -c paper_2605_23571_b200/csrc/$f.cu -o $OUT/$f.o &
 done
 wait
