@@ -66,7 +66,7 @@ int launch_pcg_alpha(int, int, const double*, const double*, double*, double*, d
 int launch_pcg_rz(int, int, int, const double*, const double*, double*, double, double*, double*, int, int32_t*,
                   int32_t*, int, cudaStream_t);
 int launch_pcg_reduce_rz(int, int, int, const double*, int, double*, const double*, double*, double, double*,
-                         double*, int, int32_t*, int32_t*, int, cudaStream_t);
+                         double*, int, int32_t*, int32_t*, int, cudaStream_t, int prescale);
 int launch_gemm_tn_parts(const double*, int64_t, const double*, int64_t, int, int, int64_t, double*, cudaStream_t);
 double* pcg_beta_ptr(int, int, double*);
 int launch_pcg_beta(int, int, const double*, const double*, double*, double*, double, double*, double*, int,
@@ -335,15 +335,17 @@ int edak_pcg_lmp_beta(int n, int k, int ncols, const double* S, const double* co
   if (nsplit == 0) nsplit = launch_gemm_tn_parts(S, n, r, n, k, ncols, n, part, st);
 #endif
   if ((rc = check_launch("k_gemm_tn"))) return rc;
+  // (W written as coef o W: the p-update then skips its scaling; same bits)
   if ((rc = launch_pcg_reduce_rz(n, ncols, k, part, nsplit, W, coef, work, rtol, hist_rz, hist_J, hist_ld, status,
-                                 iters, it, st)))
+                                 iters, it, st, 1)))
     return rc;
   // p = r + beta p + S (coef o W)  (= z + beta p, krylov.py:95 with z = P r)
 #ifdef EDAK_EXP_NOGEMM
   return EDAK_OK;
 #endif
-  if (lg && lmp_nn_ok(ncols)) return launch_lmp_nn(S, W, coef, n, k, ncols, r, pcg_beta_ptr(n, ncols, work), p, p, st);
-  return launch_gemm_nn(S, n, W, k, coef, r, n, 1.0, p, n, n, ncols, k, st, pcg_beta_ptr(n, ncols, work), p);
+  if (lg && lmp_nn_ok(ncols))
+    return launch_lmp_nn(S, W, nullptr, n, k, ncols, r, pcg_beta_ptr(n, ncols, work), p, p, st);
+  return launch_gemm_nn(S, n, W, k, nullptr, r, n, 1.0, p, n, n, ncols, k, st, pcg_beta_ptr(n, ncols, work), p);
 }
 
 int edak_pcg_small(const edak_problem* P, const int32_t* col_traj, int ncols, const double* b, const double* d,

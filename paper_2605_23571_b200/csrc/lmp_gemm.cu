@@ -201,12 +201,15 @@ __global__ void __launch_bounds__(NW * 32, 1)
   }
   loadA(0, 0);
   wait<0>();
-  // scale the resident W rows by coef (each thread its own copies' bytes)
-  for (int idx = t; idx < MM * KMAX / 2; idx += NT) {
-    const int b = idx / (KMAX / 2), a = 2 * (idx % (KMAX / 2));
-    double* w = sW + b * LDW + a;
-    w[0] *= a < k ? __ldg(coef + a) : 0.0;
-    w[1] *= a + 1 < k ? __ldg(coef + a + 1) : 0.0;
+  // scale the resident W rows by coef (each thread its own copies' bytes);
+  // coef NULL: W arrives scaled (k_pcg_reduce_rz's prescale)
+  if (coef) {
+    for (int idx = t; idx < MM * KMAX / 2; idx += NT) {
+      const int b = idx / (KMAX / 2), a = 2 * (idx % (KMAX / 2));
+      double* w = sW + b * LDW + a;
+      w[0] *= a < k ? __ldg(coef + a) : 0.0;
+      w[1] *= a + 1 < k ? __ldg(coef + a + 1) : 0.0;
+    }
   }
   double acc[FMN][FN][2];
 #pragma unroll

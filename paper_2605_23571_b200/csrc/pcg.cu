@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(1024) k_pcg_reduce_rz(int T, int M, int k, con
                                                        double* __restrict__ beta, double rtol,
                                                        double* __restrict__ hist_rz, double* __restrict__ hist_J,
                                                        int hist_ld, int32_t* __restrict__ status,
-                                                       int32_t* __restrict__ iters, int it) {
+                                                       int32_t* __restrict__ iters, int it, int prescale) {
   __shared__ double sh[32];
   __shared__ double gs[8][128];
   const int c = blockIdx.x, t = threadIdx.x;
@@ -311,7 +311,9 @@ __global__ void __launch_bounds__(1024) k_pcg_reduce_rz(int T, int M, int k, con
     if (g == 0 && i < k) {
       const double w = ((gs[0][e] + gs[1][e]) + (gs[2][e] + gs[3][e])) +
                        ((gs[4][e] + gs[5][e]) + (gs[6][e] + gs[7][e]));
-      W[i + (size_t)c * k] = w;
+      // prescale: coef o W for the p-update GEMM (the product it would form
+      // on staging, so the same bits), sparing k_lmp_nn its scaling pass
+      W[i + (size_t)c * k] = prescale ? coef[i] * w : w;
       q += coef[i] * (w * w);
     }
     __syncthreads();
@@ -341,14 +343,14 @@ __global__ void __launch_bounds__(1024) k_pcg_reduce_rz(int T, int M, int k, con
 
 int launch_pcg_reduce_rz(int n, int M, int k, const double* part, int nsplit, double* W, const double* coef,
                          double* work, double rtol, double* hist_rz, double* hist_J, int hist_ld, int32_t* status,
-                         int32_t* iters, int it, cudaStream_t st) {
+                         int32_t* iters, int it, cudaStream_t st, int prescale) {
   const int T = pcg_tiles(n);
   double* part_x = work + (size_t)M * T;
   double* part_rr = work + 2 * (size_t)M * T;
   double* rzb = work + 4 * (size_t)M * T;
   double* beta = rzb + 2 * (size_t)M;
   k_pcg_reduce_rz<<<M, 1024, 0, st>>>(T, M, k, part, nsplit, W, coef, part_rr, part_x, rzb, beta, rtol, hist_rz,
-                                     hist_J, hist_ld, status, iters, it);
+                                     hist_J, hist_ld, status, iters, it, prescale);
   count_launch();
   return check_launch("k_pcg_reduce_rz");
 }
