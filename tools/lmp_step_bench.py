@@ -14,7 +14,7 @@ from paper_2605_23571_b200 import _lib, build  # noqa: E402
 build.build()
 lib = _lib.lib()
 reps = int(os.environ.get("REPS", "200"))
-for n, k, M in ((16384, 128, 100), (262144, 128, 256)):
+for n, k, M in ((16384, 128, 100), (262144, 128, 256)) if not os.environ.get("SHAPE") else (tuple(int(v) for v in os.environ["SHAPE"].split(",")),):
     g = torch.Generator(device="cuda").manual_seed(1)
     S = torch.linalg.qr(torch.randn(n, k, dtype=torch.float64, device="cuda", generator=g))[0].t().contiguous()
     R = torch.randn(M, n, dtype=torch.float64, device="cuda", generator=g)
@@ -44,3 +44,12 @@ for n, k, M in ((16384, 128, 100), (262144, 128, 256)):
     torch.cuda.synchronize()
     print(f"n={n} k={k} M={M}: fused LMP step (S^T r + reduce/beta + p-update) "
           f"{1e3 * s.elapsed_time(e) / reps:.1f} us per call")
+    if os.environ.get("PROFILE"):
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for _ in range(50):
+                step()
+            torch.cuda.synchronize()
+        for ev in sorted(prof.key_averages(), key=lambda v: -v.device_time_total):
+            if ev.device_time_total > 0:
+                print(f"   {ev.device_time_total / 50:8.1f} us  {ev.key[:70]}")
