@@ -34,6 +34,16 @@ def build(force=False, verbose=False):
     """Compile every .cu into objects and link libedak.so; returns its path."""
     if not force and not _stale():
         return LIB
+    # one builder at a time: under torchrun every rank calls build() at once
+    import fcntl
+    with open(os.path.join(HERE, ".build.lock"), "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        if not force and not _stale():  # another rank built it while we waited
+            return LIB
+        return _build_locked(verbose)
+
+
+def _build_locked(verbose):
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
