@@ -47,6 +47,13 @@ class CirculantFactor:
         s = 1.0 if self.sigma_b is None else self.sigma_b
         return np.fft.irfft(self.symbol ** 2, n=self.n) / s ** 2
 
+    def dense(self):
+        """The factor as an (n, n) host matrix, small n only (covariance.py:53-56):
+        entry (i, j) is the generator at (i - j) mod n."""
+        u = np.fft.irfft(self.symbol, n=self.n)
+        i = np.arange(self.n)
+        return u[(i[:, None] - i[None, :]) % self.n]
+
 
 class GridCovFactor(CirculantFactor):
     """Reference diffusion-spectrum factor (covariance.py:22-39): symbol

@@ -71,6 +71,20 @@ def test_factor_taps_truncation():
     assert taps.size == 40  # full ring
 
 
+def test_factor_dense_and_correlation():
+    """covariance.py:49-56 -- the dense circulant equals the FFT apply, is
+    symmetric, and the implied correlation has a unit diagonal."""
+    from paper_2605_23571_b200.covariance import GridCovFactor
+    ub = GridCovFactor(40, 0.8, 6.0, 10)
+    d = ub.dense()
+    v = np.random.default_rng(3).standard_normal(40)
+    ref = np.fft.irfft(np.fft.rfft(v) * ub.symbol, n=40)
+    assert np.allclose(d @ v, ref, rtol=0, atol=1e-13)
+    assert np.allclose(d, d.T, rtol=0, atol=1e-15)
+    assert abs(ub.correlation()[0] - 1.0) < 1e-12
+    assert np.allclose((d @ d.T)[0] / 0.8 ** 2, ub.correlation(), rtol=0, atol=1e-13)
+
+
 def test_position_maps_time_major():
     from paper_2605_23571_b200.obs import ObsNetwork, position_maps, strided_grid
     net = ObsNetwork(strided_grid(16384, 4096), list(range(3, 25, 3)))
