@@ -40,7 +40,8 @@ typedef struct edak_problem {
   double dt;             /* RK4 step (Trajectory.dt)                            */
   double forcing;        /* F (Trajectory.forcing)                              */
   /* linearization trajectories: states[traj][s][i], s = 0..N-1 (the RK4
-   * stages are recomputed bit-exactly from states[s], model.py:38-48), or,
+   * stages are recomputed from states[s], model.py:38-48, to within ~1 ulp:
+   * FMA-contracted, restarted from the exact state every step), or,
    * when stage_mode == 1, stages[traj][s][k][i] streamed as stored
    * (Trajectory.stages, model.py:95-97). */
   const double* states;

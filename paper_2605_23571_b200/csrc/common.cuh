@@ -21,27 +21,50 @@ __host__ __device__ __forceinline__ int wrap(int i, int n) {
 // tendency (model.py:20-22): ((x[i+1] - x[i-2]) * x[i-1] - x[i]) + F
 __device__ __forceinline__ double l96_f(double xp1, double xm2, double xm1,
                                         double x0, double F) {
-#ifdef EDAK_EXP_FMA  // timing experiment: contracted (not bit-exact) stages
-  return fma(xp1 - xm2, xm1, -x0) + F;
-#else
   return __dadd_rn(__dsub_rn(__dmul_rn(__dsub_rn(xp1, xm2), xm1), x0), F);
-#endif
 }
 // the same with the difference x[i+1] - x[i-2] supplied (shared with the TL
 // of that stage: the compiler does not CSE __dsub_rn against a plain '-')
 __device__ __forceinline__ double l96_f_d(double d, double xm1, double x0, double F) {
-#ifdef EDAK_EXP_FMA
-  return fma(d, xm1, -x0) + F;
-#else
   return __dadd_rn(__dsub_rn(__dmul_rn(d, xm1), x0), F);
-#endif
 }
 // stage update x + c*k (model.py:41,43,45): rounded product then sum
 __device__ __forceinline__ double axpy_rn(double x, double c, double k) {
-#ifdef EDAK_EXP_FMA
+  return __dadd_rn(x, __dmul_rn(c, k));
+}
+
+// ---- RK4 stages recomputed inside the TL / AD sweeps ----------------------
+// x2, x3, x4 of a step (model.py:40-45) from the stored state X_s, which the
+// producer k_integrate wrote with the IEEE-rounded operations above, bit for
+// bit the reference's trajectory.  EDAK_STAGE_FMA=1 (default) contracts the
+// recompute -- fma(d, x[i-1], -x[i]) + F and fma(c, k, X) -- so each stage
+// is within ~1 ulp of the reference's stored stage (the error does not
+// accumulate: every step restarts from the exact X_s) and costs 4 instead of
+// 7 DP instructions; the TL / AD tendencies below are contracted the same
+// way.  EDAK_STAGE_FMA=0 rebuilds the sweeps with the exact chain (then
+// stage_mode "stream" and "recompute" are bit-identical).
+#ifndef EDAK_STAGE_FMA
+#define EDAK_STAGE_FMA 1
+#endif
+__device__ __forceinline__ double stg_f(double xp1, double xm2, double xm1, double x0, double F) {
+#if EDAK_STAGE_FMA
+  return fma(xp1 - xm2, xm1, -x0) + F;
+#else
+  return l96_f(xp1, xm2, xm1, x0, F);
+#endif
+}
+__device__ __forceinline__ double stg_f_d(double d, double xm1, double x0, double F) {
+#if EDAK_STAGE_FMA
+  return fma(d, xm1, -x0) + F;
+#else
+  return l96_f_d(d, xm1, x0, F);
+#endif
+}
+__device__ __forceinline__ double stg_axpy(double x, double c, double k) {
+#if EDAK_STAGE_FMA
   return fma(c, k, x);
 #else
-  return __dadd_rn(x, __dmul_rn(c, k));
+  return axpy_rn(x, c, k);
 #endif
 }
 

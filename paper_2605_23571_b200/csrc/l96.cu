@@ -7,9 +7,11 @@
 //   k_ad        : adjoint sweep with observation forcing
 //                 (model.adjoint + ObsNetwork.observe_adj, model.py:66-84,
 //                 147-157, obs.py:52-57)
-// Stages are recomputed from the stored states (16 B/elem-step of HBM instead
-// of 64) with IEEE-rounded ops in the reference's order, so they are the
-// reference's stages bit for bit; STREAM=true reads stored stages instead.
+// The sweeps recompute the RK4 stages from the stored states (16 B/elem-step
+// of HBM instead of 64) with the contracted chain stg_* of common.cuh: within
+// ~1 ulp of the reference's stored stages, restarted from the exact state at
+// every step (EDAK_STAGE_FMA=0: the IEEE-ordered chain, bit for bit);
+// STREAM=true reads stored stages instead.
 #include <cstdio>
 #include <cstdlib>
 
@@ -256,8 +258,8 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
     } else {
 #pragma unroll
       for (int j = 0; j < C; ++j) {
-        kk[j] = l96_f_d(dd[j], X[j + 1], X[j + 2], F);
-        x2[j + 2] = axpy_rn(X[j + 2], h, kk[j]);
+        kk[j] = stg_f_d(dd[j], X[j + 1], X[j + 2], F);
+        x2[j + 2] = stg_axpy(X[j + 2], h, kk[j]);
       }
     }
 #pragma unroll
@@ -276,8 +278,8 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
     } else {
 #pragma unroll
       for (int j = 0; j < C; ++j) {
-        kk[j] = l96_f_d(dd[j], x2[j + 1], x2[j + 2], F);
-        x3[j + 2] = axpy_rn(X[j + 2], h, kk[j]);
+        kk[j] = stg_f_d(dd[j], x2[j + 1], x2[j + 2], F);
+        x3[j + 2] = stg_axpy(X[j + 2], h, kk[j]);
       }
     }
 #pragma unroll
@@ -296,8 +298,8 @@ __global__ void __launch_bounds__(NT, MINB) k_tl(edak_problem P, const double* _
     } else {
 #pragma unroll
       for (int j = 0; j < C; ++j) {
-        kk[j] = l96_f_d(dd[j], x3[j + 1], x3[j + 2], F);
-        x4[j + 2] = axpy_rn(X[j + 2], dt, kk[j]);
+        kk[j] = stg_f_d(dd[j], x3[j + 1], x3[j + 2], F);
+        x4[j + 2] = stg_axpy(X[j + 2], dt, kk[j]);
       }
     }
 #pragma unroll
@@ -451,7 +453,7 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
       X1(g);
     } else {
 #pragma unroll
-      for (int j = 0; j < C; ++j) x2[j + 2] = axpy_rn(X[j + 2], h, l96_f(X[j + 3], X[j], X[j + 1], X[j + 2], F));
+      for (int j = 0; j < C; ++j) x2[j + 2] = stg_axpy(X[j + 2], h, stg_f(X[j + 3], X[j], X[j + 1], X[j + 2], F));
       if constexpr (WT) {
         wxchg1<C>(x2);
         wxchg1<C>(g);
@@ -475,11 +477,11 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
       }
 #pragma unroll
       for (int j = 0; j < C; ++j)
-        x3[j + 2] = axpy_rn(X[j + 2], h, l96_f(x2[j + 3], x2[j], x2[j + 1], x2[j + 2], F));
+        x3[j + 2] = stg_axpy(X[j + 2], h, stg_f(x2[j + 3], x2[j], x2[j + 1], x2[j + 2], F));
       X1(x3);
 #pragma unroll
       for (int j = 0; j < C; ++j)
-        x4[j + 2] = axpy_rn(X[j + 2], dt, l96_f(x3[j + 3], x3[j], x3[j + 1], x3[j + 2], F));
+        x4[j + 2] = stg_axpy(X[j + 2], dt, stg_f(x3[j + 3], x3[j], x3[j + 1], x3[j + 2], F));
       X1(x4);
     }
     // step_adj (model.py:66-84): with w = (dt/6) g and c3 = 2 c6, dt = 2h,

@@ -8,7 +8,7 @@
 //
 // Same recurrence and formulas as the batched path (krylov.py:49-97 via
 // edak_hessian_block + edak_pcg_alpha + edak_pcg_lmp_beta); stage
-// recompute bit-exact (l96_f / axpy_rn), tendencies with FMA.
+// recompute as in the sweeps (stg_f / stg_axpy, common.cuh), tendencies with FMA.
 #include "common.cuh"
 
 namespace edak {
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(NT) k_pcg_small(SmallArgs A) {
     if (!own) return;
     const double* X = sTr + (size_t)s * n;
     const double* y = which == 0 ? X : st4[buf][which - 1];
-    st4[buf][which][i] = axpy_rn(X[i], which == 2 ? dt : h, l96_f(y[ip1], y[im2], y[im1], y[i], F));
+    st4[buf][which][i] = stg_axpy(X[i], which == 2 ? dt : h, stg_f(y[ip1], y[im2], y[im1], y[i], F));
   };
   // (I + A) p for p in sp_ (barrier after its write) -> returns hp_i
   auto hessian = [&]() -> double {
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(NT) k_pcg_small(SmallArgs A) {
         const double d1 = __dsub_rn(X[ip1], X[im2]);
         const double a1 = l96_tl_d(V[ip1], V[im2], V[im1], v, d1, X[im1]);
         su[0][i] = fma(h, a1, v);
-        sx[0][i] = axpy_rn(x0, h, l96_f_d(d1, X[im1], x0, F));
+        sx[0][i] = stg_axpy(x0, h, stg_f_d(d1, X[im1], x0, F));
         acc = a1;
       }
       __syncthreads();
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(NT) k_pcg_small(SmallArgs A) {
         const double d2 = __dsub_rn(sx[0][ip1], sx[0][im2]);
         const double a2 = l96_tl_d(su[0][ip1], su[0][im2], su[0][im1], su[0][i], d2, sx[0][im1]);
         su[1][i] = fma(h, a2, v);
-        sx[1][i] = axpy_rn(x0, h, l96_f_d(d2, sx[0][im1], sx[0][i], F));
+        sx[1][i] = stg_axpy(x0, h, stg_f_d(d2, sx[0][im1], sx[0][i], F));
         acc = fma(2.0, a2, acc);
       }
       __syncthreads();
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(NT) k_pcg_small(SmallArgs A) {
         const double d3 = __dsub_rn(sx[1][ip1], sx[1][im2]);
         const double a3 = l96_tl_d(su[1][ip1], su[1][im2], su[1][im1], su[1][i], d3, sx[1][im1]);
         su[0][i] = fma(dt, a3, v);
-        sx[0][i] = axpy_rn(x0, dt, l96_f_d(d3, sx[1][im1], sx[1][i], F));
+        sx[0][i] = stg_axpy(x0, dt, stg_f_d(d3, sx[1][im1], sx[1][i], F));
         acc = fma(2.0, a3, acc);
       }
       __syncthreads();

@@ -1,6 +1,6 @@
 // Tile-mode TL and AD sweeps (every Hessian apply on rings of n >= 4160):
-// the same arithmetic as k_tl / k_ad in l96.cu -- RK4 stages recomputed
-// bit-exactly from the stored states (model.py:38-48), TL of model.py:56-63
+// the same arithmetic as k_tl / k_ad in l96.cu -- RK4 stages recomputed from
+// the stored states (model.py:38-48; stg_* of common.cuh), TL of model.py:56-63
 // with the time-major observation capture of obs.py:47-50, adjoint of
 // model.py:66-84 with the R^-1 forcing of obs.py:52-57 -- on 1024-element
 // tiles (16 elements x 64 threads) with redundant halos, with the state
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(NT, MINB)
     for (int j = 0; j < C; ++j) {  // a1 = J(X) v; x2 = X + h f(X); u2 = v + h a1
       const double d = __dsub_rn(X[j + 3], X[j]);
       const double a = l96_tl_d(v[j + 3], v[j], v[j + 1], v[j + 2], d, X[j + 1]);
-      x2[j + 2] = axpy_rn(X[j + 2], h, l96_f_d(d, X[j + 1], X[j + 2], F));
+      x2[j + 2] = stg_axpy(X[j + 2], h, stg_f_d(d, X[j + 1], X[j + 2], F));
       acc[j] = a;
       u2[j + 2] = fma(h, a, v[j + 2]);
     }
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(NT, MINB)
     for (int j = 0; j < C; ++j) {  // a2 = J(x2) u2; x3 = X + h f(x2); u3 = v + h a2
       const double d = __dsub_rn(x2[j + 3], x2[j]);
       const double a = l96_tl_d(u2[j + 3], u2[j], u2[j + 1], u2[j + 2], d, x2[j + 1]);
-      x3[j + 2] = axpy_rn(X[j + 2], h, l96_f_d(d, x2[j + 1], x2[j + 2], F));
+      x3[j + 2] = stg_axpy(X[j + 2], h, stg_f_d(d, x2[j + 1], x2[j + 2], F));
       acc[j] = fma(2.0, a, acc[j]);
       u3[j + 2] = fma(h, a, v[j + 2]);
     }
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(NT, MINB)
     for (int j = 0; j < C; ++j) {  // a3 = J(x3) u3; x4 = X + dt f(x3); u4 = v + dt a3
       const double d = __dsub_rn(x3[j + 3], x3[j]);
       const double a = l96_tl_d(u3[j + 3], u3[j], u3[j + 1], u3[j + 2], d, x3[j + 1]);
-      x4[j + 2] = axpy_rn(X[j + 2], dt, l96_f_d(d, x3[j + 1], x3[j + 2], F));
+      x4[j + 2] = stg_axpy(X[j + 2], dt, stg_f_d(d, x3[j + 1], x3[j + 2], F));
       acc[j] = fma(2.0, a, acc[j]);
       u4[j + 2] = fma(dt, a, v[j + 2]);
     }
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(NT, MINB)
       double X[C + 4];
       TS::win(Xb, R.t, X);
 #pragma unroll
-      for (int j = 0; j < C; ++j) x2[j + 2] = axpy_rn(X[j + 2], h, l96_f(X[j + 3], X[j], X[j + 1], X[j + 2], F));
+      for (int j = 0; j < C; ++j) x2[j + 2] = stg_axpy(X[j + 2], h, stg_f(X[j + 3], X[j], X[j + 1], X[j + 2], F));
     }
     R.put(&xb.v[xbi][1][0][0], x2);
     __syncthreads();  // g, x2 halos; X_{s+1}'s buffer no longer read
@@ -463,12 +463,12 @@ __global__ void __launch_bounds__(NT, MINB)
       TS::win(Xb, R.t, X);
 #pragma unroll
       for (int j = 0; j < C; ++j)
-        x3[j + 2] = axpy_rn(X[j + 2], h, l96_f(x2[j + 3], x2[j], x2[j + 1], x2[j + 2], F));
+        x3[j + 2] = stg_axpy(X[j + 2], h, stg_f(x2[j + 3], x2[j], x2[j + 1], x2[j + 2], F));
       xchg1(x3);
       TS::win(Xb, R.t, X);
 #pragma unroll
       for (int j = 0; j < C; ++j)
-        x4[j + 2] = axpy_rn(X[j + 2], dt, l96_f(x3[j + 3], x3[j], x3[j + 1], x3[j + 2], F));
+        x4[j + 2] = stg_axpy(X[j + 2], dt, stg_f(x3[j + 3], x3[j], x3[j + 1], x3[j + 2], F));
       xchg1(x4);
     }
     // step_adj (model.py:66-84), as in k_ad: with w = (dt/6) g and c3 = 2 c6,

@@ -153,7 +153,9 @@ def test_cfg5_block_properties():
     """cfg5 (n=262144, N=12, every 8th variable every step): two columns
     against the oracle, plus size-independent properties on a 32-column
     block with per-column trajectories: symmetry <Az, w> = <z, Aw> and
-    stream == recompute (bit-identical)."""
+    stream == recompute (the streamed stages are the producer's IEEE-ordered
+    ones, the recomputed ones FMA-contracted within ~1 ulp of them: Hessian
+    columns agree to rel 1e-13; bit-identical in an EDAK_STAGE_FMA=0 build)."""
     from paper_2605_23571_b200 import build
     build.build()
     from paper_2605_23571_b200.assim import Linearization
@@ -173,7 +175,7 @@ def test_cfg5_block_properties():
     ops = oracle_rows(dens, [1, 2])
     for i, op in enumerate(ops):
         assert rel(AZ[i].cpu().numpy(), op.a_apply(Z[i].cpu().numpy())) < 1e-12
-    # streamed stored stages give bit-identical blocks
+    # streamed stored stages against the recomputed ones
     from paper_2605_23571_b200.model import integrate_device
     x0 = dens.states[1:5, 0].contiguous()
     states, stages = integrate_device(x0, dens.cfg.dt, dens.cfg.n_steps, dens.cfg.forcing,
@@ -181,7 +183,8 @@ def test_cfg5_block_properties():
     a = Linearization(states, dens.cfg.dt, dens.cfg.forcing, dens.net, dens.ub, dens.rn)
     b = Linearization(states, dens.cfg.dt, dens.cfg.forcing, dens.net, dens.ub, dens.rn,
                       stages, "stream")
-    assert torch.equal(a.hessian_cols(Z[:4]), b.hessian_cols(Z[:4]))
+    Ha, Hb = a.hessian_cols(Z[:4]), b.hessian_cols(Z[:4])
+    assert float(((Ha - Hb).norm(dim=1) / Hb.norm(dim=1)).max()) < 1e-13
 
 
 def test_refresh_reproduces_ensemble(gpu_cfg4):

@@ -146,8 +146,11 @@ def test_hessian_tile_modes(gpu, n, N, stride, every, L):
 
 
 def test_stream_equals_recompute(gpu):
-    """Recomputed stages are the stored stages bit for bit, so both stage
-    modes give identical Hessian blocks."""
+    """Recomputed stages (FMA-contracted, common.cuh stg_*) are within ~1 ulp
+    of the stored IEEE-ordered ones and the error does not accumulate over the
+    window (each step restarts from the exact stored state), so both stage
+    modes give the same Hessian blocks to rel 1e-13 per column (bit-identical
+    in an EDAK_STAGE_FMA=0 build)."""
     from paper_2605_23571_b200.assim import Linearization
     from paper_2605_23571_b200.covariance import CirculantFactor, DiagonalNoise
     op = _oracle_problem(16384, 24, 4, 3, 16.0, 5)
@@ -157,7 +160,8 @@ def test_stream_equals_recompute(gpu):
     b = Linearization(op.traj.states[None], 0.025, 8.0, op.net, ub, DiagonalNoise(1.0),
                       op.traj.stages[None], "stream")
     z = torch.randn(3, 16384, dtype=torch.float64, device="cuda")
-    assert torch.equal(a.hessian_cols(z), b.hessian_cols(z))
+    Ha, Hb = a.hessian_cols(z), b.hessian_cols(z)
+    assert float(((Ha - Hb).norm(dim=1) / Hb.norm(dim=1)).max()) < 1e-13
 
 
 def test_adjoint_identity_gpu(gpu):
