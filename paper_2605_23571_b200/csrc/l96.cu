@@ -549,6 +549,8 @@ static void go(K kernel, dim3 grid, cudaStream_t st, Args... args) {
 }
 
 // pick (C, NT) and tile geometry for a sweep with halos (hl, hr) per step
+static int env_int(const char* name, int dflt);
+
 static bool plan(int n, int hl_total, int hr_total, int& C, int& NT, SweepGeom& geo, int& ntiles,
                  bool sweep = true, int force_c = 0, int force_nt = 0) {
   // periodic single tile: the whole ring in one CTA (no halo redundancy)
@@ -590,6 +592,10 @@ static bool plan(int n, int hl_total, int hr_total, int& C, int& NT, SweepGeom& 
   const int W = range - hl_total - hr_total;
   if (W < 64) return false;
   ntiles = (n + W - 1) / W;
+  if (sweep) {  // A/B: more, narrower tiles per column (wave quantisation of a member group's launch)
+    const int tmin = env_int("EDAK_SWEEP_TILES", 0);
+    if (tmin > ntiles && n / tmin >= 64) ntiles = tmin;
+  }
   geo.W = ((n + ntiles - 1) / ntiles + 1) & ~1;  // balanced tiles, even width (W budget is even)
   if (geo.W > W) geo.W = W;
   geo.HL = hl_total;
