@@ -106,6 +106,23 @@ struct TmaStage {
     }
     if (arrive) asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(mbar) : "memory");
   }
+  // the same copy for a window inside [0, n) (every tile but the two across
+  // the ring end): pair m = t + k NT sits in row (t >> 3) + (NT / 8) k at the
+  // thread's own chunk, so source and destination advance by compile-time
+  // strides -- one cp.async per pair and no wrap arithmetic (the wrapped
+  // form spends ~12 instructions per pair; the sweep prologues were ~750
+  // instructions per warp, 9% of a TL tile's instructions)
+  __device__ static __forceinline__ void linear(uint32_t buf, const double* win0) {
+    static_assert(NT % 8 == 0, "whole rows per NT pairs");
+    const int t = threadIdx.x;
+    const uint32_t dst = buf + 128u * (t >> 3) + 16u * ((t & 7) ^ ((t >> 3) & 7));
+    const double* src = win0 + 2 * t;
+#pragma unroll
+    for (int k = 0; k < (R + 4) / 2 / NT + 1; ++k)
+      if ((k + 1) * NT <= (R + 4) / 2 || t + k * NT < (R + 4) / 2)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16u * NT * k), "l"(src + 2 * NT * k)
+                     : "memory");
+  }
   // thread t's window (own elements 16t .. 16t + 15 and the 2 + 2 halo):
   // row t's chunks 0..7 and row t + 1's chunks 0, 1.  Chunk c of row r sits
   // at byte 128 r + 16 (c ^ (r & 7)) = (128 r + 16 (r & 7)) ^ 16 c of the
@@ -144,9 +161,21 @@ struct TileSmem {
 // afterwards) and read back as four 16-byte loads per thread -- the 16
 // scalar loads per thread, 64 B apart, were on the prologue's critical path.
 template <int C, int NT>
-__device__ __forceinline__ void gpos_copy(XBuf<NT>& xb, const int32_t* __restrict__ gpos, int base, int n) {
+__device__ __forceinline__ void gpos_copy(XBuf<NT>& xb, const int32_t* __restrict__ gpos, int base, int n,
+                                          bool wraps) {
   static_assert(sizeof(xb.v[1]) >= C * NT * sizeof(int32_t), "the map fits one exchange buffer");
   int32_t* gs = reinterpret_cast<int32_t*>(&xb.v[1][0][0][0]);
+  if (!wraps && (base & 3) == 0 && ((uintptr_t)gpos & 15) == 0) {
+    // a range inside [0, n) on a 16-byte boundary (CTA-uniform): C / 4
+    // 16-byte copies per thread at compile-time strides
+    const unsigned d = (unsigned)__cvta_generic_to_shared(gs + 4 * (int)threadIdx.x);
+    const int32_t* s = gpos + base + 4 * (int)threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < C / 4; ++k)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d + 16u * NT * k), "l"(s + 4 * NT * k)
+                   : "memory");
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < C; ++k) {
     const int q = (int)threadIdx.x + k * NT;
@@ -226,17 +255,20 @@ __global__ void __launch_bounds__(NT, MINB)
   const int tp0 = s0 == 0 ? __ldg(P.tpos) : -1;  // level 0's time position (before the copies)
   {
     const uint32_t sbuf = sb0 + 2 * TS::BUF;
-    TS::wrapped(sbuf, vin + (size_t)col * n, gst, n, 0, false);
-    gpos_copy<C, NT>(xb, P.gpos, R.base, n);
+    if (wraps) TS::wrapped(sbuf, vin + (size_t)col * n, gst, n, 0, false);
+    else TS::linear(sbuf, vin + (size_t)col * n + gst);
+    gpos_copy<C, NT>(xb, P.gpos, R.base, n, wraps);
     cp_commit();
     cp_wait_all();
     __syncthreads();
     TS::win(sbuf, R.t, v);
     gpos_read<C, NT>(xb, gw);
+    if (R.t * C < wlo || R.t * C + C > whi) {  // only the threads across the window's ends clip
 #pragma unroll
-    for (int j = 0; j < C; ++j) {
-      const int e = R.t * C + j;
-      if (!(e >= wlo && e < whi)) gw[j] = -1;
+      for (int j = 0; j < C; ++j) {
+        const int e = R.t * C + j;
+        if (!(e >= wlo && e < whi)) gw[j] = -1;
+      }
     }
     __syncthreads();  // the map is read: the exchange buffer's pads back
     xb.init_pads();
@@ -391,8 +423,11 @@ __global__ void __launch_bounds__(NT, MINB)
   int gp[C];
   double g[C + 4];
   const uint32_t gbuf = sb0 + (NB - 1) * TS::BUF;
-  gpos_copy<C, NT>(xb, P.gpos, R.base, n);
-  if (gin) TS::wrapped(gbuf, gin + (size_t)col * n, gst, n, 0, false);
+  gpos_copy<C, NT>(xb, P.gpos, R.base, n, wraps);
+  if (gin) {
+    if (wraps) TS::wrapped(gbuf, gin + (size_t)col * n, gst, n, 0, false);
+    else TS::linear(gbuf, gin + (size_t)col * n + gst);
+  }
   cp_commit();
   cp_wait_all();
   __syncthreads();
