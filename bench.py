@@ -87,7 +87,12 @@ def config_dict(cfg, world, scaling="weak"):
 
 # ---------------------------------------------------------------- clocks --
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region.
+
+    nvidia-smi needs a few hundred ms to print its first line, which is most
+    of a default 5-step timed region, so the sampler is started before the
+    warm-up passes (the same load) and every line is stamped on arrival;
+    stop(t0, t1) keeps the samples that arrived inside the timed region."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -102,7 +107,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -111,9 +116,9 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
-    def stop(self):
+    def stop(self, t0=None, t1=None):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -123,7 +128,16 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = list(self.lines)
+        window = "timed region"
+        if t0 is not None:
+            # a line printed at t describes the ~50 ms before it
+            inside = [(t, ln) for t, ln in lines if t0 <= t <= t1 + 0.05]
+            if inside:
+                lines = inside
+            else:
+                window = "warm-up + timed region (no line arrived inside the timed region)"
+        for _, ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 7:
                 continue
@@ -136,7 +150,7 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "window": window}
 
 
 # ------------------------------------------------------------ CPU legs ----
@@ -507,22 +521,24 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(max(args.warmup, 3)):
         res = eng.run()
     barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
     n0 = _lib.launch_count()
     barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_host0 = time.perf_counter()
     s.record()
     for _ in range(args.steps):
         res = eng.run()
     e.record()
     barrier()
+    t_host1 = time.perf_counter()
     launches = (_lib.launch_count() - n0) // args.steps
     local_s = s.elapsed_time(e) * 1e-3
-    clk = clocks.stop()
+    clk = clocks.stop(t_host0, t_host1)
     t_step = max_over_ranks(local_s, torch.device("cuda", local)) / args.steps
     value = applies / t_step
 
