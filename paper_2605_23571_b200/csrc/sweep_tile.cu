@@ -142,6 +142,20 @@ struct TmaStage {
       a[C + 2 * c + 1] = v.y;
     }
   }
+  // own elements only (a[2 .. C + 1]: row t's chunks 1..7 and row t + 1's
+  // chunk 0): the stage updates x3, x4 = X + c k read no halo of X
+  __device__ static __forceinline__ void own(uint32_t buf, int t, double (&a)[C + 4]) {
+    const uint32_t A = buf + 128u * t + 16u * (t & 7), A2 = buf + 128u * (t + 1) + 16u * ((t + 1) & 7);
+#pragma unroll
+    for (int c = 1; c < 8; ++c) {
+      const double2 v = lds2(A ^ (16u * c));
+      a[2 * c] = v.x;
+      a[2 * c + 1] = v.y;
+    }
+    const double2 v = lds2(A2);
+    a[C] = v.x;
+    a[C + 1] = v.y;
+  }
 };
 
 // shared-memory carve-up of a tile kernel: exchange buffers, NB 1024-aligned
@@ -478,12 +492,10 @@ __global__ void __launch_bounds__(NT, MINB)
     // X_s stays in its buffer for the whole step: re-read where needed
     const uint32_t Xb = sb0 + bcur * TS::BUF;
     double x2[C + 4], x3[C + 4], x4[C + 4];
-    {
-      double X[C + 4];
-      TS::win(Xb, R.t, X);
+    double X[C + 4];  // own elements held through the three stage updates
+    TS::win(Xb, R.t, X);
 #pragma unroll
-      for (int j = 0; j < C; ++j) x2[j + 2] = stg_axpy(X[j + 2], h, stg_f(X[j + 3], X[j], X[j + 1], X[j + 2], F));
-    }
+    for (int j = 0; j < C; ++j) x2[j + 2] = stg_axpy(X[j + 2], h, stg_f(X[j + 3], X[j], X[j + 1], X[j + 2], F));
     R.put(&xb.v[xbi][1][0][0], x2);
     __syncthreads();  // g, x2 halos; X_{s+1}'s buffer no longer read
     R.get(&xb.v[xbi][0][0][0], g);
@@ -494,13 +506,10 @@ __global__ void __launch_bounds__(NT, MINB)
     if (s - DEPTH >= s0) stage(s - DEPTH, bnext);  // into X_{s+1}'s buffer
     bnext = bnext + 1 == NB ? 0 : bnext + 1;
     {
-      double X[C + 4];
-      TS::win(Xb, R.t, X);
 #pragma unroll
       for (int j = 0; j < C; ++j)
         x3[j + 2] = stg_axpy(X[j + 2], h, stg_f(x2[j + 3], x2[j], x2[j + 1], x2[j + 2], F));
       xchg1(x3);
-      TS::win(Xb, R.t, X);
 #pragma unroll
       for (int j = 0; j < C; ++j)
         x4[j + 2] = stg_axpy(X[j + 2], dt, stg_f(x3[j + 3], x3[j], x3[j + 1], x3[j + 2], F));
@@ -542,8 +551,7 @@ __global__ void __launch_bounds__(NT, MINB)
     xchg1(a);
     cp_wait_group<1>();  // this level's forcing (thread-private slots) has landed
     const double* fd = FS + (size_t)(s & 1) * C * NT + threadIdx.x;
-    double X[C + 4];
-    TS::win(Xb, R.t, X);
+    TS::win(Xb, R.t, X);  // with its halos again, for the first stage's adjoint
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       const double uj = l96_ad(X[j], X[j + 1], X[j + 3], X[j + 4], a[j + 1], a[j + 2], a[j + 3], a[j + 4]);
