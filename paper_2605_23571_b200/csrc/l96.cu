@@ -484,34 +484,36 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
         x4[j + 2] = stg_axpy(X[j + 2], dt, stg_f(x3[j + 3], x3[j], x3[j + 1], x3[j + 2], F));
       X1(x4);
     }
-    // step_adj (model.py:66-84) with the factor c6 = dt/6 taken out of the
-    // stage chain (every stage adjoint is linear in its input): with u4 =
-    // J4^T g, b3 = h u4 + g, u3 = J3^T b3, b2 = h u3 + g, u2 = J2^T b2, a1 =
-    // dt u2 + g, u1 = J1^T a1 the step is g + c6 (u4 + 2 u3 + 2 u2 + u1) --
-    // the reference's a_k are c6 times these with the exact factors of two
-    // folded into the accumulation -- so the sweep's g (with its exchanged
-    // halo) feeds the fourth stage directly: no scaled copy of g (C + 4
-    // products per step), and one scaling of the sum at the end, like the TL
-    double vh[C], u[C], a[C + 4];
-    ad_sub<C>(g, x4, u);  // u4
+    // step_adj (model.py:66-84): with w = (dt/6) g and c3 = 2 c6, dt = 2h,
+    //   a3 = dt u4 + c3 g = 2 b3,  b3 = h u4 + w   (u3 = 2 J3^T b3)
+    //   a2 = h u3 + c3 g  = 2 b2,  b2 = h u3' + w  (u2 = 2 J2^T b2)
+    //   a1 = h u2 + c6 g  = dt u2' + w
+    // so the powers of two fold into the vh accumulation (exact scalings) and
+    // only w, not g, stays live through the stages
+    double vh[C], u[C], a[C + 4], w[C];
+#pragma unroll
+    for (int k = 0; k < C + 4; ++k) a[k] = c6 * g[k];  // a4 = (dt/6) g, halo included
+#pragma unroll
+    for (int j = 0; j < C; ++j) w[j] = a[j + 2];
+    ad_sub<C>(a, x4, u);
 #pragma unroll
     for (int j = 0; j < C; ++j) {
-      vh[j] = u[j];
-      a[j + 2] = fma(h, u[j], g[j + 2]);  // b3
+      vh[j] = g[j + 2] + u[j];
+      a[j + 2] = fma(h, u[j], w[j]);  // b3
     }
     X1(a);
-    ad_sub<C>(a, x3, u);  // u3
+    ad_sub<C>(a, x3, u);  // u3'
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       vh[j] = fma(2.0, u[j], vh[j]);
-      a[j + 2] = fma(h, u[j], g[j + 2]);  // b2
+      a[j + 2] = fma(h, u[j], w[j]);  // b2
     }
     X1(a);
-    ad_sub<C>(a, x2, u);  // u2
+    ad_sub<C>(a, x2, u);  // u2'
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       vh[j] = fma(2.0, u[j], vh[j]);
-      a[j + 2] = fma(dt, u[j], g[j + 2]);  // a1
+      a[j + 2] = fma(dt, u[j], w[j]);  // a1
     }
     if (!STREAM) {  // X_{s-1} landed; published by this barrier
       if (DEPTH == 1) cp_wait_all();
@@ -519,9 +521,9 @@ __global__ void __launch_bounds__(NT, MINB) k_ad(edak_problem P, const double* _
       if constexpr (WT) __syncwarp();
     }
     X1(a);
-    ad_sub<C>(a, X, u);  // u1
+    ad_sub<C>(a, X, u);
 #pragma unroll
-    for (int j = 0; j < C; ++j) g[j + 2] = fma(c6, vh[j] + u[j], g[j + 2]);
+    for (int j = 0; j < C; ++j) g[j + 2] = vh[j] + u[j];
     if (PAIR) {
       add_fetched(tp_cur, DEPTH == 1 ? (s & 1) : 0, g);
       tp_cur = tp_next;

@@ -515,17 +515,20 @@ __global__ void __launch_bounds__(NT, MINB)
         x4[j + 2] = stg_axpy(X[j + 2], dt, stg_f(x3[j + 3], x3[j], x3[j + 1], x3[j + 2], F));
       xchg1(x4);
     }
-    // step_adj (model.py:66-84), as in k_ad: c6 = dt/6 out of the stage chain,
-    //   u4 = J4^T g, b3 = h u4 + g, b2 = h u3 + g, a1 = dt u2 + g,
-    //   g += c6 (u4 + 2 u3 + 2 u2 + u1)
-    double vh[C], u[C], a[C + 4];
+    // step_adj (model.py:66-84), as in k_ad: with w = (dt/6) g and c3 = 2 c6,
+    //   b3 = h u4 + w, b2 = h u3' + w, a1 = dt u2' + w, the powers of two in vh
+    double vh[C], u[C], a[C + 4], w[C];
+#pragma unroll
+    for (int k = 0; k < C + 4; ++k) a[k] = c6 * g[k];  // a4 = (dt/6) g, halo included
+#pragma unroll
+    for (int j = 0; j < C; ++j) w[j] = a[j + 2];
 #pragma unroll
     for (int j = 0; j < C; ++j)
-      u[j] = l96_ad(x4[j], x4[j + 1], x4[j + 3], x4[j + 4], g[j + 1], g[j + 2], g[j + 3], g[j + 4]);
+      u[j] = l96_ad(x4[j], x4[j + 1], x4[j + 3], x4[j + 4], a[j + 1], a[j + 2], a[j + 3], a[j + 4]);
 #pragma unroll
     for (int j = 0; j < C; ++j) {
-      vh[j] = u[j];
-      a[j + 2] = fma(h, u[j], g[j + 2]);  // b3
+      vh[j] = g[j + 2] + u[j];
+      a[j + 2] = fma(h, u[j], w[j]);  // b3
     }
     xchg1(a);
 #pragma unroll
@@ -534,7 +537,7 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       vh[j] = fma(2.0, u[j], vh[j]);
-      a[j + 2] = fma(h, u[j], g[j + 2]);  // b2
+      a[j + 2] = fma(h, u[j], w[j]);  // b2
     }
     xchg1(a);
 #pragma unroll
@@ -543,7 +546,7 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       vh[j] = fma(2.0, u[j], vh[j]);
-      a[j + 2] = fma(dt, u[j], g[j + 2]);  // a1
+      a[j + 2] = fma(dt, u[j], w[j]);  // a1
     }
     xchg1(a);
     cp_wait_group<1>();  // this level's forcing (thread-private slots) has landed
@@ -552,7 +555,7 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll
     for (int j = 0; j < C; ++j) {
       const double uj = l96_ad(X[j], X[j + 1], X[j + 3], X[j + 4], a[j + 1], a[j + 2], a[j + 3], a[j + 4]);
-      double gj = fma(c6, vh[j] + uj, g[j + 2]);
+      double gj = vh[j] + uj;
       if (tp_cur >= 0 && gp[j] >= 0) gj += fd[j * NT] * inv_s2;
       g[j + 2] = gj;
     }
